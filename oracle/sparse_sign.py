@@ -1,0 +1,98 @@
+"""Hashed sparse-sign subspace embedding S (s x n), materialised (oracle only).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+The paper sketches with an SRDCT; BASELINE.json's north star replaces it
+by a sparse-sign embedding with zeta = 8 nonzeros per column generated from a
+seeded hash, S never stored on the GPU (reading R1 in DESIGN.md).  The paper's
+requirement on S is only the epsilon-subspace-embedding property,
+and Prop. 2.1 / eqs. (reduced_sk), (resnorm_sk) hold for any S.
+
+Definition (DESIGN.md §"Sparse-sign hash"; uint32 arithmetic mod 2^32):
+
+    mix32(x)  = x ^= x>>16; x *= 0x7feb352d; x ^= x>>15; x *= 0x846ca68b; x ^= x>>16
+    seed32    = (seed ^ (seed >> 32)) & 0xffffffff
+    G(m,t,q)  = mix32( mix32( ((m*zeta + t) << 2) | q ) ^ seed32 )
+    b         = s / zeta                      (bucket height; s % zeta == 0)
+
+  Row j of the operand belongs to group m = j >> 5, lane l = j & 31.  For each
+  bucket t in [0, zeta):
+    base  = (G(m,t,0) * b) >> 32              (in [0, b))
+    a     = 2*(G(m,t,1) & 15) + 1,  c = (G(m,t,1) >> 4) & 31
+    slot  = (base + ((a*l + c) & 31)) mod b
+    S[t*b + slot, j] = (bit l of G(m,t,2) ? -1 : +1) / sqrt(zeta)
+
+Each column has exactly one nonzero in each of the zeta buckets (so ||S e_j|| = 1),
+and the 32 rows of a group land in 32 distinct slots of every bucket when b >= 32.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import scipy.sparse as sp
+
+_M32 = np.uint64(0xFFFFFFFF)
+
+
+def mix32(x: np.ndarray) -> np.ndarray:
+    """lowbias32 integer finaliser on uint32 values (computed in uint64, masked)."""
+    x = np.asarray(x, dtype=np.uint64) & _M32
+    x ^= x >> np.uint64(16)
+    x = (x * np.uint64(0x7FEB352D)) & _M32
+    x ^= x >> np.uint64(15)
+    x = (x * np.uint64(0x846CA68B)) & _M32
+    x ^= x >> np.uint64(16)
+    return x
+
+
+def seed32(seed: int) -> np.uint64:
+    seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    return np.uint64((seed ^ (seed >> 32)) & 0xFFFFFFFF)
+
+
+def group_hash(m: np.ndarray, t: int, q: int, zeta: int, seed: int) -> np.ndarray:
+    key = ((np.asarray(m, dtype=np.uint64) * np.uint64(zeta) + np.uint64(t)) << np.uint64(2)) | np.uint64(q)
+    return mix32(mix32(key & _M32) ^ seed32(seed))
+
+
+def entries(j: np.ndarray, t: int, s: int, zeta: int, seed: int):
+    """(row index in [0,s), value) of the bucket-t nonzero of columns j (vectorised)."""
+    if s % zeta:
+        raise ValueError("s must be a multiple of zeta")
+    b = s // zeta
+    j = np.asarray(j, dtype=np.uint64)
+    m = j >> np.uint64(5)
+    lane = j & np.uint64(31)
+    g0 = group_hash(m, t, 0, zeta, seed)
+    g1 = group_hash(m, t, 1, zeta, seed)
+    g2 = group_hash(m, t, 2, zeta, seed)
+    base = (g0 * np.uint64(b)) >> np.uint64(32)
+    a = np.uint64(2) * (g1 & np.uint64(15)) + np.uint64(1)
+    c = (g1 >> np.uint64(4)) & np.uint64(31)
+    slot = (base + ((a * lane + c) & np.uint64(31))) % np.uint64(b)
+    row = np.uint64(t * b) + slot
+    neg = (g2 >> lane) & np.uint64(1)
+    val = np.where(neg == 1, -1.0, 1.0) / math.sqrt(zeta)
+    return row.astype(np.int64), val
+
+
+def matrix(n: int, s: int, zeta: int, seed: int, chunk: int = 1 << 22) -> sp.csr_matrix:
+    """Materialise S as a scipy CSR matrix (s x n, n*zeta stored entries)."""
+    rows = np.empty(n * zeta, dtype=np.int64)
+    cols = np.empty(n * zeta, dtype=np.int64)
+    vals = np.empty(n * zeta, dtype=np.float64)
+    for j0 in range(0, n, chunk):
+        j = np.arange(j0, min(n, j0 + chunk), dtype=np.int64)
+        for t in range(zeta):
+            r_, v_ = entries(j, t, s, zeta, seed)
+            sl = slice(j0 * zeta + t * j.size, j0 * zeta + (t + 1) * j.size)
+            rows[sl], cols[sl], vals[sl] = r_, j, v_
+    S = sp.csr_matrix((vals, (rows, cols)), shape=(s, n))
+    S.sum_duplicates()
+    return S
+
+
+def apply(S: sp.spmatrix, X: np.ndarray) -> np.ndarray:
+    """S X for an n x r block (the plain sparse product)."""
+    return np.asarray(S @ X)

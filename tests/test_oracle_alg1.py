@@ -1,0 +1,213 @@
+"""Pins for oracle/alg1.py against what the paper and the mathematics fix.
+
+Each test would fail on a plausible mistake in the oracle (dropped term, wrong
+sign/index, transposed operand, unhatted residual coefficients, wrong T_1, ...).
+
+  exactness       dr = n, any injective S, no truncation  -> X_d = Kronecker solution
+  galerkin        S = I, k >= d  -> X_d equals an independently built Galerkin
+                  solution (orthonormal Krylov basis via numpy QR) and rho = ||R||_F
+                  
+  sketched rho    rho == ||S_U (A X + X B - C1 C2^T) S_V^T||_F for the truncated,
+                  sketched run (eq. resnorm_sk P:323-326 with hatted coefficients, R4)
+  S-Galerkin      Uhat^T S^T S R S_V^T S_V Vhat = 0
+  arnoldi         A U_d = U_{d+1} H_und_d; window orthonormality
+  prop 2.1        S U_{d+1} = Q T, Q^T Q = I, T = R of positive-diagonal QR(S U_{d+1})
+  whitened M      [T_d|T_H] H_und T_d^{-1} = Q_d^T S A U_d T_d^{-1}
+  T_1 / beta      beta_1 = tau_1 ell (R3)
+  two-pass        replay = retained-basis product
+  breakdown       C1 = C2 = eigenvector of symmetric A = B -> X = C1 C2^T / (2 lambda)
+  true residual   factored formula == dense ||A X + X B - C1 C2^T||_F
+  schedule        R9 lists
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+from oracle import alg1, operators, sparse_sign
+from synth import inputs
+
+
+def _small(N=8, r=2, k=2, d_max=20, s=None, wA=(10.0, 10.0), wB=(-5.0, 5.0), seed_c=0):
+    cfg = inputs.small_config("stencil2d", N=N, r=r, k=k, d_max=d_max, s=s, wA=wA, wB=wB, seed_c=seed_c)
+    A, Bt, B = operators.operator_pair(cfg)
+    C1, C2 = inputs.make_rhs(cfg)
+    return cfg, A, Bt, B, C1, C2
+
+
+def _kron_solution(A, B, C1, C2):
+    n = A.shape[0]
+    Ad, Bd = A.toarray(), B.toarray()
+    K = np.kron(np.eye(n), Ad) + np.kron(Bd.T, np.eye(n))      # (I (x) A + B^T (x) I) vec X
+    x = np.linalg.solve(K, (C1 @ C2.T).reshape(-1, order="F"))
+    return x.reshape(n, n, order="F")
+
+
+def _retained(obj, d):
+    U = np.concatenate([obj.U.U[i] for i in range(1, d + 1)], axis=1)
+    V = np.concatenate([obj.V.U[i] for i in range(1, d + 1)], axis=1)
+    return U, V
+
+
+def test_exactness_when_space_is_exhausted():
+    cfg, A, Bt, B, C1, C2 = _small(N=4, r=2, k=50, d_max=8)       # n = 16, dr = 16 at d = 8
+    S_U = sparse_sign.matrix(cfg.n, 80, 8, 11)
+    S_V = sparse_sign.matrix(cfg.n, 80, 8, 12)
+    o = alg1.SylvesterSketchedKrylov(A, Bt, C1, C2, S_U, S_V, k=50)
+    o.step(8)
+    res = o.residual(8)
+    X1, X2 = o.solution(8, res.Y, rank_tol=0.0)
+    X = _kron_solution(A, B, C1, C2)
+    assert np.linalg.norm(X1 @ X2.T - X) <= 1e-8 * np.linalg.norm(X)
+    assert res.rho_rel < 1e-8
+
+
+def test_galerkin_special_case_identity_sketch():
+    cfg, A, Bt, B, C1, C2 = _small(N=8, r=2, k=50, d_max=6)
+    n, d, r = cfg.n, 6, 2
+    I = sp.identity(n, format="csr")
+    o = alg1.SylvesterSketchedKrylov(A, Bt, C1, C2, I, I, k=50)
+    o.step(d)
+    res = o.residual(d)
+    X1, X2 = o.solution(d, res.Y, rank_tol=0.0)
+    # independent Galerkin: orthonormal bases of K_d(A, C1), K_d(B^T, C2) from the power basis
+    def basis(M, C):
+        blocks, Z = [], C
+        for _ in range(d):
+            blocks.append(Z)
+            Z = np.asarray(M @ Z)
+        Q, _ = np.linalg.qr(np.concatenate(blocks, axis=1))
+        return Q
+    Uo, Vo = basis(A, C1), basis(Bt, C2)
+    Yg = sla.solve_sylvester(Uo.T @ (A @ Uo), (Vo.T @ (B.T @ Vo)).T, (Uo.T @ C1) @ (C2.T @ Vo))
+    Xg = Uo @ Yg @ Vo.T
+    X = X1 @ X2.T
+    assert np.linalg.norm(X - Xg) <= 1e-8 * np.linalg.norm(Xg)
+    R = A @ X + (B.T @ X.T).T - C1 @ C2.T
+    assert res.rho == pytest.approx(np.linalg.norm(R), rel=1e-8)
+    # T = I when S = I and the basis is orthonormal
+    assert np.allclose(o.U.T[:d * r, :d * r], np.eye(d * r), atol=1e-10)
+
+
+@pytest.mark.parametrize("k,r", [(2, 2), (3, 1), (1, 3)])
+def test_sketched_residual_identity_and_galerkin_condition(k, r):
+    cfg, A, Bt, B, C1, C2 = _small(N=12, r=r, k=k, d_max=14)
+    d = 10
+    s = 8 * math.ceil(4 * (d + 1) * r / 8)
+    S_U = sparse_sign.matrix(cfg.n, s, 8, 11)
+    S_V = sparse_sign.matrix(cfg.n, s, 8, 12)
+    o = alg1.SylvesterSketchedKrylov(A, Bt, C1, C2, S_U, S_V, k=k)
+    o.U.keep_basis = o.V.keep_basis = True
+    o.step(d)
+    res = o.residual(d)
+    U, V = _retained(o, d)
+    m = d * r
+    Uh = sla.solve_triangular(o.U.T[:m, :m], U.T, trans="T", lower=False).T      # U T^{-1}
+    Vh = sla.solve_triangular(o.V.T[:m, :m], V.T, trans="T", lower=False).T
+    X = Uh @ res.Y @ Vh.T
+    R = A @ X + (B.T @ X.T).T - C1 @ C2.T
+    SRS = np.asarray(S_U @ (S_V @ R.T).T)
+    assert res.rho == pytest.approx(np.linalg.norm(SRS), rel=1e-9)
+    # the paper's literal (unhatted) coefficients do NOT give the sketched residual norm
+    hU, hV = o.U.H[(d + 1, d)], o.V.H[(d + 1, d)]
+    lit = math.sqrt(np.linalg.norm(hU @ res.Y[m - r:]) ** 2 + np.linalg.norm(res.Y[:, m - r:] @ hV.T) ** 2)
+    assert abs(lit - res.rho) > 1e-3 * res.rho
+    # S^T S - Galerkin condition
+    G = (S_U @ Uh).T @ SRS @ (S_V @ Vh)
+    assert np.linalg.norm(G) <= 1e-9 * np.linalg.norm(SRS) * np.linalg.norm(S_U @ Uh, 2) * np.linalg.norm(S_V @ Vh, 2)
+    # two-pass replay equals the retained-basis product
+    X1, X2 = o.solution(d, res.Y, rank_tol=0.0)
+    assert np.linalg.norm(X1 @ X2.T - X) <= 1e-10 * np.linalg.norm(X)
+
+
+def test_arnoldi_and_sketched_qr_relations():
+    cfg, A, Bt, B, C1, C2 = _small(N=16, r=2, k=2, d_max=20)
+    d, r = 15, 2
+    S = sparse_sign.matrix(cfg.n, 4 * 20 * r, 8, 11)
+    seq = alg1.Sequence(A, C1, S, k=2, keep_basis=True)
+    for _ in range(d):
+        seq.step()
+    U = np.concatenate([seq.U[i] for i in range(1, d + 2)], axis=1)
+    # truncated Arnoldi relation A U_d = U_{d+1} H_und_d
+    lhs = A @ U[:, :d * r]
+    assert np.linalg.norm(lhs - U @ seq.Hbar(d)) <= 1e-12 * np.linalg.norm(lhs)
+    # local orthonormality inside the window; unit-norm blocks
+    for j in range(1, d + 2):
+        assert np.allclose(seq.U[j].T @ seq.U[j], np.eye(r), atol=1e-12)
+        for i in range(max(1, j - 2 + 1), j):
+            assert np.abs(seq.U[i].T @ seq.U[j]).max() < 1e-12
+    # global orthogonality is NOT maintained (truncation): U_1 vs U_{d+1}
+    assert np.abs(seq.U[1].T @ seq.U[d + 1]).max() > 1e-6
+    # Prop. 2.1: S U_{d+1} = Q T with orthonormal Q, T = positive-diag R of the QR
+    SU = np.asarray(S @ U)
+    assert np.linalg.norm(seq.Q @ seq.T - SU) <= 1e-12 * np.linalg.norm(SU)
+    assert np.allclose(seq.Q.T @ seq.Q, np.eye(U.shape[1]), atol=1e-12)
+    _, Rref = alg1.qr_pos(SU)
+    assert np.linalg.norm(seq.T - Rref) <= 1e-9 * np.linalg.norm(Rref)
+    assert np.allclose(np.tril(seq.T, -1), 0) and np.all(np.diag(seq.T) > 0)
+    # whitened projected matrix: direct formula = Q_d^T (S A U_d) T_d^{-1}
+    M, hhat = seq.projected(d)
+    m = d * r
+    ref = seq.Q[:, :m].T @ np.asarray(S @ lhs)
+    ref = sla.solve_triangular(seq.T[:m, :m], ref.T, trans="T", lower=False).T
+    assert np.linalg.norm(M - ref) <= 1e-10 * np.linalg.norm(ref)
+    # M is block upper Hessenberg (r subdiagonals)
+    assert np.abs(np.tril(M, -r - 1)).max() <= 1e-10 * np.abs(M).max()
+    # beta_1 = tau_1 ell (R3)
+    tau1 = seq.T[:r, :r]
+    assert np.allclose(seq.beta, tau1 @ seq.ell, rtol=1e-12, atol=1e-12 * np.abs(seq.beta).max())
+
+
+def test_breakdown_on_invariant_subspace_closed_form():
+    N = 10
+    A = operators.stencil_matrix(N, (0.0, 0.0))                 # symmetric Laplacian, B = A
+    x = np.arange(1, N + 1) / (N + 1)
+    v = np.kron(np.sin(2 * np.pi * x), np.sin(np.pi * x))[:, None] * 3.0
+    lam = float((v.T @ (A @ v)).item() / (v.T @ v).item())
+    S_U = sparse_sign.matrix(N * N, 64, 8, 11)
+    S_V = sparse_sign.matrix(N * N, 64, 8, 12)
+    o = alg1.SylvesterSketchedKrylov(A, A, v, v, S_U, S_V, k=2)
+    o.step(1)
+    assert o.breakdown
+    res = o.residual(1)
+    X1, X2 = o.solution(1, res.Y, rank_tol=0.0)
+    X = v @ v.T / (2 * lam)
+    assert np.linalg.norm(X1 @ X2.T - X) <= 1e-10 * np.linalg.norm(X)
+    assert res.rho_rel < 1e-10
+
+
+def test_true_residual_matches_dense():
+    cfg, A, Bt, B, C1, C2 = _small(N=9, r=2, k=2, d_max=10)
+    rng = np.random.default_rng(3)
+    X1, X2 = rng.standard_normal((cfg.n, 5)), rng.standard_normal((cfg.n, 5))
+    X = X1 @ X2.T
+    R = A @ X + (B.T @ X.T).T - C1 @ C2.T
+    res, rel = alg1.true_residual(A, B, C1, C2, X1, X2)
+    assert res == pytest.approx(np.linalg.norm(R), rel=1e-10)
+    assert rel == pytest.approx(np.linalg.norm(R) / np.linalg.norm(C1 @ C2.T), rel=1e-10)
+
+
+def test_check_schedule():
+    s8 = alg1.check_schedule(8, 600)
+    assert s8[:50] == list(range(1, 51))
+    assert s8[50:] == [60, 70, 80, 90, 100, 120, 140, 170, 200, 230, 270, 320, 370, 430, 500, 580, 600]
+    s4 = alg1.check_schedule(4, 1500)
+    assert s4[50:66] == list(range(60, 201, 10)) + [230]
+    assert s4[-1] == 1500
+    s1 = alg1.check_schedule(1, 300)
+    assert s1[50:] == list(range(60, 301, 10))
+
+
+def test_c0_regression_expectation():
+    """Not a pin (parity unpinned for d* on the BJ configs): c0 converges near the
+    survey-time expectation d* = 107 with a true residual of the same order."""
+    cfg = inputs.get_config("c0")
+    o = alg1.SylvesterSketchedKrylov.from_config(cfg)
+    res = alg1.solve(o, cfg.tol, cfg.d_max)
+    assert res.converged and 100 <= res.d_star <= 115
+    X1, X2 = o.solution(res.d_star, res.Y)
+    A, _, B = operators.operator_pair(cfg)
+    _, rel = alg1.true_residual(A, B, o.C1, o.C2, X1, X2)
+    assert rel < 5e-6
