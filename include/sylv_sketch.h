@@ -1,0 +1,188 @@
+/*
+ * sylv_sketch.h — C ABI of the B200 (sm_100a) sketched-and-truncated block Krylov
+ * solver for the low-rank Sylvester equation
+ *
+ *        A X + X B = C1 C2^T,        X ~ X1 X2^T
+ *
+ * following Alg. 1 of Palitta, Schweitzer, Simoncini, arXiv 2311.16019
+ * ("alg:whitening_krylov").  All arithmetic is IEEE fp64.
+ *
+ * The hot path (per block step d, for both K_d(A,C1) and K_d(B^T,C2)) runs in this
+ * library's own CUDA kernels:
+ *   a1  W~ = A U_d                          (Alg. 1 line 3,   PAPER.md:889)
+ *   a2  h_{i,d} = U_i^T W~, W~ -= U_i h_{i,d}, i = max(1,d-k+1)..d
+ *                                           (lines 4-7,       PAPER.md:890-895)
+ *   a3  U_{d+1} h_{d+1,d} = W~              (line 8,          PAPER.md:896)
+ *   a4  S U_{d+1} with a hashed sparse-sign S, never stored (BASELINE.json north star)
+ *   a5  Q_{d+1} T_{d+1} = S [U_d, U_{d+1}]  (line 9,          PAPER.md:897-898; Prop. 2.1)
+ * and, on the host at scheduled d:
+ *   a6  projected Sylvester solve + sketched residual (lines 10-13, PAPER.md:899-903,
+ *       eqs. reduced_sk PAPER.md:268-270 and resnorm_sk PAPER.md:323-325, hatted
+ *       coefficients: DESIGN.md reading R4)
+ * and once, on the device:
+ *   a7  two-pass reconstruction X1 = U_d T_d^{-1} Y1 (lines 19-20).
+ *
+ * Conventions
+ *  - Blocks (C1, C2, X1, X2, apply_sketch operands) are row-major: element (i, c) of
+ *    an n x r block is at p[i*r + c] (X: p[i*ldx + c]).
+ *  - Pointer arguments documented "host or device" are classified with
+ *    cudaPointerGetAttributes; host memory may be pageable or pinned.
+ *  - Ownership: the caller owns every pointer it passes; inputs are copied during
+ *    the call, outputs are caller-allocated.  The library owns its workspace
+ *    (allocated in init, released in destroy).
+ *  - Errors: status codes only; no exceptions cross the ABI, no abort/exit.
+ *    sylv_sketch_last_error() returns the context's last message.  After
+ *    SYLV_E_BREAKDOWN / SYLV_E_SINGULAR / SYLV_E_NOT_CONVERGED the context stays valid.
+ *  - Concurrency: a context is not thread-safe; all device work is ordered on the
+ *    stream given to init.
+ *  - Supported shapes (round 1): r in {1,2,4,8}, 1 <= k <= 4, s % zeta == 0,
+ *    s >= (d_max+1) r, n*zeta < 2^32.
+ */
+#ifndef SYLV_SKETCH_H
+#define SYLV_SKETCH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sylv_ctx sylv_ctx; /* opaque */
+
+typedef enum {
+  SYLV_OK = 0,
+  SYLV_E_INVALID = 1,       /* bad argument / unsupported shape                          */
+  SYLV_E_NOMEM = 2,         /* device or host allocation failed                          */
+  SYLV_E_CUDA = 3,          /* CUDA runtime error (message in last_error)                */
+  SYLV_E_NCCL = 4,          /* reserved for the multi-rank build                         */
+  SYLV_E_BREAKDOWN = 5,     /* min diag h_{d+1,d} <= 1e-14 ||W~||_F (R11)      */
+  SYLV_E_SINGULAR = 6,      /* projected Sylvester equation (numerically) singular       */
+  SYLV_E_NOT_CONVERGED = 7, /* d_max reached without rho_rel < tol; state stays valid    */
+  SYLV_E_STATE = 8,         /* call order violated (e.g. residual(d) with d > d_done)    */
+  SYLV_E_LOST_INDEP = 9,    /* tau_{d+1} not positive definite: sketched basis deficient */
+  SYLV_E_LAPACK = 10        /* host LAPACK not loadable (see sylv_set_lapack_path)       */
+} sylv_status;
+
+typedef enum { SYLV_OP_STENCIL2D = 1, SYLV_OP_STENCIL3D = 2, SYLV_OP_CSR = 3 } sylv_op_kind;
+
+/* A coefficient matrix of the Sylvester equation (A, or B — NOT B^T; the library
+ * forms B^T itself: for stencils by negating w (exact for central differences with
+ * constant w, R16), for CSR by an explicit transpose at init).
+ *  Stencil: -nu Laplace(u) + w . grad(u) on the unit square/cube, Dirichlet BCs,
+ *           grid[0] = N interior nodes per direction, h = 1/(N+1), x fastest,
+ *           n = N^2 or N^3  (BASELINE.json configs 0-3).
+ *  CSR:     row_ptr[n+1] (int64), col_idx[nnz] (int32), val[nnz] (fp64); host or
+ *           device; copied at init. */
+typedef struct {
+  int32_t kind;          /* sylv_op_kind */
+  int64_t n;             /* global number of rows = columns                     */
+  int32_t grid[3];       /* stencil: N (only grid[0] used; cubic/square grids)  */
+  double nu;             /* stencil diffusion coefficient (BASELINE: 1.0)       */
+  double w[3];           /* stencil convection vector                           */
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const double* val;
+  int64_t nnz;
+} sylv_operator;
+
+typedef struct {
+  int32_t r;             /* block size (rank of C1, C2)                        */
+  int32_t k;             /* truncation: orthogonalise against the last k blocks */
+  int32_t d_max;         /* maxit                                              */
+  int32_t zeta;          /* sparse-sign nonzeros per column (8)                */
+  int64_t s;             /* sketch rows; s % zeta == 0, s >= (d_max+1) r       */
+  uint64_t seed_u;       /* hash seed of S_U                                   */
+  uint64_t seed_v;       /* hash seed of S_V                                   */
+  double tol;            /* stop when rho_rel < tol (strict)                   */
+  double rank_tol;       /* Y ~ Y1 Y2^T keeps sigma_i > rank_tol * sigma_1     */
+  int32_t chunk;         /* second pass: blocks per X accumulation (0 = k+1)   */
+  int32_t flags;         /* bit 0: time the n-space passes with CUDA events    */
+} sylv_config;
+
+/* Create a context and run Alg. 1 line 1: U1 ell = C1, V1 ell' = C2
+ * (CholQR on the device), beta_1 = R(S_U C1), beta_2 = R(S_V C2), T_1 = tau_1 =
+ * beta_1 ell^{-1} (R3).  C1, C2: n x r row-major, host or device.
+ * stream: a cudaStream_t (NULL = legacy default stream).  nccl_comm must be NULL
+ * in this build (single rank). */
+sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B,
+                             const double* C1, const double* C2,
+                             const sylv_config* cfg, void* nccl_comm, void* stream,
+                             sylv_ctx** out);
+
+/* Advance both sequences by up to nsteps block steps (Alg. 1 lines 3-9).  On return
+ * *d_done = number of completed steps d (the basis holds d+1 blocks).  Returns
+ * SYLV_E_BREAKDOWN (state valid, d_done = breakdown step) or SYLV_E_NOT_CONVERGED
+ * when d_max is reached before nsteps. */
+sylv_status sylv_sketch_step(sylv_ctx* ctx, int32_t nsteps, int32_t* d_done);
+
+/* Host projected solve at 1 <= d <= d_done (Alg. 1 lines 10-13): M_U Y + Y M_V^T =
+ * E1 beta1 beta2^T E1^T with M_U = [T_d | T_H] H_und_d T_d^{-1} (R6), then
+ * rho^2 = ||hhat E_d^T Y||^2 + ||Y E_d ghat^T||^2, rho_rel = rho / ||beta1 beta2^T||_F.
+ * Y is kept in the context for sylv_sketch_solution(ctx, d, ...). */
+sylv_status sylv_sketch_residual(sylv_ctx* ctx, int32_t d, double* rho, double* rho_rel);
+
+/* Second pass (Alg. 1 lines 19-20): truncated SVD of the Y of the last residual(d)
+ * call (computed here if absent), Z = T_d^{-1} Y1, and the device replay of the
+ * Arnoldi recurrence from the stored coefficients, X1 = U_d Z1, X2 = V_d Z2.
+ * X1, X2: n x max_rank row-major with leading dimension ldx >= max_rank, host or
+ * device; columns >= *rank are zeroed. */
+sylv_status sylv_sketch_solution(sylv_ctx* ctx, int32_t d, double* X1, double* X2,
+                                 int64_t ldx, int32_t max_rank, int32_t* rank);
+
+/* Driver: step + canonical check schedule + bisection (R9).  On success
+ * *d_star is the smallest bracketed d with rho_rel < tol.  Residual history is
+ * available through sylv_sketch_history. */
+sylv_status sylv_sketch_solve(sylv_ctx* ctx, int32_t* d_star, double* rho_rel);
+
+/* Test / introspection entries -------------------------------------------------- */
+
+/* Y = S X for an n x r block X (row-major, host or device); which = 0: S_U, 1: S_V.
+ * Y: s x r row-major, host or device. */
+sylv_status sylv_sketch_apply_sketch(sylv_ctx* ctx, int32_t which, const double* X,
+                                     int32_t r, double* Y);
+
+/* Small matrices of sequence `which` after d <= d_done steps, row-major:
+ * H: (d+1)r x dr (H_und_d), T: (d+1)r x (d+1)r (T_{d+1}), beta: r x r. Any may be NULL. */
+sylv_status sylv_sketch_get_small(sylv_ctx* ctx, int32_t which, int32_t d, double* H,
+                                  double* T, double* beta);
+
+/* Normalised basis block U_j (which=0) / V_j (which=1), n x r row-major, host or
+ * device; j must still be in the window (d_done+1-k <= j <= d_done+1). */
+sylv_status sylv_sketch_get_block(sylv_ctx* ctx, int32_t which, int32_t j, double* out);
+
+/* Residual history of the last sylv_sketch_solve / residual calls: up to cap
+ * entries (d, rho_rel); returns the count in *count. */
+sylv_status sylv_sketch_history(sylv_ctx* ctx, int32_t cap, int32_t* d, double* rho_rel,
+                                int32_t* count);
+
+typedef struct {
+  int64_t launches;          /* kernels launched by this context so far           */
+  int64_t steps;             /* block steps done                                  */
+  double ms_pass1, ms_pass2; /* summed CUDA-event times of the n-space passes     */
+  int64_t n_pass1, n_pass2;  /* timed launches (flags bit 0)                      */
+  double ms_skqr;            /* summed time of the sketch-space QR (flags bit 0)  */
+  int64_t n_skqr;
+  double host_solve_s;       /* wall seconds spent in host projected solves       */
+  int64_t host_solves;
+  double kappa_T_u, kappa_T_v; /* reserved                                        */
+} sylv_stats;
+
+sylv_status sylv_sketch_stats(sylv_ctx* ctx, sylv_stats* out);
+void sylv_sketch_reset_stats(sylv_ctx* ctx);
+
+const char* sylv_sketch_last_error(const sylv_ctx* ctx);
+void sylv_sketch_destroy(sylv_ctx* ctx);
+
+/* Host LAPACK (dgees/dtrsyl/dgemm/dtrsm/dgesvd with the `scipy_` symbol prefix of
+ * SciPy's bundled OpenBLAS, LP64).  Must be set before the first residual call;
+ * returns SYLV_E_LAPACK if the library or a symbol cannot be loaded. */
+sylv_status sylv_set_lapack_path(const char* path);
+
+/* Library version string. */
+const char* sylv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SYLV_SKETCH_H */

@@ -96,3 +96,20 @@ def matrix(n: int, s: int, zeta: int, seed: int, chunk: int = 1 << 22) -> sp.csr
 def apply(S: sp.spmatrix, X: np.ndarray) -> np.ndarray:
     """S X for an n x r block (the plain sparse product)."""
     return np.asarray(S @ X)
+
+
+def apply_hashed(X: np.ndarray, s: int, zeta: int, seed: int, chunk: int = 1 << 21) -> np.ndarray:
+    """S X without materialising S (same definition; for the full-size configs):
+    (S X)[row_t(j), :] += val_t(j) X[j, :] summed with np.bincount per bucket/column."""
+    X = np.asarray(X, dtype=np.float64)
+    if X.ndim == 1:
+        X = X[:, None]
+    n, r = X.shape
+    out = np.zeros((s, r))
+    for j0 in range(0, n, chunk):
+        j = np.arange(j0, min(n, j0 + chunk), dtype=np.int64)
+        for t in range(zeta):
+            rows, vals = entries(j, t, s, zeta, seed)
+            for c in range(r):
+                out[:, c] += np.bincount(rows, weights=vals * X[j, c], minlength=s)
+    return out

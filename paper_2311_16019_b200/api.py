@@ -1,0 +1,289 @@
+"""ctypes binding of include/sylv_sketch.h (argument marshalling only).
+
+Every step of the method runs inside libsylvsketch.so (CUDA kernels for sm_100a plus
+the host projected solve).  There is no CPU fallback: if the shared library is
+missing or no CUDA device is present, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import glob
+import importlib.util
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsylvsketch.so")
+
+STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NOMEM", 3: "E_CUDA", 4: "E_NCCL", 5: "E_BREAKDOWN",
+          6: "E_SINGULAR", 7: "E_NOT_CONVERGED", 8: "E_STATE", 9: "E_LOST_INDEP", 10: "E_LAPACK"}
+OK, E_BREAKDOWN, E_SINGULAR, E_NOT_CONVERGED, E_LOST_INDEP = 0, 5, 6, 7, 9
+OP_STENCIL2D, OP_STENCIL3D, OP_CSR = 1, 2, 3
+
+
+class SylvError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Operator(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int64), ("grid", C.c_int32 * 3), ("nu", C.c_double),
+                ("w", C.c_double * 3), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p),
+                ("val", C.c_void_p), ("nnz", C.c_int64)]
+
+
+class Config(C.Structure):
+    _fields_ = [("r", C.c_int32), ("k", C.c_int32), ("d_max", C.c_int32), ("zeta", C.c_int32),
+                ("s", C.c_int64), ("seed_u", C.c_uint64), ("seed_v", C.c_uint64), ("tol", C.c_double),
+                ("rank_tol", C.c_double), ("chunk", C.c_int32), ("flags", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("steps", C.c_int64), ("ms_pass1", C.c_double),
+                ("ms_pass2", C.c_double), ("n_pass1", C.c_int64), ("n_pass2", C.c_int64),
+                ("ms_skqr", C.c_double), ("n_skqr", C.c_int64), ("host_solve_s", C.c_double),
+                ("host_solves", C.c_int64), ("kappa_T_u", C.c_double), ("kappa_T_v", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+SYMBOLS = ["sylv_sketch_init", "sylv_sketch_step", "sylv_sketch_residual", "sylv_sketch_solution",
+           "sylv_sketch_solve", "sylv_sketch_apply_sketch", "sylv_sketch_get_small",
+           "sylv_sketch_get_block", "sylv_sketch_history", "sylv_sketch_stats",
+           "sylv_sketch_reset_stats", "sylv_sketch_last_error", "sylv_sketch_destroy",
+           "sylv_set_lapack_path", "sylv_version"]
+
+
+def lapack_path() -> str:
+    spec = importlib.util.find_spec("scipy")
+    if spec is None or not spec.submodule_search_locations:
+        raise SylvError(10, "scipy (bundled OpenBLAS/LAPACK) not found")
+    site = os.path.dirname(list(spec.submodule_search_locations)[0])
+    hits = sorted(glob.glob(os.path.join(site, "scipy.libs", "libscipy_openblas*.so")))
+    if not hits:
+        raise SylvError(10, "libscipy_openblas*.so not found next to scipy")
+    return hits[0]
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libsylvsketch.so (no fallback: raises if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise SylvError(3, f"{path} missing: run `python -m paper_2311_16019_b200.build` "
+                           "(or __graft_entry__.build())")
+    lib = C.CDLL(path)
+    P = C.c_void_p
+    lib.sylv_sketch_init.argtypes = [C.POINTER(Operator), C.POINTER(Operator), P, P, C.POINTER(Config), P, P,
+                                     C.POINTER(P)]
+    lib.sylv_sketch_step.argtypes = [P, C.c_int32, C.POINTER(C.c_int32)]
+    lib.sylv_sketch_residual.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    lib.sylv_sketch_solution.argtypes = [P, C.c_int32, P, P, C.c_int64, C.c_int32, C.POINTER(C.c_int32)]
+    lib.sylv_sketch_solve.argtypes = [P, C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+    lib.sylv_sketch_apply_sketch.argtypes = [P, C.c_int32, P, C.c_int32, P]
+    lib.sylv_sketch_get_small.argtypes = [P, C.c_int32, C.c_int32, P, P, P]
+    lib.sylv_sketch_get_block.argtypes = [P, C.c_int32, C.c_int32, P]
+    lib.sylv_sketch_history.argtypes = [P, C.c_int32, P, P, C.POINTER(C.c_int32)]
+    lib.sylv_sketch_stats.argtypes = [P, C.POINTER(Stats)]
+    lib.sylv_sketch_reset_stats.argtypes = [P]
+    lib.sylv_sketch_reset_stats.restype = None
+    lib.sylv_sketch_last_error.argtypes = [P]
+    lib.sylv_sketch_last_error.restype = C.c_char_p
+    lib.sylv_sketch_destroy.argtypes = [P]
+    lib.sylv_sketch_destroy.restype = None
+    lib.sylv_set_lapack_path.argtypes = [C.c_char_p]
+    lib.sylv_version.restype = C.c_char_p
+    for name in SYMBOLS[:11]:
+        if name not in ("sylv_sketch_reset_stats",):
+            getattr(lib, name).restype = C.c_int
+    lib.sylv_set_lapack_path.restype = C.c_int
+    st = lib.sylv_set_lapack_path(lapack_path().encode())
+    if st != 0:
+        raise SylvError(st, "could not load host LAPACK")
+    _lib = lib
+    return lib
+
+
+def _ptr(x) -> Tuple[int, object]:
+    """(address, keep-alive) for a float64/int C-contiguous torch tensor or numpy array."""
+    if x is None:
+        return 0, None
+    if hasattr(x, "data_ptr"):           # torch.Tensor
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr(), x
+    a = np.ascontiguousarray(x)
+    return a.ctypes.data, a
+
+
+def stencil_operator(kind: str, N: int, w, nu: float = 1.0) -> Operator:
+    op = Operator()
+    op.kind = OP_STENCIL2D if kind == "stencil2d" else OP_STENCIL3D
+    dim = 2 if kind == "stencil2d" else 3
+    op.n = N ** dim
+    op.grid[0] = N
+    op.nu = nu
+    for i, v in enumerate(w):
+        op.w[i] = float(v)
+    return op
+
+
+def csr_operator(n: int, row_ptr, col_idx, val):
+    op = Operator()
+    op.kind = OP_CSR
+    op.n = n
+    keep = []
+    for name, arr, dt in (("row_ptr", row_ptr, np.int64), ("col_idx", col_idx, np.int32), ("val", val, np.float64)):
+        if not hasattr(arr, "data_ptr"):
+            arr = np.ascontiguousarray(arr, dtype=dt)
+        p, k = _ptr(arr)
+        setattr(op, name, p)
+        keep.append(k)
+    op.nnz = int(len(val) if not hasattr(val, "numel") else val.numel())
+    return op, keep
+
+
+class SylvSketch:
+    """One solver context (both Krylov sequences).  Mirrors the C ABI one to one."""
+
+    def __init__(self, A: Operator, B: Operator, C1, C2, *, r: int, k: int, d_max: int, s: int,
+                 zeta: int = 8, seed_u: int = 11, seed_v: int = 12, tol: float = 1e-6,
+                 rank_tol: float = 1e-12, chunk: int = 0, timing: bool = False, stream=None,
+                 keep=None):
+        self.lib = load_library()
+        self.cfg = Config(r=r, k=k, d_max=d_max, zeta=zeta, s=s, seed_u=seed_u, seed_v=seed_v, tol=tol,
+                          rank_tol=rank_tol, chunk=chunk, flags=1 if timing else 0)
+        self.n, self.r, self.s = int(A.n), r, s
+        self._keep = [A, B, keep]
+        p1, k1 = _ptr(C1)
+        p2, k2 = _ptr(C2)
+        self._ctx = C.c_void_p()
+        st = C.c_void_p(stream) if stream is not None else None
+        status = self.lib.sylv_sketch_init(C.byref(A), C.byref(B), p1, p2, C.byref(self.cfg), None, st,
+                                           C.byref(self._ctx))
+        if status != OK:
+            msg = self._err()
+            self.close()
+            raise SylvError(status, msg)
+
+    # -- helpers
+    def _err(self) -> str:
+        return self.lib.sylv_sketch_last_error(self._ctx).decode() if self._ctx else "init failed"
+
+    def _check(self, status: int, allow=()):
+        if status != OK and status not in allow:
+            raise SylvError(status, self._err())
+        return status
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self.lib.sylv_sketch_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- ABI
+    def step(self, nsteps: int = 1) -> Tuple[int, int]:
+        d = C.c_int32()
+        st = self._check(self.lib.sylv_sketch_step(self._ctx, nsteps, C.byref(d)),
+                         allow=(E_BREAKDOWN, E_NOT_CONVERGED, E_LOST_INDEP))
+        return d.value, st
+
+    def residual(self, d: int) -> Tuple[float, float]:
+        rho, rr = C.c_double(), C.c_double()
+        self._check(self.lib.sylv_sketch_residual(self._ctx, d, C.byref(rho), C.byref(rr)))
+        return rho.value, rr.value
+
+    def solve(self) -> Tuple[int, float, int]:
+        ds, rr = C.c_int32(), C.c_double()
+        st = self._check(self.lib.sylv_sketch_solve(self._ctx, C.byref(ds), C.byref(rr)), allow=(E_NOT_CONVERGED,))
+        return ds.value, rr.value, st
+
+    def solution(self, d: int, max_rank: int, X1=None, X2=None) -> Tuple[object, object, int]:
+        if X1 is None:
+            X1 = np.zeros((self.n, max_rank))
+            X2 = np.zeros((self.n, max_rank))
+        p1, _ = _ptr(X1)
+        p2, _ = _ptr(X2)
+        rank = C.c_int32()
+        self._check(self.lib.sylv_sketch_solution(self._ctx, d, p1, p2, max_rank, max_rank, C.byref(rank)))
+        return X1, X2, rank.value
+
+    def apply_sketch(self, which: int, X, out=None):
+        r = int(X.shape[1])
+        if out is None:
+            out = np.zeros((self.s, r))
+        px, _ = _ptr(X)
+        po, _ = _ptr(out)
+        self._check(self.lib.sylv_sketch_apply_sketch(self._ctx, which, px, r, po))
+        return out
+
+    def get_small(self, which: int, d: int):
+        r, m = self.r, d * self.r
+        H = np.zeros((m + r, m))
+        T = np.zeros((m + r, m + r))
+        beta = np.zeros((r, r))
+        self._check(self.lib.sylv_sketch_get_small(self._ctx, which, d, H.ctypes.data, T.ctypes.data,
+                                                   beta.ctypes.data))
+        return H, T, beta
+
+    def get_block(self, which: int, j: int, out=None):
+        if out is None:
+            out = np.zeros((self.n, self.r))
+        p, _ = _ptr(out)
+        self._check(self.lib.sylv_sketch_get_block(self._ctx, which, j, p))
+        return out
+
+    def history(self):
+        cnt = C.c_int32()
+        self.lib.sylv_sketch_history(self._ctx, 0, None, None, C.byref(cnt))
+        n = cnt.value
+        d = np.zeros(n, dtype=np.int32)
+        rr = np.zeros(n)
+        self.lib.sylv_sketch_history(self._ctx, n, d.ctypes.data, rr.ctypes.data, C.byref(cnt))
+        return list(zip(d.tolist(), rr.tolist()))
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(self.lib.sylv_sketch_stats(self._ctx, C.byref(s)))
+        return s.as_dict()
+
+    def reset_stats(self):
+        self.lib.sylv_sketch_reset_stats(self._ctx)
+
+
+def operators_for(cfg, csr_pair=None):
+    """(A, B, keepalive) C-ABI operator descriptors for a synth.Config (B, not B^T)."""
+    if cfg.kind.startswith("stencil"):
+        return stencil_operator(cfg.kind, cfg.N, cfg.wA), stencil_operator(cfg.kind, cfg.N, cfg.wB), None
+    if csr_pair is None:
+        from synth.inputs import config_csr
+        csr_pair = config_csr(cfg)
+    (ra, ca, va), (rb, cb, vb) = csr_pair
+    A, ka = csr_operator(cfg.n, ra, ca, va)
+    B, kb = csr_operator(cfg.n, rb, cb, vb)
+    return A, B, (ka, kb)
+
+
+def from_config(cfg, C1=None, C2=None, csr_pair=None, timing=False, stream=None, **kw) -> SylvSketch:
+    if C1 is None:
+        from synth.inputs import make_rhs
+        C1, C2 = make_rhs(cfg)
+    A, B, keep = operators_for(cfg, csr_pair)
+    return SylvSketch(A, B, C1, C2, r=cfg.r, k=cfg.k, d_max=cfg.d_max, s=cfg.s, zeta=cfg.zeta,
+                      seed_u=cfg.seed_u, seed_v=cfg.seed_v, tol=cfg.tol, timing=timing, stream=stream,
+                      keep=keep, **kw)
+
+
+def version() -> str:
+    return load_library().sylv_version().decode()

@@ -1,0 +1,897 @@
+// engine.cu — context, step schedule and the extern "C" boundary of include/sylv_sketch.h.
+//
+// One sylv_ctx owns two Sequence objects (U: operator A, seed_u; V: operator B^T,
+// seed_v).  A block step runs the n-space passes (nspace.cuh) and the sketch-space QR
+// update (sspace.cuh) for U then V on the context stream; small coefficient mirrors
+// are copied to pinned host memory for the host projected solve (host_solve.cpp).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sylv_sketch.h"
+#include "common.cuh"
+#include "host_solve.hpp"
+#include "nspace.cuh"
+#include "sspace.cuh"
+
+using namespace sylv;
+
+#define SYLV_VERSION "sylv_sketch 0.1 (sm_100a)"
+
+namespace {
+
+struct CudaError {
+  cudaError_t e;
+  const char* what;
+};
+
+#define CK(call)                                         \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) throw CudaError{_e, #call};   \
+  } while (0)
+
+struct Status {
+  sylv_status s;
+  std::string msg;
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+T* dalloc(size_t count) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+// ----------------------------------------------------------------------------------
+// Launch dispatch over the template parameters R in {1,2,4,8}, K in {1,2,3,4}
+// ----------------------------------------------------------------------------------
+#define SYLV_DISPATCH_R(Rv, ...)                          \
+  switch (Rv) {                                           \
+    case 1: { constexpr int R_ = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int R_ = 2; __VA_ARGS__; } break; \
+    case 4: { constexpr int R_ = 4; __VA_ARGS__; } break; \
+    case 8: { constexpr int R_ = 8; __VA_ARGS__; } break; \
+    default: break;                                       \
+  }
+#define SYLV_DISPATCH_RK(Rv, Kv, ...)                                   \
+  SYLV_DISPATCH_R(Rv, switch (Kv) {                                     \
+    case 1: { constexpr int K_ = 1; __VA_ARGS__; } break;               \
+    case 2: { constexpr int K_ = 2; __VA_ARGS__; } break;               \
+    case 3: { constexpr int K_ = 3; __VA_ARGS__; } break;               \
+    case 4: { constexpr int K_ = 4; __VA_ARGS__; } break;               \
+    default: break;                                                     \
+  })
+
+struct TimedPair {
+  cudaEvent_t a, b;
+  int kind;  // 0 pass1, 1 pass2, 2 skqr
+};
+
+}  // namespace
+
+struct Sequence {
+  int which = 0;
+  int R = 1, K = 1, dmax = 0;
+  int64_t n = 0, s = 0, ldT = 0;
+  OpParams op{};
+  SketchParams sp{};
+  // device
+  double* ring = nullptr;     // (K+1) n x R
+  double* Cdev = nullptr;     // n x R
+  double* Yt = nullptr;       // CSR: A Z_d (n x R)
+  double* sk = nullptr;       // s x R
+  double* w = nullptr;        // s x R
+  double* w2 = nullptr;       // s x R
+  double* Q = nullptr;        // s x ldT (col-major)
+  double* Tdev = nullptr;     // ldT x ldT col-major
+  double* Rall = nullptr;     // (dmax+2) R^2
+  double* Kc = nullptr;       // (dmax+1) (1+K) R^2
+  double* Hc = nullptr;       // (dmax+1) (K+1) R^2
+  double* hn2 = nullptr;      // (dmax+1)
+  int* flags = nullptr;       // (dmax+2)
+  double* part1 = nullptr;    // G x K R^2
+  double* part2 = nullptr;    // G x R^2
+  double* cpart = nullptr;    // RT x ldT x R
+  double* csum = nullptr;     // ldT x R
+  double* c2 = nullptr;       // ldT x R
+  double* qcpart = nullptr;   // CC x s x R
+  double* small = nullptr;    // scratch r x r matrices
+  int64_t* rp = nullptr;      // owned CSR (device)
+  int32_t* ci = nullptr;
+  double* cv = nullptr;
+  // host mirrors (pinned)
+  double* Hh = nullptr;       // (dmax+1) (K+1) R^2
+  double* Th = nullptr;       // ldT x ldT col-major
+  double* Rh = nullptr;       // (dmax+2) R^2 (filled on demand)
+  int* flags_h = nullptr;
+  double beta[kMaxR * kMaxR];
+  double ell[kMaxR * kMaxR];
+
+  double* slot(int j) const { return ring + (int64_t)(j % (K + 1)) * n * R; }
+};
+
+struct sylv_ctx {
+  std::string err;
+  cudaStream_t st = nullptr;
+  int R = 1, K = 1, dmax = 0, zeta = 8, chunk = 0, cflags = 0;
+  int64_t n = 0, s = 0;
+  double tol = 1e-6, rank_tol = 1e-12;
+  int sm = 148;
+  int G = 0;          // grid of the n-space passes
+  int RT = 1;         // row tiles of Q^T w
+  int64_t tileQ = 0;
+  int CC = 1;         // column chunks of Q c
+  Sequence seq[2];
+  int d_done = 0;
+  bool broken = false;
+  int breakdown_d = -1;
+  // last projected solution
+  int y_d = -1;
+  std::vector<double> Y;
+  std::vector<std::pair<int, double>> hist;
+  sylv_stats stats{};
+  std::vector<TimedPair> timed;
+  std::vector<TimedPair> free_events;
+};
+
+namespace {
+
+void count(sylv_ctx* c, int k = 1) { c->stats.launches += k; }
+
+TimedPair ev_get(sylv_ctx* c, int kind) {
+  TimedPair p;
+  if (!c->free_events.empty()) {
+    p = c->free_events.back();
+    c->free_events.pop_back();
+  } else {
+    CK(cudaEventCreate(&p.a));
+    CK(cudaEventCreate(&p.b));
+  }
+  p.kind = kind;
+  return p;
+}
+
+void ev_collect(sylv_ctx* c) {
+  for (auto& p : c->timed) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.a, p.b));
+    if (p.kind == 0) { c->stats.ms_pass1 += ms; c->stats.n_pass1++; }
+    else if (p.kind == 1) { c->stats.ms_pass2 += ms; c->stats.n_pass2++; }
+    else { c->stats.ms_skqr += ms; c->stats.n_skqr++; }
+    c->free_events.push_back(p);
+  }
+  c->timed.clear();
+}
+
+OpParams make_op(const sylv_operator* A, bool transpose) {
+  OpParams op{};
+  op.kind = A->kind;
+  op.n = A->n;
+  if (A->kind == SYLV_OP_STENCIL2D || A->kind == SYLV_OP_STENCIL3D) {
+    const int dim = (A->kind == SYLV_OP_STENCIL2D) ? 2 : 3;
+    const int N = A->grid[0];
+    op.N = N;
+    const double h = 1.0 / (N + 1);
+    const double nu = A->nu;
+    const double sg = transpose ? -1.0 : 1.0;  // B^T = stencil with -w (R16)
+    op.cd = 2.0 * dim * nu / (h * h);
+    op.cxm = -nu / (h * h) - sg * A->w[0] / (2 * h);
+    op.cxp = -nu / (h * h) + sg * A->w[0] / (2 * h);
+    op.cym = -nu / (h * h) - sg * A->w[1] / (2 * h);
+    op.cyp = -nu / (h * h) + sg * A->w[1] / (2 * h);
+    if (dim == 3) {
+      op.czm = -nu / (h * h) - sg * A->w[2] / (2 * h);
+      op.czp = -nu / (h * h) + sg * A->w[2] / (2 * h);
+    }
+  }
+  return op;
+}
+
+// Host CSR (possibly transposed) upload.
+void upload_csr(Sequence& q, const sylv_operator* A, bool transpose, cudaStream_t st) {
+  const int64_t n = A->n, nnz = A->nnz;
+  std::vector<int64_t> rp(n + 1);
+  std::vector<int32_t> ci(nnz);
+  std::vector<double> cv(nnz);
+  const bool dev = is_device_ptr(A->row_ptr);
+  if (dev) {
+    CK(cudaMemcpy(rp.data(), A->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ci.data(), A->col_idx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cv.data(), A->val, nnz * sizeof(double), cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(rp.data(), A->row_ptr, (n + 1) * sizeof(int64_t));
+    std::memcpy(ci.data(), A->col_idx, nnz * sizeof(int32_t));
+    std::memcpy(cv.data(), A->val, nnz * sizeof(double));
+  }
+  if (transpose) {  // counting-sort transpose: B^T in CSR = B in CSC (rows sorted by construction)
+    std::vector<int64_t> tp(n + 1, 0);
+    for (int64_t p = 0; p < nnz; ++p) tp[ci[p] + 1]++;
+    for (int64_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
+    std::vector<int64_t> pos(tp.begin(), tp.end() - 1);
+    std::vector<int32_t> tci(nnz);
+    std::vector<double> tcv(nnz);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int64_t dst = pos[ci[p]]++;
+        tci[dst] = (int32_t)i;
+        tcv[dst] = cv[p];
+      }
+    rp.swap(tp);
+    ci.swap(tci);
+    cv.swap(tcv);
+  }
+  q.rp = dalloc<int64_t>(n + 1);
+  q.ci = dalloc<int32_t>(nnz);
+  q.cv = dalloc<double>(nnz);
+  CK(cudaMemcpyAsync(q.rp, rp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(q.ci, ci.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(q.cv, cv.data(), nnz * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  q.op.rp = q.rp;
+  q.op.ci = q.ci;
+  q.op.cv = q.cv;
+}
+
+void free_seq(Sequence& q) {
+  double* dp[] = {q.ring, q.Cdev, q.Yt, q.sk, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
+                  q.part1, q.part2, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv};
+  for (double* p : dp)
+    if (p) cudaFree(p);
+  if (q.flags) cudaFree(q.flags);
+  if (q.rp) cudaFree(q.rp);
+  if (q.ci) cudaFree(q.ci);
+  if (q.Hh) cudaFreeHost(q.Hh);
+  if (q.Th) cudaFreeHost(q.Th);
+  if (q.Rh) cudaFreeHost(q.Rh);
+  if (q.flags_h) cudaFreeHost(q.flags_h);
+  q = Sequence{};
+}
+
+// CholQR2 of the s x R block `in` (destroyed): q written to Q[:, col0:col0+R]
+// (column-major), R-factor tau (positive diagonal) to `tau_out` (device, R x R).
+void cholqr2(sylv_ctx* c, Sequence& q, double* in, int64_t col0, double* tau_out, int flag_slot) {
+  const int R = c->R;
+  const int gs = (int)std::min<int64_t>(c->G, (q.s + 255) / 256);
+  double* ta = q.small;            // R^2
+  double* tai = q.small + 64;      // R^2
+  double* tbi = q.small + 128;     // R^2
+  SYLV_DISPATCH_R(R, {
+    k_sketch_gram<R_><<<gs, kThreads, 0, c->st>>>(q.s, in, q.sp, nullptr, q.part2);
+    k_chol_small<R_><<<1, 64, 0, c->st>>>(q.part2, gs, ta, tai, nullptr, q.flags, flag_slot);
+    k_rmul<R_><<<gs, kThreads, 0, c->st>>>(q.s, in, tai, q.w2, 0);
+    k_sketch_gram<R_><<<gs, kThreads, 0, c->st>>>(q.s, q.w2, q.sp, nullptr, q.part2);
+    k_chol_small<R_><<<1, 64, 0, c->st>>>(q.part2, gs, tau_out, tbi, ta, q.flags, flag_slot);
+    k_rmul<R_><<<gs, kThreads, 0, c->st>>>(q.s, q.w2, tbi, q.Q + col0 * q.s, q.s);
+  });
+  count(c, 6);
+  CK(cudaGetLastError());
+}
+
+void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, bool transpose,
+                   const double* C, uint64_t seed) {
+  q.which = which;
+  q.R = c->R;
+  q.K = c->K;
+  q.dmax = c->dmax;
+  q.n = c->n;
+  q.s = c->s;
+  q.ldT = (int64_t)(c->dmax + 1) * c->R;
+  q.op = make_op(A, transpose);
+  q.sp.seed = (uint32_t)(seed ^ (seed >> 32));
+  q.sp.zeta = (uint32_t)c->zeta;
+  q.sp.b = (uint32_t)(c->s / c->zeta);
+  q.sp.scale = 1.0 / std::sqrt((double)c->zeta);
+  const int R = c->R, K = c->K;
+  const int64_t nR = c->n * R, sR = c->s * R, ldT = q.ldT;
+  if (A->kind == SYLV_OP_CSR) upload_csr(q, A, transpose, c->st);
+
+  q.ring = dalloc<double>((size_t)(K + 1) * nR);
+  q.Cdev = dalloc<double>(nR);
+  if (A->kind == SYLV_OP_CSR) q.Yt = dalloc<double>(nR);
+  q.sk = dalloc<double>(sR);
+  q.w = dalloc<double>(sR);
+  q.w2 = dalloc<double>(sR);
+  q.Q = dalloc<double>((size_t)c->s * ldT);
+  q.Tdev = dalloc<double>((size_t)ldT * ldT);
+  q.Rall = dalloc<double>((size_t)(c->dmax + 2) * R * R);
+  q.Kc = dalloc<double>((size_t)(c->dmax + 1) * (1 + K) * R * R);
+  q.Hc = dalloc<double>((size_t)(c->dmax + 1) * (K + 1) * R * R);
+  q.hn2 = dalloc<double>(c->dmax + 1);
+  q.flags = dalloc<int>(c->dmax + 2);
+  q.part1 = dalloc<double>((size_t)c->G * K * R * R);
+  q.part2 = dalloc<double>((size_t)c->G * R * R);
+  q.cpart = dalloc<double>((size_t)c->RT * ldT * R);
+  q.csum = dalloc<double>(ldT * R);
+  q.c2 = dalloc<double>(ldT * R);
+  q.qcpart = dalloc<double>((size_t)c->CC * sR);
+  q.small = dalloc<double>(512);
+  CK(cudaMemsetAsync(q.Tdev, 0, (size_t)ldT * ldT * sizeof(double), c->st));
+  CK(cudaMemsetAsync(q.flags, 0, (c->dmax + 2) * sizeof(int), c->st));
+  CK(cudaMemsetAsync(q.Hc, 0, (size_t)(c->dmax + 1) * (K + 1) * R * R * sizeof(double), c->st));
+  CK(cudaMallocHost(&q.Hh, (size_t)(c->dmax + 1) * (K + 1) * R * R * sizeof(double)));
+  CK(cudaMallocHost(&q.Th, (size_t)ldT * ldT * sizeof(double)));
+  CK(cudaMallocHost(&q.Rh, (size_t)(c->dmax + 2) * R * R * sizeof(double)));
+  CK(cudaMallocHost(&q.flags_h, (c->dmax + 2) * sizeof(int)));
+  std::memset(q.Th, 0, (size_t)ldT * ldT * sizeof(double));
+  std::memset(q.Hh, 0, (size_t)(c->dmax + 1) * (K + 1) * R * R * sizeof(double));
+
+  // C -> Cdev and Z_1 (ring slot 1)
+  CK(cudaMemcpyAsync(q.Cdev, C, nR * sizeof(double), cudaMemcpyDefault, c->st));
+  CK(cudaMemcpyAsync(q.slot(1), q.Cdev, nR * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  // Alg. 1 line 1: ell = chol(C^T C) (U_1 ell = C), S C -> CholQR2 -> beta, Q_1
+  CK(cudaMemsetAsync(q.sk, 0, sR * sizeof(double), c->st));
+  double* ell_d = q.small + 192;
+  double* elli_d = q.small + 256;
+  double* beta_d = q.small + 320;
+  SYLV_DISPATCH_R(R, {
+    k_sketch_gram<R_><<<c->G, kThreads, 0, c->st>>>(c->n, q.Cdev, q.sp, q.sk, q.part2);
+    k_chol_small<R_><<<1, 64, 0, c->st>>>(q.part2, c->G, ell_d, elli_d, nullptr, q.flags, 0);
+  });
+  count(c, 2);
+  CK(cudaGetLastError());
+  cholqr2(c, q, q.sk, 0, beta_d, 0);
+  SYLV_DISPATCH_R(R, { k_init_tau<R_><<<1, 1, 0, c->st>>>(beta_d, ell_d, q.Tdev, ldT, q.Rall + R * R); });
+  count(c);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(q.beta, beta_d, R * R * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(q.ell, ell_d, R * R * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpy2DAsync(q.Th, ldT * sizeof(double), q.Tdev, ldT * sizeof(double), R * sizeof(double),
+                       R, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(q.flags_h, q.flags, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (q.flags_h[0]) throw Status{SYLV_E_INVALID, "C1 or C2 (or its sketch) is rank deficient"};
+}
+
+// One block step j (1-based) of one sequence: Alg. 1 lines 3-9.
+void step_sequence(sylv_ctx* c, Sequence& q, int j) {
+  const int R = c->R, K = c->K;
+  const int nwin = std::min(K, j);
+  Win win{};
+  for (int i = 0; i < nwin; ++i) win.p[i] = q.slot(j - nwin + 1 + i);
+  const bool timing = (c->cflags & 1) != 0;
+  cudaStream_t st = c->st;
+  const int G = c->G;
+  TimedPair t1{}, t2{}, t3{};
+  // ---- a1 + a2 coefficients: pass 1
+  if (timing) { t1 = ev_get(c, 0); CK(cudaEventRecord(t1.a, st)); }
+  SYLV_DISPATCH_RK(R, K, {
+    k_pass1<R_, K_><<<G, kThreads, 0, st>>>(q.op, win, nwin, q.Yt, q.part1);
+  });
+  if (timing) { CK(cudaEventRecord(t1.b, st)); c->timed.push_back(t1); }
+  SYLV_DISPATCH_RK(R, K, {
+    k_coef1<R_, K_><<<1, kThreads, 0, st>>>(q.part1, G, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
+  });
+  CK(cudaMemsetAsync(q.sk, 0, q.s * R * sizeof(double), st));
+  // ---- a2 update + a3 Gram + a4 sketch: pass 2
+  if (timing) { t2 = ev_get(c, 1); CK(cudaEventRecord(t2.a, st)); }
+  SYLV_DISPATCH_RK(R, K, {
+    k_pass2<R_, K_, true><<<G, kThreads, 0, st>>>(q.op, win, nwin, q.Yt,
+                                                   q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1),
+                                                   q.part2, q.sp, q.sk);
+  });
+  if (timing) { CK(cudaEventRecord(t2.b, st)); c->timed.push_back(t2); }
+  SYLV_DISPATCH_RK(R, K, {
+    k_coef2<R_, K_><<<1, kThreads, 0, st>>>(q.part2, G, j, q.Rall, q.Hc, q.hn2, q.flags);
+  });
+  count(c, 4);
+  CK(cudaGetLastError());
+  // ---- a5: w = (S W') R_{j+1}; block CGS2 against Q (m = j R columns); CholQR2; T column
+  if (timing) { t3 = ev_get(c, 2); CK(cudaEventRecord(t3.a, st)); }
+  const int m = j * R;
+  const int gs = (int)std::min<int64_t>(G, (q.s + 255) / 256);
+  const dim3 gq((m + kWarps - 1) / kWarps, c->RT);
+  const int cols_per_chunk = (m + c->CC - 1) / c->CC;
+  const int ncc = (m + cols_per_chunk - 1) / cols_per_chunk;
+  const dim3 gc((unsigned)((q.s + kThreads - 1) / kThreads), ncc);
+  const int64_t mR = (int64_t)m * R;
+  const int gr = (int)std::min<int64_t>(1024, (mR + 255) / 256);
+  const int gw = (int)std::min<int64_t>(1024, (q.s * R + 255) / 256);
+  SYLV_DISPATCH_R(R, {
+    k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, q.sk, q.Rall + (int64_t)(j + 1) * R * R, q.w, 0);
+    // pass A: c1 = Q^T w
+    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, q.s, m, q.w, c->tileQ, q.cpart);
+    k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.csum, nullptr);
+    // w -= Q c1
+    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, q.s, m, q.csum, cols_per_chunk, q.qcpart);
+    k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, q.s * R);
+    // pass B: c2 = Q^T w, csum += c2
+    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, q.s, m, q.w, c->tileQ, q.cpart);
+    k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.c2, q.csum);
+    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, q.s, m, q.c2, cols_per_chunk, q.qcpart);
+    k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, q.s * R);
+  });
+  count(c, 9);
+  CK(cudaGetLastError());
+  double* tau_d = q.small + 384;
+  cholqr2(c, q, q.w, m, tau_d, j + 1);
+  SYLV_DISPATCH_R(R, {
+    k_tcol<R_><<<std::max(1, (int)std::min<int64_t>(256, ((int64_t)(m + R) * R + 255) / 256)), 256, 0, st>>>(
+        q.csum, tau_d, q.Tdev, q.ldT, m);
+  });
+  count(c);
+  CK(cudaGetLastError());
+  if (timing) { CK(cudaEventRecord(t3.b, st)); c->timed.push_back(t3); }
+  // ---- mirrors: H column j, T columns m..m+R (rows 0..m+R)
+  const size_t hb = (size_t)(K + 1) * R * R;
+  CK(cudaMemcpyAsync(q.Hh + (size_t)j * hb, q.Hc + (size_t)j * hb, hb * sizeof(double),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpy2DAsync(q.Th + (int64_t)m * q.ldT, q.ldT * sizeof(double), q.Tdev + (int64_t)m * q.ldT,
+                       q.ldT * sizeof(double), (size_t)(m + R) * sizeof(double), R,
+                       cudaMemcpyDeviceToHost, st));
+}
+
+sylv_status fail(sylv_ctx* c, sylv_status s, const std::string& m) {
+  if (c) c->err = m;
+  return s;
+}
+
+template <typename F>
+sylv_status guard(sylv_ctx* c, F&& f) {
+  try {
+    return f();
+  } catch (const CudaError& e) {
+    return fail(c, SYLV_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
+  } catch (const Status& s) {
+    return fail(c, s.s, s.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(c, SYLV_E_NOMEM, "host allocation failed");
+  }
+}
+
+}  // namespace
+
+// ====================================================================================
+// extern "C" boundary
+// ====================================================================================
+extern "C" {
+
+const char* sylv_version(void) { return SYLV_VERSION; }
+
+sylv_status sylv_set_lapack_path(const char* path) {
+  std::string err;
+  if (!path || !lapack_load(path, err)) {
+    std::fprintf(stderr, "sylv_set_lapack_path: %s\n", err.c_str());
+    return SYLV_E_LAPACK;
+  }
+  return SYLV_OK;
+}
+
+const char* sylv_sketch_last_error(const sylv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void sylv_sketch_destroy(sylv_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  for (auto& q : ctx->seq) free_seq(q);
+  for (auto& p : ctx->free_events) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  for (auto& p : ctx->timed) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  delete ctx;
+}
+
+sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, const double* C1,
+                             const double* C2, const sylv_config* cfg, void* nccl_comm, void* stream,
+                             sylv_ctx** out) {
+  if (!out) return SYLV_E_INVALID;
+  *out = nullptr;
+  if (!A || !B || !C1 || !C2 || !cfg) return SYLV_E_INVALID;
+  sylv_ctx* c = new sylv_ctx();
+  *out = c;
+  const int r = cfg->r;
+  if (!(r == 1 || r == 2 || r == 4 || r == 8)) return fail(c, SYLV_E_INVALID, "r must be 1, 2, 4 or 8");
+  if (cfg->k < 1 || cfg->k > kMaxK) return fail(c, SYLV_E_INVALID, "k must be in [1, 4]");
+  if (cfg->d_max < 1) return fail(c, SYLV_E_INVALID, "d_max must be >= 1");
+  if (cfg->zeta < 1 || cfg->s <= 0 || cfg->s % cfg->zeta) return fail(c, SYLV_E_INVALID, "s must be a positive multiple of zeta");
+  if (cfg->s < (int64_t)(cfg->d_max + 1) * r) return fail(c, SYLV_E_INVALID, "s must be >= (d_max+1) r");
+  if (nccl_comm) return fail(c, SYLV_E_NCCL, "multi-rank contexts are not part of this build");
+  if (A->n != B->n || A->n <= 0) return fail(c, SYLV_E_INVALID, "A and B must be n x n with equal n");
+  if ((uint64_t)A->n * cfg->zeta >= (1ull << 32)) return fail(c, SYLV_E_INVALID, "n*zeta must be < 2^32");
+  for (const sylv_operator* o : {A, B}) {
+    if (o->kind == SYLV_OP_STENCIL2D || o->kind == SYLV_OP_STENCIL3D) {
+      const int64_t N = o->grid[0];
+      const int64_t nn = (o->kind == SYLV_OP_STENCIL2D) ? N * N : N * N * N;
+      if (N < 1 || nn != o->n) return fail(c, SYLV_E_INVALID, "stencil grid does not match n");
+    } else if (o->kind == SYLV_OP_CSR) {
+      if (!o->row_ptr || !o->col_idx || !o->val || o->nnz < 0) return fail(c, SYLV_E_INVALID, "CSR arrays missing");
+    } else {
+      return fail(c, SYLV_E_INVALID, "unknown operator kind");
+    }
+  }
+  return guard(c, [&]() -> sylv_status {
+    c->st = (cudaStream_t)stream;
+    c->R = r;
+    c->K = cfg->k;
+    c->dmax = cfg->d_max;
+    c->zeta = cfg->zeta;
+    c->n = A->n;
+    c->s = cfg->s;
+    c->tol = cfg->tol;
+    c->rank_tol = cfg->rank_tol > 0 ? cfg->rank_tol : 1e-12;
+    c->chunk = cfg->chunk > 0 ? std::min(cfg->chunk, kMaxChunk) : std::min(cfg->k + 1, kMaxChunk);
+    c->cflags = cfg->flags;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&c->sm, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t rows_per_cta = (int64_t)kWarps * (32 / r);
+    c->G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sm * 4, (c->n + rows_per_cta - 1) / rows_per_cta));
+    // Q^T w: (ceil(m/8) x RT) CTAs; at least 2 per SM at the smallest m
+    c->RT = (int)std::max<int64_t>(1, std::min<int64_t>(64, c->s / 512));
+    c->tileQ = (c->s + c->RT - 1) / c->RT;
+    c->CC = (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * c->sm + (c->s / 256)) / std::max<int64_t>(1, c->s / 256)));
+    init_sequence(c, c->seq[0], 0, A, false, C1, cfg->seed_u);
+    init_sequence(c, c->seq[1], 1, B, true, C2, cfg->seed_v);
+    return SYLV_OK;
+  });
+}
+
+sylv_status sylv_sketch_step(sylv_ctx* c, int32_t nsteps, int32_t* d_done) {
+  if (!c) return SYLV_E_INVALID;
+  if (d_done) *d_done = c->d_done;
+  if (c->broken) return fail(c, SYLV_E_BREAKDOWN, "breakdown at step " + std::to_string(c->breakdown_d));
+  return guard(c, [&]() -> sylv_status {
+    const int first = c->d_done + 1;
+    const int last = std::min(c->dmax, c->d_done + std::max(0, nsteps));
+    for (int j = first; j <= last; ++j) {
+      step_sequence(c, c->seq[0], j);
+      step_sequence(c, c->seq[1], j);
+    }
+    if (last >= first) {
+      for (auto& q : c->seq)
+        CK(cudaMemcpyAsync(q.flags_h + first, q.flags + first, (last - first + 2) * sizeof(int),
+                           cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      ev_collect(c);
+      for (int j = first; j <= last; ++j) {
+        const int f = c->seq[0].flags_h[j] | c->seq[1].flags_h[j];
+        if (f & 1 || f & 2) {
+          c->d_done = j;
+          c->stats.steps += j - first + 1;
+          c->broken = true;
+          c->breakdown_d = j;
+          if (d_done) *d_done = j;
+          return fail(c, SYLV_E_BREAKDOWN, "breakdown at step " + std::to_string(j));
+        }
+        const int g = c->seq[0].flags_h[j + 1] | c->seq[1].flags_h[j + 1];
+        if (g & 4) {
+          c->d_done = j;
+          c->stats.steps += j - first + 1;
+          if (d_done) *d_done = j;
+          return fail(c, SYLV_E_LOST_INDEP, "sketched basis lost independence at step " + std::to_string(j));
+        }
+      }
+      c->stats.steps += last - first + 1;
+      c->d_done = last;
+    }
+    if (d_done) *d_done = c->d_done;
+    if (nsteps > 0 && std::max(0, last - first + 1) < nsteps)
+      return fail(c, SYLV_E_NOT_CONVERGED, "d_max reached");
+    return SYLV_OK;
+  });
+}
+
+sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rho_rel) {
+  if (!c) return SYLV_E_INVALID;
+  if (d < 1 || d > c->d_done) return fail(c, SYLV_E_STATE, "residual(d) needs 1 <= d <= d_done");
+  if (!lapack_loaded()) return fail(c, SYLV_E_LAPACK, "host LAPACK not loaded: call sylv_set_lapack_path");
+  return guard(c, [&]() -> sylv_status {
+    auto t0 = std::chrono::steady_clock::now();
+    const int r = c->R, m = d * r;
+    Sequence& U = c->seq[0];
+    Sequence& V = c->seq[1];
+    std::vector<double> MU, MV;
+    build_projected(d, r, c->K, U.Th, U.ldT, U.Hh, MU);
+    build_projected(d, r, c->K, V.Th, V.ldT, V.Hh, MV);
+    double hhat[kMaxR * kMaxR], ghat[kMaxR * kMaxR], Bm[kMaxR * kMaxR];
+    hat_coefficient(d, r, c->K, U.Th, U.ldT, U.Hh, hhat);
+    hat_coefficient(d, r, c->K, V.Th, V.ldT, V.Hh, ghat);
+    double bn = 0.0;
+    for (int a = 0; a < r; ++a)
+      for (int b = 0; b < r; ++b) {
+        double s = 0.0;
+        for (int p = 0; p < r; ++p) s += U.beta[a * r + p] * V.beta[b * r + p];
+        Bm[a * r + b] = s;
+        bn += s * s;
+      }
+    bn = std::sqrt(bn);
+    std::string err;
+    const int info = sylvester_bs(m, r, MU, MV, Bm, c->Y, err);
+    c->stats.host_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    c->stats.host_solves++;
+    if (info < 0) return fail(c, SYLV_E_LAPACK, err);
+    if (info > 0) {
+      c->y_d = -1;
+      if (rho) *rho = NAN;
+      if (rho_rel) *rho_rel = NAN;
+      return fail(c, SYLV_E_SINGULAR, err);
+    }
+    c->y_d = d;
+    // rho^2 = ||hhat E_d^T Y||^2 + ||Y E_d ghat^T||^2 (Y col-major m x m)
+    double s1 = 0.0, s2 = 0.0;
+    for (int col = 0; col < m; ++col)
+      for (int a = 0; a < r; ++a) {
+        double v = 0.0;
+        for (int p = 0; p < r; ++p) v += hhat[a * r + p] * c->Y[(size_t)col * m + (m - r + p)];
+        s1 += v * v;
+      }
+    for (int row = 0; row < m; ++row)
+      for (int a = 0; a < r; ++a) {
+        double v = 0.0;
+        for (int p = 0; p < r; ++p) v += c->Y[(size_t)(m - r + p) * m + row] * ghat[a * r + p];
+        s2 += v * v;
+      }
+    const double rh = std::sqrt(s1 + s2);
+    if (rho) *rho = rh;
+    if (rho_rel) *rho_rel = rh / bn;
+    c->hist.emplace_back(d, rh / bn);
+    return SYLV_OK;
+  });
+}
+
+sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2, int64_t ldx,
+                                 int32_t max_rank, int32_t* rank) {
+  if (!c) return SYLV_E_INVALID;
+  if (d < 1 || d > c->d_done) return fail(c, SYLV_E_STATE, "solution(d) needs 1 <= d <= d_done");
+  if (!X1 || !X2 || max_rank < 0 || ldx < max_rank) return fail(c, SYLV_E_INVALID, "bad output buffers");
+  if (c->y_d != d) {
+    double rho, rr;
+    sylv_status s = sylv_sketch_residual(c, d, &rho, &rr);
+    if (s != SYLV_OK) return s;
+  }
+  return guard(c, [&]() -> sylv_status {
+    const int r = c->R, m = d * r, K = c->K;
+    std::vector<double> Y1, Y2;
+    std::string err;
+    const int l = svd_truncate(m, c->Y, c->rank_tol, max_rank, Y1, Y2, err);
+    if (l < 0) return fail(c, SYLV_E_LAPACK, err);
+    if (rank) *rank = l;
+    double* Xout[2] = {X1, X2};
+    std::vector<double>* Ys[2] = {&Y1, &Y2};
+    const int C = c->chunk;
+    for (int qi = 0; qi < 2; ++qi) {
+      Sequence& q = c->seq[qi];
+      // Z = T_d^{-1} Y_q ; M_b = R_b Z[b-block]  (U_b = Z_b R_b)
+      trsm_left_upper(m, l, q.Th, q.ldT, Ys[qi]->data());
+      CK(cudaMemcpyAsync(q.Rh, q.Rall, (size_t)(d + 2) * r * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      std::vector<double> M((size_t)m * std::max(l, 1), 0.0);
+      for (int b = 1; b <= d; ++b)
+        for (int a = 0; a < r; ++a)
+          for (int col = 0; col < l; ++col) {
+            double s = 0.0;
+            for (int p = 0; p < r; ++p)
+              s += q.Rh[(size_t)b * r * r + a * r + p] * (*Ys[qi])[(size_t)col * m + (b - 1) * r + p];
+            M[(size_t)((b - 1) * r + a) * l + col] = s;
+          }
+      const bool dev_out = is_device_ptr(Xout[qi]);
+      double* Xd = dev_out ? Xout[qi] : dalloc<double>((size_t)c->n * ldx);
+      CK(cudaMemsetAsync(Xd, 0, (size_t)c->n * ldx * sizeof(double), c->st));
+      if (l > 0) {
+        double* Md = dalloc<double>(M.size());
+        double* rbuf = dalloc<double>((size_t)(K + C) * c->n * r);
+        CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+        auto rslot = [&](int j) { return rbuf + (int64_t)(j % (K + C)) * c->n * r; };
+        CK(cudaMemcpyAsync(rslot(1), q.Cdev, (size_t)c->n * r * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+        int j0 = 1;
+        for (int j = 1; j <= d; ++j) {
+          if (j >= 2) {  // Z_j from Z_{j-nwin..j-1} with the stored pass-2 coefficients of step j-1
+            const int jp = j - 1;
+            const int nwin = std::min(K, jp);
+            Win win{};
+            for (int i = 0; i < nwin; ++i) win.p[i] = rslot(jp - nwin + 1 + i);
+            SYLV_DISPATCH_RK(r, K, {
+              k_pass2<R_, K_, false><<<c->G, kThreads, 0, c->st>>>(q.op, win, nwin, nullptr,
+                                                                   q.Kc + (int64_t)jp * (1 + K) * r * r,
+                                                                   rslot(j), nullptr, q.sp, nullptr);
+            });
+            count(c);
+          }
+          if (j - j0 + 1 == C || j == d) {
+            ChunkPtrs cp{};
+            for (int b = j0; b <= j; ++b) cp.p[b - j0] = rslot(b);
+            const int64_t tot = c->n * (int64_t)l;
+            const int gx = (int)std::min<int64_t>((int64_t)c->sm * 8, (tot + 255) / 256);
+            SYLV_DISPATCH_R(r, {
+              k_xacc<R_><<<gx, kThreads, 0, c->st>>>(c->n, cp, j - j0 + 1, Md + (int64_t)(j0 - 1) * r * l, l, Xd, ldx);
+            });
+            count(c);
+            j0 = j + 1;
+          }
+          CK(cudaGetLastError());
+        }
+        CK(cudaStreamSynchronize(c->st));
+        cudaFree(Md);
+        cudaFree(rbuf);
+      }
+      if (!dev_out) {
+        CK(cudaMemcpyAsync(Xout[qi], Xd, (size_t)c->n * ldx * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        cudaFree(Xd);
+      }
+    }
+    CK(cudaStreamSynchronize(c->st));
+    return SYLV_OK;
+  });
+}
+
+sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
+  if (!c) return SYLV_E_INVALID;
+  // canonical schedule (R9): every step to 50, every 10 while d r <= 800,
+  // then d_next = 10 ceil(1.15 d_prev / 10); d_max included; bisection after a pass.
+  std::vector<int> sched;
+  for (int d = 1; d <= std::min(50, c->dmax); ++d) sched.push_back(d);
+  int d = 50;
+  while (true) {
+    if ((d + 10) * c->R <= 800) d += 10;
+    else d = 10 * (int)std::ceil(1.15 * d / 10.0);
+    if (d >= c->dmax) break;
+    sched.push_back(d);
+  }
+  if (sched.empty() || sched.back() != c->dmax) sched.push_back(c->dmax);
+  int d_fail = 0, d_pass = -1, skips = 0;
+  double rr_pass = NAN, last_rr = NAN;
+  for (int dc : sched) {
+    if (dc > c->dmax) break;
+    if (c->d_done < dc && !c->broken) {
+      int dd = 0;
+      sylv_status s = sylv_sketch_step(c, dc - c->d_done, &dd);
+      if (s != SYLV_OK && s != SYLV_E_BREAKDOWN && s != SYLV_E_NOT_CONVERGED) return s;
+    }
+    const int dchk = std::min(dc, c->d_done);
+    double rho, rr;
+    sylv_status s = sylv_sketch_residual(c, dchk, &rho, &rr);
+    if (s == SYLV_E_SINGULAR) {
+      if (++skips >= 5) break;
+      continue;
+    }
+    if (s != SYLV_OK) return s;
+    skips = 0;
+    last_rr = rr;
+    if (rr < c->tol || c->broken) {
+      d_pass = dchk;
+      rr_pass = rr;
+      break;
+    }
+    d_fail = dchk;
+  }
+  if (d_pass < 0) {
+    if (d_star) *d_star = c->d_done;
+    if (rho_rel) *rho_rel = last_rr;
+    return fail(c, SYLV_E_NOT_CONVERGED, "tolerance not reached by d_max");
+  }
+  int lo = d_fail, hi = d_pass;
+  while (hi - lo > 1 && !c->broken) {
+    const int mid = (lo + hi) / 2;
+    double rho, rr;
+    sylv_status s = sylv_sketch_residual(c, mid, &rho, &rr);
+    if (s == SYLV_OK && rr < c->tol) {
+      hi = mid;
+      rr_pass = rr;
+    } else {
+      lo = mid;
+    }
+  }
+  if (c->y_d != hi) {
+    double rho, rr;
+    sylv_sketch_residual(c, hi, &rho, &rr);
+  }
+  if (d_star) *d_star = hi;
+  if (rho_rel) *rho_rel = rr_pass;
+  return SYLV_OK;
+}
+
+sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X, int32_t r, double* Yout) {
+  if (!c || !X || !Yout || (which != 0 && which != 1)) return SYLV_E_INVALID;
+  if (!(r == 1 || r == 2 || r == 4 || r == 8)) return fail(c, SYLV_E_INVALID, "r must be 1, 2, 4 or 8");
+  return guard(c, [&]() -> sylv_status {
+    Sequence& q = c->seq[which];
+    const bool xin = is_device_ptr(X), yout = is_device_ptr(Yout);
+    const double* Xd = X;
+    double* Xtmp = nullptr;
+    if (!xin) {
+      Xtmp = dalloc<double>((size_t)c->n * r);
+      CK(cudaMemcpyAsync(Xtmp, X, (size_t)c->n * r * sizeof(double), cudaMemcpyHostToDevice, c->st));
+      Xd = Xtmp;
+    }
+    double* Yd = yout ? Yout : dalloc<double>((size_t)c->s * r);
+    CK(cudaMemsetAsync(Yd, 0, (size_t)c->s * r * sizeof(double), c->st));
+    const int64_t rows_per_cta = (int64_t)kWarps * (32 / r);
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sm * 4, (c->n + rows_per_cta - 1) / rows_per_cta));
+    SYLV_DISPATCH_R(r, { k_sketch_gram<R_><<<g, kThreads, 0, c->st>>>(c->n, Xd, q.sp, Yd, nullptr); });
+    count(c);
+    CK(cudaGetLastError());
+    if (!yout) {
+      CK(cudaMemcpyAsync(Yout, Yd, (size_t)c->s * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    if (Xtmp) cudaFree(Xtmp);
+    if (!yout) cudaFree(Yd);
+    return SYLV_OK;
+  });
+}
+
+sylv_status sylv_sketch_get_small(sylv_ctx* c, int32_t which, int32_t d, double* H, double* T, double* beta) {
+  if (!c || (which != 0 && which != 1)) return SYLV_E_INVALID;
+  if (d < 0 || d > c->d_done) return fail(c, SYLV_E_STATE, "get_small(d) needs 0 <= d <= d_done");
+  const Sequence& q = c->seq[which];
+  const int r = c->R, K = c->K, m = d * r;
+  if (H) {
+    std::fill(H, H + (size_t)(m + r) * m, 0.0);
+    for (int j = 1; j <= d; ++j) {
+      const int nwin = std::min(K, j);
+      for (int ii = 0; ii <= nwin; ++ii) {
+        const int i = (ii < nwin) ? (j - nwin + 1 + ii) : (j + 1);
+        const double* h = q.Hh + (size_t)j * (K + 1) * r * r + (size_t)((ii < nwin) ? ii : K) * r * r;
+        for (int a = 0; a < r; ++a)
+          for (int b = 0; b < r; ++b) H[(size_t)((i - 1) * r + a) * m + (j - 1) * r + b] = h[a * r + b];
+      }
+    }
+  }
+  if (T) {
+    for (int a = 0; a < m + r; ++a)
+      for (int b = 0; b < m + r; ++b) T[(size_t)a * (m + r) + b] = q.Th[(int64_t)b * q.ldT + a];
+  }
+  if (beta) std::memcpy(beta, q.beta, r * r * sizeof(double));
+  return SYLV_OK;
+}
+
+sylv_status sylv_sketch_get_block(sylv_ctx* c, int32_t which, int32_t j, double* out) {
+  if (!c || !out || (which != 0 && which != 1)) return SYLV_E_INVALID;
+  if (j < 1 || j > c->d_done + 1 || j < c->d_done + 1 - c->K)
+    return fail(c, SYLV_E_STATE, "block j is not in the window");
+  return guard(c, [&]() -> sylv_status {
+    Sequence& q = c->seq[which];
+    const int r = c->R;
+    const bool dev = is_device_ptr(out);
+    double* od = dev ? out : dalloc<double>((size_t)c->n * r);
+    SYLV_DISPATCH_R(r, { k_zr<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, q.slot(j), q.Rall + (int64_t)j * r * r, od); });
+    count(c);
+    CK(cudaGetLastError());
+    if (!dev) CK(cudaMemcpyAsync(out, od, (size_t)c->n * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (!dev) cudaFree(od);
+    return SYLV_OK;
+  });
+}
+
+sylv_status sylv_sketch_history(sylv_ctx* c, int32_t cap, int32_t* d, double* rho_rel, int32_t* cnt) {
+  if (!c) return SYLV_E_INVALID;
+  const int n = (int)std::min<size_t>(c->hist.size(), (size_t)std::max(0, cap));
+  for (int i = 0; i < n; ++i) {
+    if (d) d[i] = c->hist[i].first;
+    if (rho_rel) rho_rel[i] = c->hist[i].second;
+  }
+  if (cnt) *cnt = (int32_t)c->hist.size();
+  return SYLV_OK;
+}
+
+sylv_status sylv_sketch_stats(sylv_ctx* c, sylv_stats* out) {
+  if (!c || !out) return SYLV_E_INVALID;
+  *out = c->stats;
+  return SYLV_OK;
+}
+
+void sylv_sketch_reset_stats(sylv_ctx* c) {
+  if (!c) return;
+  const int64_t l = c->stats.launches, s = c->stats.steps;
+  c->stats = sylv_stats{};
+  c->stats.launches = l;
+  c->stats.steps = s;
+}
+
+}  // extern "C"

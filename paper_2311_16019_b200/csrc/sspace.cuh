@@ -1,0 +1,253 @@
+// sspace.cuh — coefficient kernels (one CTA) and sketch-space QR update kernels
+// (SURVEY §8(a) rows a2/a3 coefficients and a5; Alg. 1 line 9).
+//
+// Sketch-space data: Q (s x m, column-major, ld = s, orthonormal columns), T (mT x mT,
+// column-major, upper triangular), w (s x R row-major, the new sketched block).
+// The update is block CGS2:  c1 = Q^T w, w -= Q c1, c2 = Q^T w, w -= Q c2,
+// w = q tau (CholQR2, positive diagonal), T_H = c1 + c2  (R7).
+#pragma once
+#include "common.cuh"
+
+namespace sylv {
+
+// Deterministic column sums of per-CTA partials: out[e] = sum_p partial[p*len + e].
+__device__ __forceinline__ double sum_parts(const double* __restrict__ partial, int nparts,
+                                            int64_t len, int64_t e) {
+  double s = 0.0;
+  for (int p = 0; p < nparts; ++p) s += partial[(int64_t)p * len + e];
+  return s;
+}
+
+// h_{i,j} = R_i^T P_i R_j, K_i = R_i h_{i,j}; Kc[j] = [R_j, K_0..]; Hc[j] = [h_.., 0.., h_{j+1,j}]
+template <int R, int K>
+__global__ void k_coef1(const double* __restrict__ partial, int nparts, int nwin, int j,
+                        const double* __restrict__ Rall, double* __restrict__ Kc,
+                        double* __restrict__ Hc, double* __restrict__ hnorm2) {
+  __shared__ double P[K * R * R];
+  for (int e = threadIdx.x; e < nwin * R * R; e += blockDim.x)
+    P[e] = sum_parts(partial, nparts, K * R * R, e);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const double* Rd = Rall + (int64_t)j * R * R;
+  double* Kout = Kc + (int64_t)j * (1 + K) * R * R;
+  double* Hout = Hc + (int64_t)j * (K + 1) * R * R;
+  for (int e = 0; e < R * R; ++e) Kout[e] = Rd[e];
+  double tmp[R * R], h[R * R], kk[R * R];
+  double hn = 0.0;
+  for (int i = 0; i < K; ++i) {
+    if (i < nwin) {
+      const double* Ri = Rall + (int64_t)(j - nwin + 1 + i) * R * R;
+      mtm<R>(Ri, P + i * R * R, tmp);
+      mm<R>(tmp, Rd, h);
+      mm<R>(Ri, h, kk);
+      for (int e = 0; e < R * R; ++e) {
+        Hout[i * R * R + e] = h[e];
+        Kout[(1 + i) * R * R + e] = kk[e];
+        hn += h[e] * h[e];
+      }
+    } else {
+      for (int e = 0; e < R * R; ++e) Hout[i * R * R + e] = 0.0;
+    }
+  }
+  hnorm2[j] = hn;
+}
+
+// G = W'^T W' -> h_{j+1,j} = chol(G) (upper, positive diagonal), R_{j+1} = h^{-1};
+// breakdown flag (bit 0) if min diag h <= 1e-14 ||W~||_F  (R11), with
+// ||W~||_F^2 = ||W'||_F^2 + sum_i ||h_{i,j}||_F^2 (window orthonormal); bit 1 if G not PD.
+template <int R, int K>
+__global__ void k_coef2(const double* __restrict__ partial, int nparts, int j,
+                        double* __restrict__ Rall, double* __restrict__ Hc,
+                        const double* __restrict__ hnorm2, int* __restrict__ flags) {
+  __shared__ double G[R * R];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) G[e] = sum_parts(partial, nparts, R * R, e);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double h[R * R], hi[R * R];
+  int fl = 0;
+  if (!chol_upper<R>(G, h)) {
+    fl |= 2;
+    for (int e = 0; e < R * R; ++e) h[e] = (e % (R + 1) == 0) ? 1.0 : 0.0;
+  }
+  inv_upper<R>(h, hi);
+  double tr = 0.0, mind = 1e300;
+  for (int a = 0; a < R; ++a) {
+    tr += G[a * R + a];
+    mind = fmin(mind, h[a * R + a]);
+  }
+  const double wn = sqrt(tr + hnorm2[j]);
+  if (mind <= 1e-14 * wn) fl |= 1;
+  double* Hout = Hc + (int64_t)j * (K + 1) * R * R + K * R * R;
+  double* Rn = Rall + (int64_t)(j + 1) * R * R;
+  for (int e = 0; e < R * R; ++e) {
+    Hout[e] = h[e];
+    Rn[e] = hi[e];
+  }
+  flags[j] |= fl;
+}
+
+// tau = chol(sum of Gram partials) (upper); tinv = tau^{-1}; if prev: tau_out = tau * prev.
+// Sets flags[slot] bit 2 if not positive definite (lost independence).
+template <int R>
+__global__ void k_chol_small(const double* __restrict__ partial, int nparts,
+                             double* __restrict__ tau_out, double* __restrict__ tinv_out,
+                             const double* __restrict__ prev, int* __restrict__ flags, int slot) {
+  __shared__ double G[R * R];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) G[e] = sum_parts(partial, nparts, R * R, e);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double t[R * R], ti[R * R];
+  if (!chol_upper<R>(G, t)) {
+    flags[slot] |= 4;
+    for (int e = 0; e < R * R; ++e) t[e] = (e % (R + 1) == 0) ? 1.0 : 0.0;
+  }
+  inv_upper<R>(t, ti);
+  for (int e = 0; e < R * R; ++e) tinv_out[e] = ti[e];
+  if (prev) {
+    double tp[R * R];
+    mm<R>(t, prev, tp);
+    for (int e = 0; e < R * R; ++e) tau_out[e] = tp[e];
+  } else {
+    for (int e = 0; e < R * R; ++e) tau_out[e] = t[e];
+  }
+}
+
+// out = A M for a rows x R row-major A; if colmajor_ld > 0 the result is written
+// column-major (out[c*ld + row], the Q layout), else row-major.
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_rmul(int64_t rows, const double* __restrict__ A,
+                                                   const double* __restrict__ M, double* __restrict__ out,
+                                                   int64_t colmajor_ld) {
+  __shared__ double ms[R * R];
+  if (threadIdx.x < R * R) ms[threadIdx.x] = M[threadIdx.x];
+  __syncthreads();
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < rows * R;
+       e += (int64_t)gridDim.x * kThreads) {
+    const int64_t row = e / R;
+    const int c = (int)(e - row * R);
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; ++a) s = fma(A[row * R + a], ms[a * R + c], s);
+    if (colmajor_ld > 0)
+      out[(int64_t)c * colmajor_ld + row] = s;
+    else
+      out[e] = s;
+  }
+}
+
+// partial[(rt*m + j)*R + c] = sum_{rows in tile rt} Q[j*s + row] w[row*R + c]
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_qtw(const double* __restrict__ Q, int64_t s, int m,
+                                                  const double* __restrict__ w, int64_t tile,
+                                                  double* __restrict__ partial) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.x * kWarps + warp;
+  const int rt = blockIdx.y;
+  const int64_t r0 = (int64_t)rt * tile;
+  const int64_t r1 = min(s, r0 + tile);
+  double acc[R];
+#pragma unroll
+  for (int c = 0; c < R; ++c) acc[c] = 0.0;
+  if (j < m) {
+    const double* __restrict__ q = Q + (int64_t)j * s;
+    for (int64_t row = r0 + lane; row < r1; row += 32) {
+      const double qv = __ldg(q + row);
+#pragma unroll
+      for (int c = 0; c < R; ++c) acc[c] = fma(qv, __ldg(w + row * R + c), acc[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < R; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(SYLV_FULL_MASK, v, off);
+    acc[c] = v;
+  }
+  if (j < m && lane == 0) {
+#pragma unroll
+    for (int c = 0; c < R; ++c) partial[((int64_t)rt * m + j) * R + c] = acc[c];
+  }
+}
+
+// out[e] = sum_rt partial[rt*len + e]  (+ optional accumulation into acc_out: acc_out[e] += out[e])
+__global__ void k_red_parts(const double* __restrict__ partial, int nparts, int64_t len,
+                            double* __restrict__ out, double* __restrict__ acc_out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = sum_parts(partial, nparts, len, e);
+    out[e] = v;
+    if (acc_out) acc_out[e] += v;
+  }
+}
+
+// partial2[(cc*s + row)*R + c] = sum_{j in chunk cc} Q[j*s + row] cvec[j*R + c]
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_qc_part(const double* __restrict__ Q, int64_t s, int m,
+                                                      const double* __restrict__ cvec, int cols_per_chunk,
+                                                      double* __restrict__ partial2) {
+  constexpr int kStage = 256;
+  __shared__ double cs[kStage * R];
+  const int cc = blockIdx.y;
+  const int j0 = cc * cols_per_chunk;
+  const int j1 = min(m, j0 + cols_per_chunk);
+  const int64_t row = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  double acc[R];
+#pragma unroll
+  for (int c = 0; c < R; ++c) acc[c] = 0.0;
+  for (int jj = j0; jj < j1; jj += kStage) {
+    const int nj = min(kStage, j1 - jj);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nj * R; e += kThreads) cs[e] = cvec[(int64_t)jj * R + e];
+    __syncthreads();
+    if (row < s) {
+      const double* __restrict__ q = Q + (int64_t)jj * s + row;
+      for (int t = 0; t < nj; ++t) {
+        const double qv = __ldg(q + (int64_t)t * s);
+#pragma unroll
+        for (int c = 0; c < R; ++c) acc[c] = fma(qv, cs[t * R + c], acc[c]);
+      }
+    }
+  }
+  if (row < s) {
+#pragma unroll
+    for (int c = 0; c < R; ++c) partial2[((int64_t)cc * s + row) * R + c] = acc[c];
+  }
+}
+
+// w[row*R + c] -= sum_cc partial2[(cc*s + row)*R + c]
+__global__ void k_wsub(double* __restrict__ w, const double* __restrict__ partial2, int ncc,
+                       int64_t len) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < ncc; ++p) s += partial2[(int64_t)p * len + e];
+    w[e] -= s;
+  }
+}
+
+// T[:, m:m+R] = [c1 + c2 (m x R); tau (R x R)]  (column-major, ld = ldT)
+template <int R>
+__global__ void k_tcol(const double* __restrict__ csum, const double* __restrict__ tau,
+                       double* __restrict__ T, int64_t ldT, int m) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (m + R) * R; e += gridDim.x * blockDim.x) {
+    const int cc = e / (m + R);
+    const int i = e - cc * (m + R);
+    const double v = (i < m) ? csum[(int64_t)i * R + cc] : tau[(i - m) * R + cc];
+    T[(int64_t)(m + cc) * ldT + i] = v;
+  }
+}
+
+// tau_1 = beta ell^{-1}  (R3), written to T[0:R, 0:R]; ell = chol(C^T C)
+template <int R>
+__global__ void k_init_tau(const double* __restrict__ beta, const double* __restrict__ ell,
+                           double* __restrict__ T, int64_t ldT, double* __restrict__ R1) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double li[R * R], t[R * R];
+  inv_upper<R>(ell, li);
+  mm<R>(beta, li, t);
+  for (int a = 0; a < R; ++a)
+    for (int c = 0; c < R; ++c) T[(int64_t)c * ldT + a] = t[a * R + c];
+  for (int e = 0; e < R * R; ++e) R1[e] = li[e];
+}
+
+}  // namespace sylv

@@ -1,0 +1,181 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU fp64 oracle on the
+same seeded inputs.  Tolerances (BASELINE.json north star):
+  sketch of a fixed block          1e-12 relative (max-norm)
+  per-step rho_rel (first 50 steps) 1e-8 relative
+  small matrices H, T, beta, and the window blocks U_j: 1e-9 relative (Frobenius)
+  d* within +-2, true relative residual within 10% of the oracle's at the same d.
+Sizes span several CTAs and a ragged tail (n not a multiple of the rows per CTA).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import alg1, operators, sparse_sign  # noqa: E402
+from synth import inputs  # noqa: E402
+
+
+def _pkg():
+    import paper_2311_16019_b200 as pkg
+    return pkg
+
+
+CASES = {
+    "2d-r1": dict(kind="stencil2d", N=23, r=1, k=2, d_max=60),
+    "2d-r4": dict(kind="stencil2d", N=37, r=4, k=2, d_max=60),
+    "3d-r8k3": dict(kind="stencil3d", N=19, r=8, k=3, d_max=55),
+    "3d-r2k1": dict(kind="stencil3d", N=11, r=2, k=1, d_max=55),
+    "csr-r2": dict(kind="csr", n=20011, nnz_off=20, band=300, r=2, k=2, d_max=55),
+    "csr-r4k4": dict(kind="csr", n=5003, nnz_off=6, band=40, r=4, k=4, d_max=55),
+}
+
+
+def _setup(name, keep_basis=False):
+    cfg = inputs.small_config(**CASES[name])
+    csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
+    C1, C2 = inputs.make_rhs(cfg)
+    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2, csr_pair=csr, keep_basis=keep_basis)
+    gpu = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr,
+                             stream=torch.cuda.current_stream().cuda_stream)
+    return cfg, csr, C1, C2, orc, gpu
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_sketch_of_fixed_block(name):
+    cfg = inputs.small_config(**CASES[name])
+    gpu = _setup(name)[-1]
+    rng = np.random.default_rng(7)
+    for which, seed in ((0, cfg.seed_u), (1, cfg.seed_v)):
+        X = rng.standard_normal((cfg.n, cfg.r))
+        got = gpu.apply_sketch(which, torch.from_numpy(X).cuda())
+        want = sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, seed) @ X
+        assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_per_step_rho_and_small_matrices(name):
+    cfg, csr, C1, C2, orc, gpu = _setup(name, keep_basis=True)
+    worst = 0.0
+    for d in range(1, 51):
+        gpu.step(1)
+        orc.step(1)
+        _, rr = gpu.residual(d)
+        ro = orc.residual(d).rho_rel
+        worst = max(worst, abs(rr - ro) / ro)
+    assert worst <= 1e-8, worst
+    for which, seq in ((0, orc.U), (1, orc.V)):
+        d = 12
+        H, T, beta = gpu.get_small(which, d)
+        m = d * cfg.r
+        assert _rel(H, seq.Hbar(d)) <= 1e-9
+        assert _rel(T, seq.T[:m + cfg.r, :m + cfg.r]) <= 1e-9
+        assert _rel(beta, seq.beta) <= 1e-12
+        for j in range(51 - cfg.k + 1, 52):
+            Ug = gpu.get_block(which, j)
+            assert _rel(Ug, seq.U[j]) <= 1e-8, (which, j)
+
+
+@pytest.mark.parametrize("name", ["2d-r1", "csr-r2", "3d-r8k3"])
+def test_solution_and_true_residual(name):
+    cfg, csr, C1, C2, orc, gpu = _setup(name)
+    d = 30
+    gpu.step(d)
+    orc.step(d)
+    res = orc.residual(d)
+    _, rr = gpu.residual(d)
+    assert abs(rr - res.rho_rel) <= 1e-8 * res.rho_rel
+    X1o, X2o = orc.solution(d, res.Y)
+    max_rank = X1o.shape[1] + 8
+    X1, X2, rank = gpu.solution(d, max_rank)
+    assert abs(rank - X1o.shape[1]) <= 1
+    A, _, B = operators.operator_pair(cfg, csr)
+    _, tro = alg1.true_residual(A, B, C1, C2, X1o, X2o)
+    _, trg = alg1.true_residual(A, B, C1, C2, X1[:, :rank], X2[:, :rank])
+    assert abs(trg - tro) <= 0.1 * tro
+    Xo = X1o @ X2o.T
+    Xg = X1[:, :rank] @ X2[:, :rank].T
+    assert _rel(Xg, Xo) <= 1e-6
+
+
+def test_full_solve_c0_matches_oracle():
+    cfg = inputs.get_config("c0")
+    C1, C2 = inputs.make_rhs(cfg)
+    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2)
+    ro = alg1.solve(orc, cfg.tol, cfg.d_max)
+    gpu = _pkg().from_config(cfg, C1=C1, C2=C2)
+    d_star, rr, st = gpu.solve()
+    assert st == 0 and ro.converged
+    assert abs(d_star - ro.d_star) <= 2
+    X1o, X2o = orc.solution(ro.d_star, ro.Y)
+    X1, X2, rank = gpu.solution(d_star, X1o.shape[1] + 16)
+    A, _, B = operators.operator_pair(cfg)
+    _, tro = alg1.true_residual(A, B, C1, C2, X1o, X2o)
+    _, trg = alg1.true_residual(A, B, C1, C2, X1[:, :rank], X2[:, :rank])
+    assert abs(trg - tro) <= 0.1 * tro
+
+
+def test_edge_tiny_n_and_small_buckets():
+    """n = 16 < 32 rows (one partial warp group), b = s/zeta = 6 < 32 slots per bucket."""
+    cfg = inputs.small_config("stencil2d", N=4, r=1, k=2, d_max=5, s=48)
+    C1, C2 = inputs.make_rhs(cfg)
+    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2)
+    gpu = _pkg().from_config(cfg, C1=C1, C2=C2)
+    for d in range(1, 5):
+        gpu.step(1)
+        orc.step(1)
+        _, rr = gpu.residual(d)
+        ro = orc.residual(d).rho_rel
+        assert abs(rr - ro) <= 1e-8 * ro
+
+
+def test_breakdown_closed_form():
+    N = 10
+    x = np.arange(1, N + 1) / (N + 1)
+    v = np.kron(np.sin(2 * np.pi * x), np.sin(np.pi * x))[:, None] * 3.0
+    A = operators.stencil_matrix(N, (0.0, 0.0))
+    lam = float((v.T @ (A @ v)).item() / (v.T @ v).item())
+    pkg = _pkg()
+    op = pkg.stencil_operator("stencil2d", N, (0.0, 0.0))
+    gpu = pkg.SylvSketch(op, op, v, v, r=1, k=2, d_max=10, s=64)
+    d, st = gpu.step(3)
+    assert st == 5 and d == 1          # SYLV_E_BREAKDOWN at d = 1
+    _, rr = gpu.residual(1)
+    assert rr < 1e-10
+    X1, X2, rank = gpu.solution(1, 2)
+    X = v @ v.T / (2 * lam)
+    assert _rel(X1[:, :rank] @ X2[:, :rank].T, X) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3", "c4"])
+def test_sketch_full_config_sizes(name):
+    """S X at every BASELINE config's (n, r, s), both seeds, vs the oracle's hashed S."""
+    cfg = inputs.get_config(name)
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((cfg.n, cfg.r))
+    Xd = torch.from_numpy(X).cuda()
+    pkg = _pkg()
+    op = pkg.stencil_operator("stencil2d", 4, (0.0, 0.0))
+    op.n = cfg.n          # apply_sketch only needs n; a context of the right n and s
+    small = np.ones((cfg.n, cfg.r))
+    # build a context with the config's sizes but a 1-step d_max (no stepping happens)
+    if cfg.kind.startswith("stencil"):
+        A = pkg.stencil_operator(cfg.kind, cfg.N, cfg.wA)
+    else:
+        A = pkg.stencil_operator("stencil2d", 2048, (0.0, 0.0))   # n = 2^22 = c4's n
+    C1 = torch.from_numpy(rng.standard_normal((cfg.n, cfg.r))).cuda()
+    gpu = pkg.SylvSketch(A, A, C1, C1, r=cfg.r, k=cfg.k, d_max=2, s=cfg.s, seed_u=cfg.seed_u,
+                         seed_v=cfg.seed_v)
+    del small
+    for which, seed in ((0, cfg.seed_u), (1, cfg.seed_v)):
+        got = gpu.apply_sketch(which, Xd)
+        want = sparse_sign.apply_hashed(X, cfg.s, cfg.zeta, seed)
+        assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+    gpu.close()

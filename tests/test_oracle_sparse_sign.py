@@ -118,3 +118,12 @@ def test_marchenko_pastur_edges(n, m, s):
     sv = np.linalg.svd(S @ V, compute_uv=False) ** 2
     lo, hi = (1 - math.sqrt(m / s)) ** 2, (1 + math.sqrt(m / s)) ** 2
     assert sv.min() > lo - 0.08 and sv.max() < hi + 0.15
+
+
+def test_apply_hashed_equals_materialised_product():
+    rng = np.random.default_rng(5)
+    n, s, r = 10007, 640, 3
+    X = rng.standard_normal((n, r))
+    S = sparse_sign.matrix(n, s, 8, 12)
+    got = sparse_sign.apply_hashed(X, s, 8, 12, chunk=3000)
+    assert np.allclose(got, S @ X, rtol=1e-13, atol=1e-13 * np.abs(X).sum())
