@@ -178,6 +178,19 @@ void sylv_sketch_destroy(sylv_ctx* ctx);
  * returns SYLV_E_LAPACK if the library or a symbol cannot be loaded. */
 sylv_status sylv_set_lapack_path(const char* path);
 
+/* Host-only entries of the a6 step (no device work; used by the CPU test suite).
+ * sylv_host_projected: M = [T_d | T_H] H_und_d T_d^{-1} (R6) from T (col-major,
+ *   ld ldT, >= (d+1)r square) and the per-step coefficient layout of the library:
+ *   H[j*(k+1)*r*r + slot*r*r + a*r + c], slot i < min(k,j) -> h_{j-min(k,j)+1+i, j},
+ *   slot k -> h_{j+1,j} (row-major r x r blocks).  M: dr x dr col-major.
+ * sylv_host_sylvester: Bartels-Stewart for MU Y + Y MV^T = E1 B E1^T (B r x r row-major),
+ *   MU, MV, Y: m x m col-major (MU, MV are overwritten).  Returns SYLV_E_SINGULAR when
+ *   the solve breaks down, SYLV_E_LAPACK when LAPACK is missing. */
+sylv_status sylv_host_projected(int32_t d, int32_t r, int32_t k, const double* T, int64_t ldT,
+                                const double* H, double* M);
+sylv_status sylv_host_sylvester(int32_t m, int32_t r, double* MU, double* MV, const double* B,
+                                double* Y);
+
 /* Library version string. */
 const char* sylv_version(void);
 

@@ -56,7 +56,7 @@ SYMBOLS = ["sylv_sketch_init", "sylv_sketch_step", "sylv_sketch_residual", "sylv
            "sylv_sketch_solve", "sylv_sketch_apply_sketch", "sylv_sketch_get_small",
            "sylv_sketch_get_block", "sylv_sketch_history", "sylv_sketch_stats",
            "sylv_sketch_reset_stats", "sylv_sketch_last_error", "sylv_sketch_destroy",
-           "sylv_set_lapack_path", "sylv_version"]
+           "sylv_set_lapack_path", "sylv_version", "sylv_host_projected", "sylv_host_sylvester"]
 
 
 def lapack_path() -> str:
@@ -99,6 +99,10 @@ def load_library(path: str = LIB_PATH):
     lib.sylv_sketch_destroy.restype = None
     lib.sylv_set_lapack_path.argtypes = [C.c_char_p]
     lib.sylv_version.restype = C.c_char_p
+    lib.sylv_host_projected.argtypes = [C.c_int32, C.c_int32, C.c_int32, P, C.c_int64, P, P]
+    lib.sylv_host_projected.restype = C.c_int
+    lib.sylv_host_sylvester.argtypes = [C.c_int32, C.c_int32, P, P, P, P]
+    lib.sylv_host_sylvester.restype = C.c_int
     for name in SYMBOLS[:11]:
         if name not in ("sylv_sketch_reset_stats",):
             getattr(lib, name).restype = C.c_int
@@ -283,6 +287,32 @@ def from_config(cfg, C1=None, C2=None, csr_pair=None, timing=False, stream=None,
     return SylvSketch(A, B, C1, C2, r=cfg.r, k=cfg.k, d_max=cfg.d_max, s=cfg.s, zeta=cfg.zeta,
                       seed_u=cfg.seed_u, seed_v=cfg.seed_v, tol=cfg.tol, timing=timing, stream=stream,
                       keep=keep, **kw)
+
+
+def host_projected(d: int, r: int, k: int, T: np.ndarray, H: np.ndarray) -> np.ndarray:
+    """Host a6 helper (no GPU): M = [T_d|T_H] H_und T_d^{-1}; T col-major (F-order) array."""
+    lib = load_library()
+    T = np.asfortranarray(T, dtype=np.float64)
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    M = np.zeros((d * r, d * r), order="F")
+    st = lib.sylv_host_projected(d, r, k, T.ctypes.data, T.shape[0], H.ctypes.data, M.ctypes.data)
+    if st != OK:
+        raise SylvError(st, "sylv_host_projected failed")
+    return M
+
+
+def host_sylvester(MU: np.ndarray, MV: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """Host a6 helper (no GPU): Y with MU Y + Y MV^T = E1 B E1^T."""
+    lib = load_library()
+    m, r = MU.shape[0], B.shape[0]
+    a = np.asfortranarray(MU, dtype=np.float64).copy(order="F")
+    b = np.asfortranarray(MV, dtype=np.float64).copy(order="F")
+    Bc = np.ascontiguousarray(B, dtype=np.float64)
+    Y = np.zeros((m, m), order="F")
+    st = lib.sylv_host_sylvester(m, r, a.ctypes.data, b.ctypes.data, Bc.ctypes.data, Y.ctypes.data)
+    if st != OK:
+        raise SylvError(st, "sylv_host_sylvester failed")
+    return Y
 
 
 def version() -> str:

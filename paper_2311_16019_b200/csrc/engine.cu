@@ -465,6 +465,28 @@ extern "C" {
 
 const char* sylv_version(void) { return SYLV_VERSION; }
 
+sylv_status sylv_host_projected(int32_t d, int32_t r, int32_t k, const double* T, int64_t ldT,
+                                const double* H, double* M) {
+  if (d < 1 || r < 1 || k < 1 || !T || !H || !M || ldT < (int64_t)(d + 1) * r) return SYLV_E_INVALID;
+  if (!lapack_loaded()) return SYLV_E_LAPACK;
+  std::vector<double> Mv;
+  build_projected(d, r, k, T, ldT, H, Mv);
+  std::memcpy(M, Mv.data(), Mv.size() * sizeof(double));
+  return SYLV_OK;
+}
+
+sylv_status sylv_host_sylvester(int32_t m, int32_t r, double* MU, double* MV, const double* B, double* Y) {
+  if (m < 1 || r < 1 || r > m || !MU || !MV || !B || !Y) return SYLV_E_INVALID;
+  if (!lapack_loaded()) return SYLV_E_LAPACK;
+  std::vector<double> a(MU, MU + (size_t)m * m), b(MV, MV + (size_t)m * m), y;
+  std::string err;
+  const int info = sylvester_bs(m, r, a, b, B, y, err);
+  if (info < 0) return SYLV_E_LAPACK;
+  if (info > 0) return SYLV_E_SINGULAR;
+  std::memcpy(Y, y.data(), y.size() * sizeof(double));
+  return SYLV_OK;
+}
+
 sylv_status sylv_set_lapack_path(const char* path) {
   std::string err;
   if (!path || !lapack_load(path, err)) {

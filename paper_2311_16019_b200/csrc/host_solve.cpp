@@ -186,7 +186,7 @@ int sylvester_bs(int m, int r, std::vector<double>& MU, std::vector<double>& MV,
   std::vector<double> Bc(r * r), tmp((size_t)r * m), F((size_t)m * m);
   for (int a = 0; a < r; ++a)
     for (int c = 0; c < r; ++c) Bc[c * r + a] = B[a * r + c];  // col-major
-  gemm('N', 'T', r, m, r, 1.0, Bc.data(), r, ZV.data(), m, 0.0, tmp.data(), r);   // B * ZV[0:r,:]
+  gemm('N', 'N', r, m, r, 1.0, Bc.data(), r, ZV.data(), m, 0.0, tmp.data(), r);   // B * ZV[0:r,:]
   gemm('T', 'N', m, m, r, 1.0, ZU.data(), m, tmp.data(), r, 0.0, F.data(), m);    // ZU[0:r,:]^T tmp
   // TU X + X TV^T = scale F
   const char ta = 'N', tb = 'T';
