@@ -44,6 +44,14 @@ def _setup(name, keep_basis=False):
     return cfg, csr, C1, C2, orc, gpu
 
 
+def _rho_close(rr, ro):
+    """1e-8 relative while rho_rel >= 1e-9 (three decades below tol = 1e-6); below that the
+    iteration has converged past the tolerance and rho is rounding noise: both must be tiny."""
+    if ro >= 1e-9:
+        return abs(rr - ro) <= 1e-8 * ro
+    return abs(rr - ro) <= 1e-12
+
+
 def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
@@ -63,14 +71,15 @@ def test_sketch_of_fixed_block(name):
 @pytest.mark.parametrize("name", list(CASES))
 def test_per_step_rho_and_small_matrices(name):
     cfg, csr, C1, C2, orc, gpu = _setup(name, keep_basis=True)
-    worst = 0.0
+    bad = []
     for d in range(1, 51):
         gpu.step(1)
         orc.step(1)
         _, rr = gpu.residual(d)
         ro = orc.residual(d).rho_rel
-        worst = max(worst, abs(rr - ro) / ro)
-    assert worst <= 1e-8, worst
+        if not _rho_close(rr, ro):
+            bad.append((d, rr, ro))
+    assert not bad, bad[:5]
     for which, seq in ((0, orc.U), (1, orc.V)):
         d = 12
         H, T, beta = gpu.get_small(which, d)
@@ -78,20 +87,31 @@ def test_per_step_rho_and_small_matrices(name):
         assert _rel(H, seq.Hbar(d)) <= 1e-9
         assert _rel(T, seq.T[:m + cfg.r, :m + cfg.r]) <= 1e-9
         assert _rel(beta, seq.beta) <= 1e-12
-        for j in range(51 - cfg.k + 1, 52):
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_window_blocks(name):
+    """The normalised window blocks U_j = Z_j R_j equal the oracle's Householder/MGS blocks
+    (before convergence: d = 5 for the fast-converging CSR cases, 15 otherwise)."""
+    cfg, csr, C1, C2, orc, gpu = _setup(name, keep_basis=True)
+    d = 5 if cfg.kind == "csr" else 15
+    gpu.step(d)
+    orc.step(d)
+    for which, seq in ((0, orc.U), (1, orc.V)):
+        for j in range(d + 2 - cfg.k, d + 2):
             Ug = gpu.get_block(which, j)
-            assert _rel(Ug, seq.U[j]) <= 1e-8, (which, j)
+            assert _rel(Ug, seq.U[j]) <= 1e-9, (which, j)
 
 
 @pytest.mark.parametrize("name", ["2d-r1", "csr-r2", "3d-r8k3"])
 def test_solution_and_true_residual(name):
     cfg, csr, C1, C2, orc, gpu = _setup(name)
-    d = 30
+    d = 6 if cfg.kind == "csr" else 30          # the banded CSR case converges in ~8 steps
     gpu.step(d)
     orc.step(d)
     res = orc.residual(d)
     _, rr = gpu.residual(d)
-    assert abs(rr - res.rho_rel) <= 1e-8 * res.rho_rel
+    assert res.rho_rel > 1e-9 and _rho_close(rr, res.rho_rel)
     X1o, X2o = orc.solution(d, res.Y)
     max_rank = X1o.shape[1] + 8
     X1, X2, rank = gpu.solution(d, max_rank)
@@ -162,9 +182,6 @@ def test_sketch_full_config_sizes(name):
     X = rng.standard_normal((cfg.n, cfg.r))
     Xd = torch.from_numpy(X).cuda()
     pkg = _pkg()
-    op = pkg.stencil_operator("stencil2d", 4, (0.0, 0.0))
-    op.n = cfg.n          # apply_sketch only needs n; a context of the right n and s
-    small = np.ones((cfg.n, cfg.r))
     # build a context with the config's sizes but a 1-step d_max (no stepping happens)
     if cfg.kind.startswith("stencil"):
         A = pkg.stencil_operator(cfg.kind, cfg.N, cfg.wA)
@@ -173,7 +190,6 @@ def test_sketch_full_config_sizes(name):
     C1 = torch.from_numpy(rng.standard_normal((cfg.n, cfg.r))).cuda()
     gpu = pkg.SylvSketch(A, A, C1, C1, r=cfg.r, k=cfg.k, d_max=2, s=cfg.s, seed_u=cfg.seed_u,
                          seed_v=cfg.seed_v)
-    del small
     for which, seed in ((0, cfg.seed_u), (1, cfg.seed_v)):
         got = gpu.apply_sketch(which, Xd)
         want = sparse_sign.apply_hashed(X, cfg.s, cfg.zeta, seed)
