@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""Benchmark: Krylov block steps/s of Alg. 1 (both sequences)
+on a BASELINE.json config, through the C ABI of libsylvsketch.so.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+One "step" = one block step d -> d+1 of BOTH Krylov sequences: SpMM + k-truncated block
+Gram-Schmidt + CholQR normalisation + hashed sparse-sign sketch + sketch-space QR update.
+The host projected solve (a6) and the second pass (a7) are timed separately (--ttt).
+Prints ONE JSON line (rank 0).  See DESIGN.md §Measurement for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-rel.residual 1e-6 (s); Krylov block-steps/s; HBM GB/s vs 8 TB/s peak"
+UNIT = "block-steps/s"
+NOMINAL_HBM_GBS = 8000.0
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _workload_desc(cfg):
+    if cfg.kind.startswith("stencil"):
+        dim = cfg.dim
+        return (f"{cfg.name}: {dim}-D convection-diffusion {cfg.N}^{dim} (n={cfg.n}), w_A={cfg.wA}, w_B={cfg.wB}, "
+                f"r={cfg.r}, k={cfg.k}, s={cfg.s}, zeta={cfg.zeta}, fp64")
+    return (f"{cfg.name}: banded random CSR n={cfg.n}, {cfg.csr_nnz_off}+1 nnz/row, band +-{cfg.csr_band}, "
+            f"r={cfg.r}, k={cfg.k}, s={cfg.s}, zeta={cfg.zeta}, fp64")
+
+
+def algorithmic_bytes(cfg):
+    """Per block step (both sequences): stencil B_n = 2*8*n*r*(2k+1);
+    CSR B_n = 2*[12 nnz + 4(n+1) + 8 n r (2k+3)].  Per launch: pass 1 reads k blocks,
+    pass 2 reads k blocks and writes 1 (stencil; CSR pass 1 also reads A and writes A Z,
+    pass 2 reads A Z)."""
+    n, r, k = cfg.n, cfg.r, cfg.k
+    blk = 8 * n * r
+    if cfg.kind == "csr":
+        nnz = n * (cfg.csr_nnz_off + 1)
+        mat = 12 * nnz + 4 * (n + 1)
+        p1 = mat + blk * (k + 1)          # A, Z_d gathers (counted once), k-1 other window blocks, write AZ
+        p2 = blk * (k + 1) + blk          # read AZ + k window blocks, write W'
+        return {"pass1": p1, "pass2": p2, "step": 2 * (p1 + p2)}
+    p1 = blk * k
+    p2 = blk * (k + 1)
+    return {"pass1": p1, "pass2": p2, "step": 2 * (p1 + p2)}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def traffic_for(cfg_name, kernel):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    v = d.get(cfg_name, {}).get(kernel)
+    return v
+
+
+def oracle_steps(cfg, nsteps, budget_s, warmup=0):
+    """The CPU oracle as it stands: setup (excluded), then up to `nsteps` block steps
+    (stops early once budget_s is exceeded).  Returns (steps, seconds, setup_s)."""
+    from oracle import alg1
+    from synth import inputs
+    t0 = time.perf_counter()
+    csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
+    C1, C2 = inputs.make_rhs(cfg)
+    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2, csr_pair=csr)
+    setup = time.perf_counter() - t0
+    for _ in range(warmup):
+        orc.step(1)
+    t0 = time.perf_counter()
+    done = 0
+    while done < nsteps:
+        orc.step(1)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    return done, time.perf_counter() - t0, setup
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import torch  # noqa: F401  (threads report only)
+    cores = os.cpu_count()
+    budget = float(os.environ.get("SYLV_REF_BUDGET_S", "150"))
+    steps, secs, setup = oracle_steps(cfg, args.steps, budget, warmup=0)
+    v = steps / secs
+    sample = (f"{steps} oracle block steps (both sequences) of {cfg.name} from d=1 after a {setup:.0f} s oracle setup "
+              f"(excluded); stops early after {budget:.0f} s (warm-up steps skipped: the oracle has no caches to warm)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": steps,
+            "warmup": 0, "requested_steps": args.steps, "ms_per_step": 1e3 * secs / steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": _workload_desc(cfg)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("SYLV_BENCH_CONFIG", "c3"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    from synth import inputs
+    cfg = inputs.get_config(args.config)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import numpy as np
+    import torch
+    import paper_2311_16019_b200 as pkg
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+
+    assert args.warmup >= 3 or os.environ.get("SYLV_ALLOW_SHORT_WARMUP"), "W >= 3 warm-up steps required"
+    if args.warmup + args.steps > cfg.d_max:
+        raise SystemExit(f"warmup+steps must be <= d_max={cfg.d_max}")
+
+    # ---- inputs (synthetic, seeded); replicas: each rank solves its own copy of the config
+    csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
+    C1, C2 = inputs.make_rhs(cfg)
+    C1d = torch.from_numpy(C1).to(dev)
+    C2d = torch.from_numpy(C2).to(dev)
+    solver = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, timing=True, stream=stream.cuda_stream)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    solver.step(args.warmup)
+    torch.cuda.synchronize()
+    solver.reset_stats()
+    l0 = solver.stats()["launches"]
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        d_done, st = solver.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    stats = solver.stats()
+    launches = stats["launches"] - l0
+    if ws > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    solver.close()
+    del C1d, C2d
+    torch.cuda.empty_cache()
+
+    value = ws * args.steps / (ms * 1e-3)
+    ab = algorithmic_bytes(cfg)
+    peak, peak_src = _peaks()
+    p2_ms = stats["ms_pass2"] / max(1, stats["n_pass2"])
+    p1_ms = stats["ms_pass1"] / max(1, stats["n_pass1"])
+    # dominant kernel = the slower of the two n-space passes
+    if p2_ms >= p1_ms:
+        dom, dom_ms, dom_bytes = "pass2", p2_ms, ab["pass2"]
+    else:
+        dom, dom_ms, dom_bytes = "pass1", p1_ms, ab["pass1"]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = traffic_for(cfg.name, dom)
+    step_gbs = ab["step"] / (ms / args.steps * 1e-3) / 1e9
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the region
+    e2e = None
+    if not args.no_e2e:
+        C1h = torch.from_numpy(C1).pin_memory()
+        C2h = torch.from_numpy(C2).pin_memory()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s2 = pkg.from_config(cfg, C1=C1h, C2=C2h, csr_pair=csr, stream=stream.cuda_stream)
+        s2.step(args.warmup + args.steps)
+        rho, rr = s2.residual(args.warmup + args.steps)          # D2H of the step's result (host solve)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        s2.close()
+        if ws > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        nst = args.warmup + args.steps
+        mirror = 2 * 8 * ((cfg.k + 1) * cfg.r ** 2 + cfg.r * ((nst // 2 + 1) * cfg.r + cfg.r))
+        e2e = {"value": ws * nst / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(2 * 8 * cfg.n * cfg.r / nst),
+               "d2h_bytes_per_step": int(mirror),
+               "region": f"init(host C1,C2 pinned; H2D) + {nst} steps + residual(d) host solve; wall clock, "
+                         f"max over ranks", "rho_rel": rr}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        budget = float(os.environ.get("SYLV_CPU_BUDGET_S", "30"))
+        steps_o, secs_o, setup_o = oracle_steps(cfg, 50, budget)
+        cpu = {"value": steps_o / secs_o, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"{steps_o} oracle block steps (both sequences) of {cfg.name} from d=1, "
+                         f"after {setup_o:.0f} s oracle setup (excluded); ~{budget:.0f} s budget"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": _workload_desc(cfg), "d_range": [args.warmup + 1, args.warmup + args.steps],
+                       "parallelism": ("replicas" if ws > 1 else "single GPU"),
+                       "l2": "inputs larger than L2 (window of k+1 blocks per sequence >> 126 MB)"
+                       if 8 * cfg.n * cfg.r * (cfg.k + 1) > 126e6 else "working set may be L2-resident"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
+                         "pass1_ms": p1_ms, "pass2_ms": p2_ms,
+                         "skqr_ms": stats["ms_skqr"] / max(1, stats["n_skqr"])},
+            "n_space_GBps": step_gbs, "n_space_frac_of_8TBps": step_gbs / NOMINAL_HBM_GBS,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

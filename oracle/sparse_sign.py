@@ -32,28 +32,27 @@ import math
 import numpy as np
 import scipy.sparse as sp
 
-_M32 = np.uint64(0xFFFFFFFF)
-
-
 def mix32(x: np.ndarray) -> np.ndarray:
-    """lowbias32 integer finaliser on uint32 values (computed in uint64, masked)."""
-    x = np.asarray(x, dtype=np.uint64) & _M32
-    x ^= x >> np.uint64(16)
-    x = (x * np.uint64(0x7FEB352D)) & _M32
-    x ^= x >> np.uint64(15)
-    x = (x * np.uint64(0x846CA68B)) & _M32
-    x ^= x >> np.uint64(16)
+    """lowbias32 integer finaliser on uint32 values (numpy uint32 arithmetic wraps mod 2^32)."""
+    x = np.asarray(x, dtype=np.uint32).copy()
+    x ^= x >> np.uint32(16)
+    x *= np.uint32(0x7FEB352D)
+    x ^= x >> np.uint32(15)
+    x *= np.uint32(0x846CA68B)
+    x ^= x >> np.uint32(16)
     return x
 
 
-def seed32(seed: int) -> np.uint64:
+def seed32(seed: int) -> np.uint32:
     seed = int(seed) & 0xFFFFFFFFFFFFFFFF
-    return np.uint64((seed ^ (seed >> 32)) & 0xFFFFFFFF)
+    return np.uint32((seed ^ (seed >> 32)) & 0xFFFFFFFF)
 
 
 def group_hash(m: np.ndarray, t: int, q: int, zeta: int, seed: int) -> np.ndarray:
-    key = ((np.asarray(m, dtype=np.uint64) * np.uint64(zeta) + np.uint64(t)) << np.uint64(2)) | np.uint64(q)
-    return mix32(mix32(key & _M32) ^ seed32(seed))
+    """G(m, t, q) = mix32(mix32(((m*zeta + t) << 2) | q) ^ seed32), uint32."""
+    m = np.asarray(m, dtype=np.uint32)
+    key = ((m * np.uint32(zeta) + np.uint32(t)) << np.uint32(2)) | np.uint32(q)
+    return mix32(mix32(key) ^ seed32(seed))
 
 
 def entries(j: np.ndarray, t: int, s: int, zeta: int, seed: int):
@@ -61,36 +60,38 @@ def entries(j: np.ndarray, t: int, s: int, zeta: int, seed: int):
     if s % zeta:
         raise ValueError("s must be a multiple of zeta")
     b = s // zeta
-    j = np.asarray(j, dtype=np.uint64)
-    m = j >> np.uint64(5)
-    lane = j & np.uint64(31)
-    g0 = group_hash(m, t, 0, zeta, seed)
-    g1 = group_hash(m, t, 1, zeta, seed)
-    g2 = group_hash(m, t, 2, zeta, seed)
-    base = (g0 * np.uint64(b)) >> np.uint64(32)
-    a = np.uint64(2) * (g1 & np.uint64(15)) + np.uint64(1)
-    c = (g1 >> np.uint64(4)) & np.uint64(31)
-    slot = (base + ((a * lane + c) & np.uint64(31))) % np.uint64(b)
-    row = np.uint64(t * b) + slot
-    neg = (g2 >> lane) & np.uint64(1)
+    j = np.asarray(j, dtype=np.int64)
+    if j.size == 0:
+        return np.zeros(0, dtype=np.int64), np.zeros(0)
+    m = j >> 5
+    lane = (j & 31).astype(np.uint32)
+    m0 = int(m.min())
+    groups = np.arange(m0, int(m.max()) + 1, dtype=np.int64)
+    gi = m - m0                                   # the three group hashes, once per 32-row group
+    g0 = group_hash(groups, t, 0, zeta, seed)[gi].astype(np.uint64)
+    g1 = group_hash(groups, t, 1, zeta, seed)[gi]
+    g2 = group_hash(groups, t, 2, zeta, seed)[gi]
+    base = ((g0 * np.uint64(b)) >> np.uint64(32)).astype(np.int64)
+    a = np.uint32(2) * (g1 & np.uint32(15)) + np.uint32(1)
+    c = (g1 >> np.uint32(4)) & np.uint32(31)
+    slot = (base + ((a * lane + c) & np.uint32(31)).astype(np.int64)) % b
+    row = t * b + slot
+    neg = (g2 >> lane) & np.uint32(1)
     val = np.where(neg == 1, -1.0, 1.0) / math.sqrt(zeta)
-    return row.astype(np.int64), val
+    return row, val
 
 
-def matrix(n: int, s: int, zeta: int, seed: int, chunk: int = 1 << 22) -> sp.csr_matrix:
-    """Materialise S as a scipy CSR matrix (s x n, n*zeta stored entries)."""
-    rows = np.empty(n * zeta, dtype=np.int64)
-    cols = np.empty(n * zeta, dtype=np.int64)
-    vals = np.empty(n * zeta, dtype=np.float64)
+def matrix(n: int, s: int, zeta: int, seed: int, chunk: int = 1 << 22) -> sp.csc_matrix:
+    """Materialise S as a scipy CSC matrix (s x n, exactly zeta stored entries per column,
+    row indices increasing because bucket t occupies rows [t*b, (t+1)*b))."""
+    rows = np.empty((n, zeta), dtype=np.int64)
+    vals = np.empty((n, zeta), dtype=np.float64)
     for j0 in range(0, n, chunk):
         j = np.arange(j0, min(n, j0 + chunk), dtype=np.int64)
         for t in range(zeta):
-            r_, v_ = entries(j, t, s, zeta, seed)
-            sl = slice(j0 * zeta + t * j.size, j0 * zeta + (t + 1) * j.size)
-            rows[sl], cols[sl], vals[sl] = r_, j, v_
-    S = sp.csr_matrix((vals, (rows, cols)), shape=(s, n))
-    S.sum_duplicates()
-    return S
+            rows[j0:j0 + j.size, t], vals[j0:j0 + j.size, t] = entries(j, t, s, zeta, seed)
+    indptr = np.arange(0, n * zeta + 1, zeta, dtype=np.int64)
+    return sp.csc_matrix((vals.reshape(-1), rows.reshape(-1), indptr), shape=(s, n))
 
 
 def apply(S: sp.spmatrix, X: np.ndarray) -> np.ndarray:

@@ -87,7 +87,7 @@ def test_group_slots_distinct():
 
 def test_uniform_rows_and_signs():
     n, s, zeta, seed = 320000, 8000, 8, 11
-    S = sparse_sign.matrix(n, s, zeta, seed)
+    S = sparse_sign.matrix(n, s, zeta, seed).tocsr()
     counts = np.diff(S.indptr)                       # nonzeros per sketch row
     expected = n * zeta / s
     b = s // zeta
