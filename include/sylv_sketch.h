@@ -96,7 +96,9 @@ typedef struct {
   double tol;            /* stop when rho_rel < tol (strict)                   */
   double rank_tol;       /* Y ~ Y1 Y2^T keeps sigma_i > rank_tol * sigma_1     */
   int32_t chunk;         /* second pass: blocks per X accumulation (0 = k+1)   */
-  int32_t flags;         /* bit 0: time the n-space passes with CUDA events    */
+  int32_t flags;         /* bit 0: time the n-space passes with CUDA events;
+                            bit 1: run both sequences on one stream (isolated
+                            kernel timings; default overlaps U and V on two streams) */
 } sylv_config;
 
 /* Create a context and run Alg. 1 line 1: U1 ell = C1, V1 ell' = C2

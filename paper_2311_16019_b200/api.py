@@ -159,10 +159,10 @@ class SylvSketch:
     def __init__(self, A: Operator, B: Operator, C1, C2, *, r: int, k: int, d_max: int, s: int,
                  zeta: int = 8, seed_u: int = 11, seed_v: int = 12, tol: float = 1e-6,
                  rank_tol: float = 1e-12, chunk: int = 0, timing: bool = False, stream=None,
-                 keep=None):
+                 keep=None, serial: bool = False):
         self.lib = load_library()
         self.cfg = Config(r=r, k=k, d_max=d_max, zeta=zeta, s=s, seed_u=seed_u, seed_v=seed_v, tol=tol,
-                          rank_tol=rank_tol, chunk=chunk, flags=1 if timing else 0)
+                          rank_tol=rank_tol, chunk=chunk, flags=(1 if timing else 0) | (2 if serial else 0))
         self.n, self.r, self.s = int(A.n), r, s
         self._keep = [A, B, keep]
         p1, k1 = _ptr(C1)

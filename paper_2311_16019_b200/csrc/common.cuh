@@ -57,6 +57,25 @@ __device__ __forceinline__ SkEntry sk_entry(const SketchParams& sp, uint32_t m, 
   return e;
 }
 
+// ---- fast 32-bit division by a runtime constant (round-up method, exact for all x) ----
+struct FastDiv {
+  uint32_t d, m, s;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;
+  f.s = s;
+  f.m = (uint32_t)((((1ull << s) - d) << 32) / d + 1);
+  return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
+  return (uint32_t)(((uint64_t)__umulhi(x, f.m) + x) >> f.s);
+}
+
 // ---- operator descriptors -----------------------------------------------------------
 enum OpKind : int { kStencil2D = 1, kStencil3D = 2, kCSR = 3 };
 
@@ -64,6 +83,7 @@ struct OpParams {
   int kind;
   int64_t n;
   int N;              // stencil grid size
+  FastDiv divN;       // division by N
   double cd;          // diagonal 2*dim*nu/h^2
   double cxm, cxp;    // x-1 / x+1 neighbour coefficients
   double cym, cyp;
@@ -72,42 +92,6 @@ struct OpParams {
   const int32_t* ci;
   const double* cv;
 };
-
-// Element (row, c) of A Z for a row-major n x R block Z.
-template <int R>
-__device__ __forceinline__ double op_apply(const OpParams& op, const double* __restrict__ Z,
-                                           int64_t row, int c) {
-  if (op.kind == kCSR) {
-    double v = 0.0;
-    const int64_t p1 = op.rp[row + 1];
-    for (int64_t p = op.rp[row]; p < p1; ++p)
-      v = fma(__ldg(op.cv + p), __ldg(Z + (int64_t)__ldg(op.ci + p) * R + c), v);
-    return v;
-  }
-  const uint32_t N = (uint32_t)op.N;
-  const uint32_t r32 = (uint32_t)row;
-  const uint32_t q1 = r32 / N;
-  const uint32_t x = r32 - q1 * N;
-  const double* z = Z + row * R + c;
-  double v = op.cd * z[0];
-  if (x > 0) v = fma(op.cxm, z[-R], v);
-  if (x + 1 < N) v = fma(op.cxp, z[R], v);
-  const int64_t sy = (int64_t)N * R;
-  if (op.kind == kStencil2D) {
-    const uint32_t y = q1;
-    if (y > 0) v = fma(op.cym, z[-sy], v);
-    if (y + 1 < N) v = fma(op.cyp, z[sy], v);
-  } else {
-    const uint32_t zq = q1 / N;
-    const uint32_t y = q1 - zq * N;
-    const int64_t sz = sy * N;
-    if (y > 0) v = fma(op.cym, z[-sy], v);
-    if (y + 1 < N) v = fma(op.cyp, z[sy], v);
-    if (zq > 0) v = fma(op.czm, z[-sz], v);
-    if (zq + 1 < N) v = fma(op.czp, z[sz], v);
-  }
-  return v;
-}
 
 // ---- tiny dense r x r helpers (row-major, one thread) ------------------------------
 template <int R>

@@ -71,6 +71,21 @@ T* dalloc(size_t count) {
     case 8: { constexpr int R_ = 8; __VA_ARGS__; } break; \
     default: break;                                       \
   }
+#define SYLV_DISPATCH_R124(Rv, ...)                                     \
+  switch (Rv) {                                                         \
+    case 1: { constexpr int R_ = 1; __VA_ARGS__; } break;               \
+    case 2: { constexpr int R_ = 2; __VA_ARGS__; } break;               \
+    case 4: { constexpr int R_ = 4; __VA_ARGS__; } break;               \
+    default: break;                                                     \
+  }
+#define SYLV_DISPATCH_R124_K(Rv, Kv, ...)                               \
+  SYLV_DISPATCH_R124(Rv, switch (Kv) {                                  \
+    case 1: { constexpr int K_ = 1; __VA_ARGS__; } break;               \
+    case 2: { constexpr int K_ = 2; __VA_ARGS__; } break;               \
+    case 3: { constexpr int K_ = 3; __VA_ARGS__; } break;               \
+    case 4: { constexpr int K_ = 4; __VA_ARGS__; } break;               \
+    default: break;                                                     \
+  })
 #define SYLV_DISPATCH_RK(Rv, Kv, ...)                                   \
   SYLV_DISPATCH_R(Rv, switch (Kv) {                                     \
     case 1: { constexpr int K_ = 1; __VA_ARGS__; } break;               \
@@ -90,14 +105,15 @@ struct TimedPair {
 struct Sequence {
   int which = 0;
   int R = 1, K = 1, dmax = 0;
-  int64_t n = 0, s = 0, ldT = 0;
+  int64_t n = 0, s = 0, ldT = 0, ld = 0;   // ld: SoA column stride (n rounded up to 64)
   OpParams op{};
   SketchParams sp{};
   // device
-  double* ring = nullptr;     // (K+1) n x R
-  double* Cdev = nullptr;     // n x R
-  double* Yt = nullptr;       // CSR: A Z_d (n x R)
-  double* sk = nullptr;       // s x R
+  double* ring = nullptr;     // (K+1) blocks, SoA R x ld
+  double* Cdev = nullptr;     // SoA R x ld
+  double* Yt = nullptr;       // CSR: A Z_d (SoA)
+  double* sk = nullptr;       // s x R (row-major)
+  double* skpart = nullptr;   // nchunk x R x s sketch partials
   double* w = nullptr;        // s x R
   double* w2 = nullptr;       // s x R
   double* Q = nullptr;        // s x ldT (col-major)
@@ -125,7 +141,7 @@ struct Sequence {
   double beta[kMaxR * kMaxR];
   double ell[kMaxR * kMaxR];
 
-  double* slot(int j) const { return ring + (int64_t)(j % (K + 1)) * n * R; }
+  double* slot(int j) const { return ring + (int64_t)(j % (K + 1)) * ld * R; }
 };
 
 struct sylv_ctx {
@@ -139,6 +155,11 @@ struct sylv_ctx {
   int RT = 1;         // row tiles of Q^T w
   int64_t tileQ = 0;
   int CC = 1;         // column chunks of Q c
+  int nchunk = 1;     // row chunks of the sketch kernel (grid nchunk x R)
+  int64_t gpc = 32;   // 32-row groups per sketch chunk
+  size_t sk_smem = 0; // dynamic shared memory of the sketch kernel
+  cudaStream_t st2 = nullptr;  // second stream: the V sequence runs concurrently with U
+  cudaEvent_t fork = nullptr, join = nullptr;
   Sequence seq[2];
   int d_done = 0;
   bool broken = false;
@@ -189,6 +210,7 @@ OpParams make_op(const sylv_operator* A, bool transpose) {
     const int dim = (A->kind == SYLV_OP_STENCIL2D) ? 2 : 3;
     const int N = A->grid[0];
     op.N = N;
+    op.divN = make_fastdiv((uint32_t)N);
     const double h = 1.0 / (N + 1);
     const double nu = A->nu;
     const double sg = transpose ? -1.0 : 1.0;  // B^T = stencil with -w (R16)
@@ -251,7 +273,7 @@ void upload_csr(Sequence& q, const sylv_operator* A, bool transpose, cudaStream_
 }
 
 void free_seq(Sequence& q) {
-  double* dp[] = {q.ring, q.Cdev, q.Yt, q.sk, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
+  double* dp[] = {q.ring, q.Cdev, q.Yt, q.sk, q.skpart, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
                   q.part1, q.part2, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv};
   for (double* p : dp)
     if (p) cudaFree(p);
@@ -267,22 +289,68 @@ void free_seq(Sequence& q) {
 
 // CholQR2 of the s x R block `in` (destroyed): q written to Q[:, col0:col0+R]
 // (column-major), R-factor tau (positive diagonal) to `tau_out` (device, R x R).
-void cholqr2(sylv_ctx* c, Sequence& q, double* in, int64_t col0, double* tau_out, int flag_slot) {
+void cholqr2(sylv_ctx* c, Sequence& q, double* in, int64_t col0, double* tau_out, int flag_slot,
+             cudaStream_t st) {
   const int R = c->R;
   const int gs = (int)std::min<int64_t>(c->G, (q.s + 255) / 256);
   double* ta = q.small;            // R^2
   double* tai = q.small + 64;      // R^2
   double* tbi = q.small + 128;     // R^2
   SYLV_DISPATCH_R(R, {
-    k_sketch_gram<R_><<<gs, kThreads, 0, c->st>>>(q.s, in, q.sp, nullptr, q.part2);
-    k_chol_small<R_><<<1, 64, 0, c->st>>>(q.part2, gs, ta, tai, nullptr, q.flags, flag_slot);
-    k_rmul<R_><<<gs, kThreads, 0, c->st>>>(q.s, in, tai, q.w2, 0);
-    k_sketch_gram<R_><<<gs, kThreads, 0, c->st>>>(q.s, q.w2, q.sp, nullptr, q.part2);
-    k_chol_small<R_><<<1, 64, 0, c->st>>>(q.part2, gs, tau_out, tbi, ta, q.flags, flag_slot);
-    k_rmul<R_><<<gs, kThreads, 0, c->st>>>(q.s, q.w2, tbi, q.Q + col0 * q.s, q.s);
+    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, in, q.part2);
+    k_chol_small<R_><<<1, 64, 0, st>>>(q.part2, gs, ta, tai, nullptr, q.flags, flag_slot);
+    k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, in, tai, q.w2, 0);
+    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, q.w2, q.part2);
+    k_chol_small<R_><<<1, 64, 0, st>>>(q.part2, gs, tau_out, tbi, ta, q.flags, flag_slot);
+    k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, q.w2, tbi, q.Q + col0 * q.s, q.s);
   });
   count(c, 6);
   CK(cudaGetLastError());
+}
+
+// n-space pass launchers (R <= 4: thread-per-row FMA kernels; R = 8: DMMA warp tiles)
+void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, cudaStream_t st) {
+  const int R = c->R, K = c->K;
+  if (R == 8) {
+    switch (K) {
+      case 1: k_pass1_r8<1><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); break;
+      case 2: k_pass1_r8<2><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); break;
+      case 3: k_pass1_r8<3><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); break;
+      case 4: k_pass1_r8<4><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); break;
+    }
+  } else {
+    SYLV_DISPATCH_R124_K(R, K, { k_pass1_rows<R_, K_><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); });
+  }
+  count(c);
+}
+
+template <bool GRAM>
+void launch_pass2(sylv_ctx* c, Sequence& q, const Win& win, int nwin, const double* Yt, const double* coef,
+                  double* out, cudaStream_t st) {
+  const int R = c->R, K = c->K;
+  if (R == 8) {
+    switch (K) {
+      case 1: k_pass2_r8<1, GRAM><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, Yt, coef, out, q.part2); break;
+      case 2: k_pass2_r8<2, GRAM><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, Yt, coef, out, q.part2); break;
+      case 3: k_pass2_r8<3, GRAM><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, Yt, coef, out, q.part2); break;
+      case 4: k_pass2_r8<4, GRAM><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, Yt, coef, out, q.part2); break;
+    }
+  } else {
+    SYLV_DISPATCH_R124_K(R, K, {
+      k_pass2_rows<R_, K_, GRAM><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, Yt, coef, out, q.part2);
+    });
+  }
+  count(c);
+}
+
+// S X for an SoA block -> w (s x R row-major) = (S X) M  (M = nullptr: identity)
+void launch_sketch(sylv_ctx* c, Sequence& q, const double* X, int R, const double* M, double* w, cudaStream_t st) {
+  const dim3 g(c->nchunk, R);
+  SYLV_DISPATCH_R(R, {
+    k_sketch_cols<R_><<<g, kThreads, c->sk_smem, st>>>(c->n, X, q.ld, q.sp, c->gpc, q.skpart);
+    k_sketch_reduce<R_><<<(int)std::min<int64_t>(4 * c->sm, (q.s + 255) / 256), 256, 0, st>>>(q.skpart, c->nchunk, q.s, M, w);
+  });
+  count(c, 2);
 }
 
 void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, bool transpose,
@@ -293,6 +361,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.dmax = c->dmax;
   q.n = c->n;
   q.s = c->s;
+  q.ld = (c->n + 63) / 64 * 64;
   q.ldT = (int64_t)(c->dmax + 1) * c->R;
   q.op = make_op(A, transpose);
   q.sp.seed = (uint32_t)(seed ^ (seed >> 32));
@@ -300,13 +369,14 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.sp.b = (uint32_t)(c->s / c->zeta);
   q.sp.scale = 1.0 / std::sqrt((double)c->zeta);
   const int R = c->R, K = c->K;
-  const int64_t nR = c->n * R, sR = c->s * R, ldT = q.ldT;
+  const int64_t blk = q.ld * R, sR = c->s * R, ldT = q.ldT;
   if (A->kind == SYLV_OP_CSR) upload_csr(q, A, transpose, c->st);
 
-  q.ring = dalloc<double>((size_t)(K + 1) * nR);
-  q.Cdev = dalloc<double>(nR);
-  if (A->kind == SYLV_OP_CSR) q.Yt = dalloc<double>(nR);
+  q.ring = dalloc<double>((size_t)(K + 1) * blk);
+  q.Cdev = dalloc<double>(blk);
+  if (A->kind == SYLV_OP_CSR) q.Yt = dalloc<double>(blk);
   q.sk = dalloc<double>(sR);
+  q.skpart = dalloc<double>((size_t)c->nchunk * sR);
   q.w = dalloc<double>(sR);
   q.w2 = dalloc<double>(sR);
   q.Q = dalloc<double>((size_t)c->s * ldT);
@@ -323,6 +393,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.c2 = dalloc<double>(ldT * R);
   q.qcpart = dalloc<double>((size_t)c->CC * sR);
   q.small = dalloc<double>(512);
+  CK(cudaMemsetAsync(q.ring, 0, (size_t)(K + 1) * blk * sizeof(double), c->st));
   CK(cudaMemsetAsync(q.Tdev, 0, (size_t)ldT * ldT * sizeof(double), c->st));
   CK(cudaMemsetAsync(q.flags, 0, (c->dmax + 2) * sizeof(int), c->st));
   CK(cudaMemsetAsync(q.Hc, 0, (size_t)(c->dmax + 1) * (K + 1) * R * R * sizeof(double), c->st));
@@ -333,21 +404,31 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   std::memset(q.Th, 0, (size_t)ldT * ldT * sizeof(double));
   std::memset(q.Hh, 0, (size_t)(c->dmax + 1) * (K + 1) * R * R * sizeof(double));
 
-  // C -> Cdev and Z_1 (ring slot 1)
-  CK(cudaMemcpyAsync(q.Cdev, C, nR * sizeof(double), cudaMemcpyDefault, c->st));
-  CK(cudaMemcpyAsync(q.slot(1), q.Cdev, nR * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  // C (row-major, host or device) -> Cdev (SoA) and Z_1 (ring slot 1)
+  {
+    const bool dev = is_device_ptr(C);
+    double* tmp = dalloc<double>((size_t)c->n * R);
+    CK(cudaMemcpyAsync(tmp, C, (size_t)c->n * R * sizeof(double), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(q.Cdev, 0, blk * sizeof(double), c->st));
+    SYLV_DISPATCH_R(R, { k_to_soa<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, tmp, q.Cdev, q.ld); });
+    count(c);
+    CK(cudaMemcpyAsync(q.slot(1), q.Cdev, blk * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    cudaFree(tmp);
+  }
   // Alg. 1 line 1: ell = chol(C^T C) (U_1 ell = C), S C -> CholQR2 -> beta, Q_1
-  CK(cudaMemsetAsync(q.sk, 0, sR * sizeof(double), c->st));
   double* ell_d = q.small + 192;
   double* elli_d = q.small + 256;
   double* beta_d = q.small + 320;
   SYLV_DISPATCH_R(R, {
-    k_sketch_gram<R_><<<c->G, kThreads, 0, c->st>>>(c->n, q.Cdev, q.sp, q.sk, q.part2);
+    k_gram_soa<R_><<<c->G, kThreads, 0, c->st>>>(c->n, q.Cdev, q.ld, q.part2);
     k_chol_small<R_><<<1, 64, 0, c->st>>>(q.part2, c->G, ell_d, elli_d, nullptr, q.flags, 0);
   });
   count(c, 2);
   CK(cudaGetLastError());
-  cholqr2(c, q, q.sk, 0, beta_d, 0);
+  launch_sketch(c, q, q.Cdev, R, nullptr, q.sk, c->st);
+  CK(cudaGetLastError());
+  cholqr2(c, q, q.sk, 0, beta_d, 0, c->st);
   SYLV_DISPATCH_R(R, { k_init_tau<R_><<<1, 1, 0, c->st>>>(beta_d, ell_d, q.Tdev, ldT, q.Rall + R * R); });
   count(c);
   CK(cudaGetLastError());
@@ -360,43 +441,36 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   if (q.flags_h[0]) throw Status{SYLV_E_INVALID, "C1 or C2 (or its sketch) is rank deficient"};
 }
 
-// One block step j (1-based) of one sequence: Alg. 1 lines 3-9.
-void step_sequence(sylv_ctx* c, Sequence& q, int j) {
+// One block step j (1-based) of one sequence on stream st: Alg. 1 lines 3-9.
+void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
   const int R = c->R, K = c->K;
   const int nwin = std::min(K, j);
   Win win{};
   for (int i = 0; i < nwin; ++i) win.p[i] = q.slot(j - nwin + 1 + i);
   const bool timing = (c->cflags & 1) != 0;
-  cudaStream_t st = c->st;
   const int G = c->G;
   TimedPair t1{}, t2{}, t3{};
   // ---- a1 + a2 coefficients: pass 1
   if (timing) { t1 = ev_get(c, 0); CK(cudaEventRecord(t1.a, st)); }
-  SYLV_DISPATCH_RK(R, K, {
-    k_pass1<R_, K_><<<G, kThreads, 0, st>>>(q.op, win, nwin, q.Yt, q.part1);
-  });
+  launch_pass1(c, q, win, nwin, st);
   if (timing) { CK(cudaEventRecord(t1.b, st)); c->timed.push_back(t1); }
   SYLV_DISPATCH_RK(R, K, {
     k_coef1<R_, K_><<<1, kThreads, 0, st>>>(q.part1, G, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
   });
-  CK(cudaMemsetAsync(q.sk, 0, q.s * R * sizeof(double), st));
-  // ---- a2 update + a3 Gram + a4 sketch: pass 2
+  // ---- a2 update + a3 Gram: pass 2 (writes Z_{j+1} = W')
   if (timing) { t2 = ev_get(c, 1); CK(cudaEventRecord(t2.a, st)); }
-  SYLV_DISPATCH_RK(R, K, {
-    k_pass2<R_, K_, true><<<G, kThreads, 0, st>>>(q.op, win, nwin, q.Yt,
-                                                   q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1),
-                                                   q.part2, q.sp, q.sk);
-  });
+  launch_pass2<true>(c, q, win, nwin, q.Yt, q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1), st);
   if (timing) { CK(cudaEventRecord(t2.b, st)); c->timed.push_back(t2); }
   SYLV_DISPATCH_RK(R, K, {
     k_coef2<R_, K_><<<1, kThreads, 0, st>>>(q.part2, G, j, q.Rall, q.Hc, q.hn2, q.flags);
   });
-  count(c, 4);
+  count(c, 2);
   CK(cudaGetLastError());
-  // ---- a5: w = (S W') R_{j+1}; block CGS2 against Q (m = j R columns); CholQR2; T column
+  // ---- a4: w = (S W') R_{j+1}   (a5 timing includes the sketch)
   if (timing) { t3 = ev_get(c, 2); CK(cudaEventRecord(t3.a, st)); }
+  launch_sketch(c, q, q.slot(j + 1), R, q.Rall + (int64_t)(j + 1) * R * R, q.w, st);
+  // ---- a5: block CGS2 against Q (m = j R columns); CholQR2; T column
   const int m = j * R;
-  const int gs = (int)std::min<int64_t>(G, (q.s + 255) / 256);
   const dim3 gq((m + kWarps - 1) / kWarps, c->RT);
   const int cols_per_chunk = (m + c->CC - 1) / c->CC;
   const int ncc = (m + cols_per_chunk - 1) / cols_per_chunk;
@@ -405,7 +479,6 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j) {
   const int gr = (int)std::min<int64_t>(1024, (mR + 255) / 256);
   const int gw = (int)std::min<int64_t>(1024, (q.s * R + 255) / 256);
   SYLV_DISPATCH_R(R, {
-    k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, q.sk, q.Rall + (int64_t)(j + 1) * R * R, q.w, 0);
     // pass A: c1 = Q^T w
     k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, q.s, m, q.w, c->tileQ, q.cpart);
     k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.csum, nullptr);
@@ -418,10 +491,10 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j) {
     k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, q.s, m, q.c2, cols_per_chunk, q.qcpart);
     k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, q.s * R);
   });
-  count(c, 9);
+  count(c, 8);
   CK(cudaGetLastError());
   double* tau_d = q.small + 384;
-  cholqr2(c, q, q.w, m, tau_d, j + 1);
+  cholqr2(c, q, q.w, m, tau_d, j + 1, st);
   SYLV_DISPATCH_R(R, {
     k_tcol<R_><<<std::max(1, (int)std::min<int64_t>(256, ((int64_t)(m + R) * R + 255) / 256)), 256, 0, st>>>(
         q.csum, tau_d, q.Tdev, q.ldT, m);
@@ -501,7 +574,11 @@ const char* sylv_sketch_last_error(const sylv_ctx* ctx) { return ctx ? ctx->err.
 void sylv_sketch_destroy(sylv_ctx* ctx) {
   if (!ctx) return;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
+  if (ctx->st2) cudaStreamSynchronize(ctx->st2);
   for (auto& q : ctx->seq) free_seq(q);
+  if (ctx->st2) cudaStreamDestroy(ctx->st2);
+  if (ctx->fork) cudaEventDestroy(ctx->fork);
+  if (ctx->join) cudaEventDestroy(ctx->join);
   for (auto& p : ctx->free_events) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto& p : ctx->timed) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   delete ctx;
@@ -556,6 +633,25 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     c->RT = (int)std::max<int64_t>(1, std::min<int64_t>(64, c->s / 512));
     c->tileQ = (c->s + c->RT - 1) / c->RT;
     c->CC = (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * c->sm + (c->s / 256)) / std::max<int64_t>(1, c->s / 256)));
+    // sketch kernel: whole sketch column (s doubles) in shared memory per CTA
+    c->sk_smem = (size_t)c->s * sizeof(double);
+    int max_optin = 0;
+    CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (c->sk_smem > (size_t)max_optin)
+      throw Status{SYLV_E_INVALID, "s too large: the sketch column (8 s bytes) must fit in shared memory"};
+    SYLV_DISPATCH_R(r, {
+      CK(cudaFuncSetAttribute(k_sketch_cols<R_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sk_smem));
+    });
+    int smem_sm = 0;
+    CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    const int per_sm = std::max(1, (int)(smem_sm / (c->sk_smem + 1024)));
+    const int64_t ngroups = (c->n + 31) / 32;
+    c->nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(ngroups, (int64_t)c->sm * per_sm / r));
+    c->gpc = (ngroups + c->nchunk - 1) / c->nchunk;
+    c->nchunk = (int)((ngroups + c->gpc - 1) / c->gpc);
+    CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
     init_sequence(c, c->seq[0], 0, A, false, C1, cfg->seed_u);
     init_sequence(c, c->seq[1], 1, B, true, C2, cfg->seed_v);
     return SYLV_OK;
@@ -569,14 +665,22 @@ sylv_status sylv_sketch_step(sylv_ctx* c, int32_t nsteps, int32_t* d_done) {
   return guard(c, [&]() -> sylv_status {
     const int first = c->d_done + 1;
     const int last = std::min(c->dmax, c->d_done + std::max(0, nsteps));
-    for (int j = first; j <= last; ++j) {
-      step_sequence(c, c->seq[0], j);
-      step_sequence(c, c->seq[1], j);
+    if (last >= first) {
+      // U on the context stream, V on st2 (independent sequences; their kernels overlap)
+      CK(cudaEventRecord(c->fork, c->st));
+      CK(cudaStreamWaitEvent(c->st2, c->fork, 0));
+      for (int j = first; j <= last; ++j) {
+        step_sequence(c, c->seq[0], j, c->st);
+        step_sequence(c, c->seq[1], j, (c->cflags & 2) ? c->st : c->st2);
+      }
+      CK(cudaMemcpyAsync(c->seq[1].flags_h + first, c->seq[1].flags + first, (last - first + 2) * sizeof(int),
+                         cudaMemcpyDeviceToHost, c->st2));
+      CK(cudaEventRecord(c->join, c->st2));
+      CK(cudaStreamWaitEvent(c->st, c->join, 0));
     }
     if (last >= first) {
-      for (auto& q : c->seq)
-        CK(cudaMemcpyAsync(q.flags_h + first, q.flags + first, (last - first + 2) * sizeof(int),
-                           cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(c->seq[0].flags_h + first, c->seq[0].flags + first, (last - first + 2) * sizeof(int),
+                         cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
       ev_collect(c);
       for (int j = first; j <= last; ++j) {
@@ -705,10 +809,10 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
       CK(cudaMemsetAsync(Xd, 0, (size_t)c->n * ldx * sizeof(double), c->st));
       if (l > 0) {
         double* Md = dalloc<double>(M.size());
-        double* rbuf = dalloc<double>((size_t)(K + C) * c->n * r);
+        double* rbuf = dalloc<double>((size_t)(K + C) * q.ld * r);
         CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
-        auto rslot = [&](int j) { return rbuf + (int64_t)(j % (K + C)) * c->n * r; };
-        CK(cudaMemcpyAsync(rslot(1), q.Cdev, (size_t)c->n * r * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+        auto rslot = [&](int j) { return rbuf + (int64_t)(j % (K + C)) * q.ld * r; };
+        CK(cudaMemcpyAsync(rslot(1), q.Cdev, (size_t)q.ld * r * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
         int j0 = 1;
         for (int j = 1; j <= d; ++j) {
           if (j >= 2) {  // Z_j from Z_{j-nwin..j-1} with the stored pass-2 coefficients of step j-1
@@ -716,12 +820,7 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
             const int nwin = std::min(K, jp);
             Win win{};
             for (int i = 0; i < nwin; ++i) win.p[i] = rslot(jp - nwin + 1 + i);
-            SYLV_DISPATCH_RK(r, K, {
-              k_pass2<R_, K_, false><<<c->G, kThreads, 0, c->st>>>(q.op, win, nwin, nullptr,
-                                                                   q.Kc + (int64_t)jp * (1 + K) * r * r,
-                                                                   rslot(j), nullptr, q.sp, nullptr);
-            });
-            count(c);
+            launch_pass2<false>(c, q, win, nwin, nullptr, q.Kc + (int64_t)jp * (1 + K) * r * r, rslot(j), c->st);
           }
           if (j - j0 + 1 == C || j == d) {
             ChunkPtrs cp{};
@@ -729,7 +828,7 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
             const int64_t tot = c->n * (int64_t)l;
             const int gx = (int)std::min<int64_t>((int64_t)c->sm * 8, (tot + 255) / 256);
             SYLV_DISPATCH_R(r, {
-              k_xacc<R_><<<gx, kThreads, 0, c->st>>>(c->n, cp, j - j0 + 1, Md + (int64_t)(j0 - 1) * r * l, l, Xd, ldx);
+              k_xacc<R_><<<gx, kThreads, 0, c->st>>>(c->n, cp, j - j0 + 1, q.ld, Md + (int64_t)(j0 - 1) * r * l, l, Xd, ldx);
             });
             count(c);
             j0 = j + 1;
@@ -823,25 +922,35 @@ sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X
   return guard(c, [&]() -> sylv_status {
     Sequence& q = c->seq[which];
     const bool xin = is_device_ptr(X), yout = is_device_ptr(Yout);
-    const double* Xd = X;
-    double* Xtmp = nullptr;
-    if (!xin) {
-      Xtmp = dalloc<double>((size_t)c->n * r);
-      CK(cudaMemcpyAsync(Xtmp, X, (size_t)c->n * r * sizeof(double), cudaMemcpyHostToDevice, c->st));
-      Xd = Xtmp;
-    }
-    double* Yd = yout ? Yout : dalloc<double>((size_t)c->s * r);
-    CK(cudaMemsetAsync(Yd, 0, (size_t)c->s * r * sizeof(double), c->st));
-    const int64_t rows_per_cta = (int64_t)kWarps * (32 / r);
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sm * 4, (c->n + rows_per_cta - 1) / rows_per_cta));
-    SYLV_DISPATCH_R(r, { k_sketch_gram<R_><<<g, kThreads, 0, c->st>>>(c->n, Xd, q.sp, Yd, nullptr); });
+    double* Xtmp = dalloc<double>((size_t)c->n * r);
+    double* Xs = dalloc<double>((size_t)q.ld * r);
+    CK(cudaMemcpyAsync(Xtmp, X, (size_t)c->n * r * sizeof(double), xin ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(Xs, 0, (size_t)q.ld * r * sizeof(double), c->st));
+    SYLV_DISPATCH_R(r, { k_to_soa<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, Xtmp, Xs, q.ld); });
     count(c);
+    double* Yd = yout ? Yout : dalloc<double>((size_t)c->s * r);
+    if (r != c->R) {
+      // the sketch kernel's shared memory attribute is set for R = c->R at init
+      SYLV_DISPATCH_R(r, {
+        CK(cudaFuncSetAttribute(k_sketch_cols<R_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sk_smem));
+      });
+    }
+    // partials buffer is sized for nchunk x R x s; r <= R fits, larger r needs a temporary
+    double* saved = q.skpart;
+    if (r > c->R) q.skpart = dalloc<double>((size_t)c->nchunk * c->s * r);
+    launch_sketch(c, q, Xs, r, nullptr, Yd, c->st);
     CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->st));
+    if (q.skpart != saved) {
+      cudaFree(q.skpart);
+      q.skpart = saved;
+    }
+    cudaFree(Xtmp);
+    cudaFree(Xs);
     if (!yout) {
       CK(cudaMemcpyAsync(Yout, Yd, (size_t)c->s * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     }
     CK(cudaStreamSynchronize(c->st));
-    if (Xtmp) cudaFree(Xtmp);
     if (!yout) cudaFree(Yd);
     return SYLV_OK;
   });
@@ -881,7 +990,7 @@ sylv_status sylv_sketch_get_block(sylv_ctx* c, int32_t which, int32_t j, double*
     const int r = c->R;
     const bool dev = is_device_ptr(out);
     double* od = dev ? out : dalloc<double>((size_t)c->n * r);
-    SYLV_DISPATCH_R(r, { k_zr<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, q.slot(j), q.Rall + (int64_t)j * r * r, od); });
+    SYLV_DISPATCH_R(r, { k_soa_mul_rowmajor<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, q.slot(j), q.ld, q.Rall + (int64_t)j * r * r, od); });
     count(c);
     CK(cudaGetLastError());
     if (!dev) CK(cudaMemcpyAsync(out, od, (size_t)c->n * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));

@@ -7,219 +7,553 @@
 //   pass 1  Yt = A Z_d (a1, on the fly),  P_i = Z_i^T Yt  for the k window blocks
 //           -> h_{i,d} = U_i^T W~ = R_i^T P_i R_d            (a2 coefficients, CGS)
 //   pass 2  W' = Yt R_d - sum_i Z_i (R_i h_{i,d})  = W~ - sum_i U_i h_{i,d}  (a2 update)
-//           written as Z_{d+1};  G = W'^T W' (a3 Gram);  S W' scattered (a4)
-//           -> h_{d+1,d} = chol(G),  R_{d+1} = h_{d+1,d}^{-1},  S U_{d+1} = (S W') R_{d+1}
+//           written as Z_{d+1};  G = W'^T W' (a3 Gram)
+//           -> h_{d+1,d} = chol(G),  R_{d+1} = h_{d+1,d}^{-1}
+//   sketch  S W' with the hashed sparse-sign S (a4), shared-memory privatised per column
+//           -> S U_{d+1} = (S W') R_{d+1}
 //
-// CGS over the k-window equals the paper's MGS in exact arithmetic because the
-// window blocks are mutually orthonormal (R5).  Blocks are row-major n x R
-// ("row-interleaved": the R values of one grid row are contiguous).
+// CGS over the k-window equals the paper's MGS in exact arithmetic because the window
+// blocks are mutually orthonormal (R5).
+//
+// Layout ("SoA"): an n x R block is R columns of length ld (ld = n rounded up to 64),
+// element (row, c) at X[c*ld + row].  Warps read 32/64-byte column segments, so every
+// 32-byte sector fetched is fully used for any R.
+//
+// r = 8 uses the fp64 tensor-core MMA (mma.sync.m8n8k4.f64, DMMA) for the block inner
+// products, the block update and the Gram: one instruction per 256 FMAs and 2 accumulator
+// registers per lane per r x r product.  r <= 4 uses one thread per row with FMAs.
 #pragma once
 #include "common.cuh"
 
 namespace sylv {
 
 struct Win {
-  const double* p[kMaxK];  // window blocks Z_{d-nwin+1..d}, oldest first
+  const double* p[kMaxK];  // window blocks Z_{d-nwin+1..d}, oldest first (Z_d = p[nwin-1])
 };
 
-// Reduce acc (per-lane column c = lane % R) over the lanes of a warp with equal c.
-template <int R>
-__device__ __forceinline__ double warp_sum_same_col(double v) {
-#pragma unroll
-  for (int off = R; off < 32; off <<= 1) v += __shfl_xor_sync(SYLV_FULL_MASK, v, off);
+// D(8x8) += A(8x4) B(4x8), fp64; fragments per PTX ISA m8n8k4 .f64:
+// A: lane holds A[lane>>2][lane&3]; B: B[lane&3][lane>>2]; D: D[lane>>2][2*(lane&3)+{0,1}].
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Stencil grid coordinates of `row` (x fastest).
+struct Coord {
+  uint32_t x, y, z;
+};
+__device__ __forceinline__ Coord coords(const OpParams& op, uint32_t row) {
+  Coord c;
+  const uint32_t q1 = fdiv(row, op.divN);
+  c.x = row - q1 * (uint32_t)op.N;
+  if (op.kind == kStencil2D) {
+    c.y = q1;
+    c.z = 0;
+  } else {
+    c.z = fdiv(q1, op.divN);
+    c.y = q1 - c.z * (uint32_t)op.N;
+  }
+  return c;
+}
+
+// (A Z)[row] for one SoA column `z` (= Z + c*ld).  `center` returns z[row].
+__device__ __forceinline__ double stencil_col(const OpParams& op, const double* __restrict__ z,
+                                              uint32_t row, const Coord& q, double& center) {
+  const uint32_t N = (uint32_t)op.N;
+  const double* p = z + row;
+  center = __ldg(p);
+  double v = op.cd * center;
+  if (q.x > 0) v = fma(op.cxm, __ldg(p - 1), v);
+  if (q.x + 1 < N) v = fma(op.cxp, __ldg(p + 1), v);
+  if (q.y > 0) v = fma(op.cym, __ldg(p - N), v);
+  if (q.y + 1 < N) v = fma(op.cyp, __ldg(p + N), v);
+  if (op.kind == kStencil3D) {
+    const uint32_t NN = N * N;
+    if (q.z > 0) v = fma(op.czm, __ldg(p - NN), v);
+    if (q.z + 1 < N) v = fma(op.czp, __ldg(p + NN), v);
+  }
   return v;
 }
 
-// ---------------------------------------------------------------------------------
-// pass 1: Yt = A Z_d,  partial[blk][(i*R + a)*R + c] = sum_rows Z_i[row,a] Yt[row,c]
-// ---------------------------------------------------------------------------------
-template <int R, int K>
-__global__ void __launch_bounds__(kThreads) k_pass1(OpParams op, Win win, int nwin,
-                                                    double* __restrict__ Yt,
-                                                    double* __restrict__ partial) {
-  constexpr int RPW = 32 / R;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = lane % R, rl = lane / R;
-  const double* __restrict__ Zd = win.p[nwin - 1];
-  double acc[K][R];
-#pragma unroll
-  for (int i = 0; i < K; ++i)
-#pragma unroll
-    for (int a = 0; a < R; ++a) acc[i][a] = 0.0;
+__device__ __forceinline__ double csr_col(const OpParams& op, const double* __restrict__ z, int64_t row) {
+  double v = 0.0;
+  const int64_t p1 = __ldg(op.rp + row + 1);
+  for (int64_t p = __ldg(op.rp + row); p < p1; ++p) v = fma(__ldg(op.cv + p), __ldg(z + __ldg(op.ci + p)), v);
+  return v;
+}
 
-  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  for (int64_t rg = (int64_t)blockIdx.x * kWarps + warp; rg * RPW < op.n; rg += nwarps) {
-    const int64_t row = rg * RPW + rl;
-    if (row < op.n) {
-      const double y = op_apply<R>(op, Zd, row, c);
-      if (Yt) Yt[row * R + c] = y;
+// Deterministic CTA reduction of NV per-thread values -> partial[blockIdx.x*NV + e].
+template <int NV>
+__device__ __forceinline__ void cta_reduce_store(const double (&v)[NV], double* __restrict__ partial,
+                                                 double* sm /* kWarps*NV */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        if (i < nwin) {
-          const double* __restrict__ zi = win.p[i] + row * R;
+  for (int e = 0; e < NV; ++e) {
+    double s = v[e];
 #pragma unroll
-          for (int a = 0; a < R; ++a) acc[i][a] = fma(__ldg(zi + a), y, acc[i][a]);
-        }
-      }
-    }
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(SYLV_FULL_MASK, s, off);
+    if (lane == 0) sm[warp * NV + e] = s;
   }
-  __shared__ double sm[kWarps][K * R * R];
-#pragma unroll
-  for (int i = 0; i < K; ++i)
-#pragma unroll
-    for (int a = 0; a < R; ++a) {
-      const double v = warp_sum_same_col<R>(acc[i][a]);
-      if (lane < R) sm[warp][(i * R + a) * R + lane] = v;
-    }
   __syncthreads();
-  for (int e = threadIdx.x; e < K * R * R; e += kThreads) {
+  for (int e = threadIdx.x; e < NV; e += blockDim.x) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += sm[w][e];
-    partial[(int64_t)blockIdx.x * K * R * R + e] = s;
+    for (int w = 0; w < kWarps; ++w) s += sm[w * NV + e];
+    partial[(int64_t)blockIdx.x * NV + e] = s;
   }
 }
 
-// ---------------------------------------------------------------------------------
-// pass 2: W' = Yt R_d - sum_i Z_i K_i (coef = [R_d, K_0..K_{nwin-1}]), write W';
-//         optional Gram partial (G[a][c]) and sparse-sign scatter of W' into sk.
-// Also the replay kernel of the second pass (GRAM_SKETCH = false).
-// ---------------------------------------------------------------------------------
-template <int R, int K, bool GRAM_SKETCH>
-__global__ void __launch_bounds__(kThreads) k_pass2(OpParams op, Win win, int nwin,
-                                                    const double* __restrict__ Yt,
-                                                    const double* __restrict__ coef,
-                                                    double* __restrict__ Wout,
-                                                    double* __restrict__ partial,
-                                                    SketchParams sp, double* __restrict__ sk) {
-  constexpr int RPW = 32 / R;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = lane % R, rl = lane / R;
-  __shared__ double cs[(K + 1) * R * R];
-  for (int e = threadIdx.x; e < (1 + nwin) * R * R; e += kThreads) cs[e] = coef[e];
-  __syncthreads();
+// =====================================================================================
+// r <= 4: one thread per row
+// =====================================================================================
+
+// pass 1: partial[blk][(i*R + a)*R + c] = sum_rows Z_i[row,a] Yt[row,c]
+template <int R, int K>
+__global__ void __launch_bounds__(kThreads) k_pass1_rows(OpParams op, Win win, int nwin, int64_t ld,
+                                                         double* __restrict__ Yt,
+                                                         double* __restrict__ partial) {
+  __shared__ double sm[kWarps * K * R * R];
+  double acc[K * R * R];
+#pragma unroll
+  for (int e = 0; e < K * R * R; ++e) acc[e] = 0.0;
   const double* __restrict__ Zd = win.p[nwin - 1];
-  double g[R];
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t row = (int64_t)blockIdx.x * kThreads + threadIdx.x; row < op.n; row += stride) {
+    double y[R], zc[R];
+    if (op.kind == kCSR) {
 #pragma unroll
-  for (int a = 0; a < R; ++a) g[a] = 0.0;
-
-  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  for (int64_t rg = (int64_t)blockIdx.x * kWarps + warp; rg * RPW < op.n; rg += nwarps) {
-    const int64_t row = rg * RPW + rl;
-    const bool valid = row < op.n;
-    double y = 0.0;
-    if (valid) y = Yt ? Yt[row * R + c] : op_apply<R>(op, Zd, row, c);
-    double wv = 0.0;
-#pragma unroll
-    for (int a = 0; a < R; ++a) {
-      const double ya = (R == 1) ? y : __shfl_sync(SYLV_FULL_MASK, y, rl * R + a);
-      wv = fma(ya, cs[a * R + c], wv);
-    }
-    if (valid) {
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        if (i < nwin) {
-          const double* __restrict__ zi = win.p[i] + row * R;
-          const double* ki = cs + (1 + i) * R * R;
-#pragma unroll
-          for (int a = 0; a < R; ++a) wv = fma(-__ldg(zi + a), ki[a * R + c], wv);
-        }
+      for (int c = 0; c < R; ++c) {
+        y[c] = csr_col(op, Zd + c * ld, row);
+        zc[c] = __ldg(Zd + c * ld + row);
       }
-      Wout[row * R + c] = wv;
+      if (Yt) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) Yt[c * ld + row] = y[c];
+      }
     } else {
-      wv = 0.0;
-    }
-    if (GRAM_SKETCH) {
+      const Coord q = coords(op, (uint32_t)row);
 #pragma unroll
-      for (int a = 0; a < R; ++a) {
-        const double wa = (R == 1) ? wv : __shfl_sync(SYLV_FULL_MASK, wv, rl * R + a);
-        g[a] = fma(wa, wv, g[a]);
+      for (int c = 0; c < R; ++c) y[c] = stencil_col(op, Zd + c * ld, (uint32_t)row, q, zc[c]);
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (i < nwin) {
+        double z[R];
+        if (i == nwin - 1) {
+#pragma unroll
+          for (int a = 0; a < R; ++a) z[a] = zc[a];
+        } else {
+#pragma unroll
+          for (int a = 0; a < R; ++a) z[a] = __ldg(win.p[i] + a * ld + row);
+        }
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+#pragma unroll
+          for (int c = 0; c < R; ++c) acc[(i * R + a) * R + c] = fma(z[a], y[c], acc[(i * R + a) * R + c]);
       }
-      if (valid && sk) {
-        const uint32_t m = (uint32_t)(row >> 5), l = (uint32_t)(row & 31);
-        for (uint32_t t = 0; t < sp.zeta; ++t) {
-          const SkEntry e = sk_entry(sp, m, l, t);
-          atomicAdd(sk + (int64_t)e.row * R + c, e.val * wv);
+    }
+  }
+  cta_reduce_store<K * R * R>(acc, partial, sm);
+}
+
+// pass 2: W' = Yt R_d - sum_i Z_i K_i  (coef = [R_d, K_0..K_{nwin-1}]); Gram partial.
+// GRAM = false: the second-pass replay (no Gram).
+template <int R, int K, bool GRAM>
+__global__ void __launch_bounds__(kThreads) k_pass2_rows(OpParams op, Win win, int nwin, int64_t ld,
+                                                         const double* __restrict__ Yt,
+                                                         const double* __restrict__ coef,
+                                                         double* __restrict__ Wout,
+                                                         double* __restrict__ partial) {
+  __shared__ double cs[(K + 1) * R * R];
+  __shared__ double sm[GRAM ? kWarps * R * R : 1];
+  for (int e = threadIdx.x; e < (1 + nwin) * R * R; e += blockDim.x) cs[e] = coef[e];
+  __syncthreads();
+  double g[R * R];
+#pragma unroll
+  for (int e = 0; e < R * R; ++e) g[e] = 0.0;
+  const double* __restrict__ Zd = win.p[nwin - 1];
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t row = (int64_t)blockIdx.x * kThreads + threadIdx.x; row < op.n; row += stride) {
+    double y[R], zc[R];
+    if (Yt) {
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        y[c] = __ldg(Yt + c * ld + row);
+        zc[c] = __ldg(Zd + c * ld + row);
+      }
+    } else if (op.kind == kCSR) {
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        y[c] = csr_col(op, Zd + c * ld, row);
+        zc[c] = __ldg(Zd + c * ld + row);
+      }
+    } else {
+      const Coord q = coords(op, (uint32_t)row);
+#pragma unroll
+      for (int c = 0; c < R; ++c) y[c] = stencil_col(op, Zd + c * ld, (uint32_t)row, q, zc[c]);
+    }
+    double w[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < R; ++a) s = fma(y[a], cs[a * R + c], s);
+      w[c] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (i < nwin) {
+        double z[R];
+        if (i == nwin - 1) {
+#pragma unroll
+          for (int a = 0; a < R; ++a) z[a] = zc[a];
+        } else {
+#pragma unroll
+          for (int a = 0; a < R; ++a) z[a] = __ldg(win.p[i] + a * ld + row);
+        }
+        const double* ki = cs + (1 + i) * R * R;
+#pragma unroll
+        for (int c = 0; c < R; ++c)
+#pragma unroll
+          for (int a = 0; a < R; ++a) w[c] = fma(-z[a], ki[a * R + c], w[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < R; ++c) Wout[c * ld + row] = w[c];
+    if (GRAM) {
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+#pragma unroll
+        for (int c = 0; c < R; ++c) g[a * R + c] = fma(w[a], w[c], g[a * R + c]);
+    }
+  }
+  if (GRAM) cta_reduce_store<R * R>(g, partial, sm);
+}
+
+// =====================================================================================
+// r = 8: DMMA warp tiles
+// =====================================================================================
+
+// pass 1, 4-row tiles: lane <-> element (row0 + (lane&3), col lane>>2) of every block.
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_pass1_r8(OpParams op, Win win, int nwin, int64_t ld,
+                                                       double* __restrict__ Yt,
+                                                       double* __restrict__ partial) {
+  constexpr int R = 8;
+  __shared__ double sm[kWarps * K * 64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rr = lane & 3, c = lane >> 2;
+  double acc[K][2];
+#pragma unroll
+  for (int i = 0; i < K; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const double* __restrict__ Zd = win.p[nwin - 1] + c * ld;
+  const int64_t ntiles = (op.n + 3) >> 2;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  for (int64_t t = (int64_t)blockIdx.x * kWarps + warp; t < ntiles; t += wstride) {
+    const int64_t row = t * 4 + rr;
+    double y = 0.0, zc = 0.0;
+    if (row < op.n) {
+      if (op.kind == kCSR) {
+        y = csr_col(op, Zd, row);
+        zc = __ldg(Zd + row);
+        if (Yt) Yt[c * ld + row] = y;
+      } else {
+        const Coord q = coords(op, (uint32_t)row);
+        y = stencil_col(op, Zd, (uint32_t)row, q, zc);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (i < nwin) {
+        const double z = (i == nwin - 1) ? zc : (row < op.n ? __ldg(win.p[i] + c * ld + row) : 0.0);
+        dmma(acc[i], z, y);  // P_i[a][c'] += Z_i[row][a] Yt[row][c']
+      }
+    }
+  }
+  // D fragment: lane holds P_i[lane>>2][2*(lane&3) + e]
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    sm[(warp * K + i) * 64 + c * 8 + 2 * rr] = acc[i][0];
+    sm[(warp * K + i) * 64 + c * 8 + 2 * rr + 1] = acc[i][1];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < K * 64; e += kThreads) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += sm[w * K * 64 + e];
+    partial[(int64_t)blockIdx.x * K * 64 + e] = s;
+  }
+  (void)R;
+}
+
+// pass 2, 8-row tiles.  A fragments: lane holds X[row0 + (lane>>2)][(lane&3) + 4h], h = 0, 1.
+template <int K, bool GRAM>
+__global__ void __launch_bounds__(kThreads) k_pass2_r8(OpParams op, Win win, int nwin, int64_t ld,
+                                                       const double* __restrict__ Yt,
+                                                       const double* __restrict__ coef,
+                                                       double* __restrict__ Wout,
+                                                       double* __restrict__ partial) {
+  __shared__ double sm[GRAM ? kWarps * 64 : 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ra = lane >> 2, ka = lane & 3;  // A: row ra, k-col ka (+4h); B: k-row ka (+4h), col ra
+  // B fragments of the coefficient matrices (row-major 8x8): R_d and -K_i
+  double bR[2], bK[K][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) bR[h] = __ldg(coef + (ka + 4 * h) * 8 + ra);
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) bK[i][h] = (i < nwin) ? -__ldg(coef + (1 + i) * 64 + (ka + 4 * h) * 8 + ra) : 0.0;
+  double G[2] = {0.0, 0.0};
+  const double* __restrict__ Zd = win.p[nwin - 1];
+  const int64_t ntiles = (op.n + 7) >> 3;
+  const int64_t wstride = (int64_t)gridDim.x * kWarps;
+  for (int64_t t = (int64_t)blockIdx.x * kWarps + warp; t < ntiles; t += wstride) {
+    const int64_t row = t * 8 + ra;
+    const bool valid = row < op.n;
+    double y[2] = {0.0, 0.0}, zc[2] = {0.0, 0.0};
+    if (valid) {
+      if (Yt) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          y[h] = __ldg(Yt + (ka + 4 * h) * ld + row);
+          zc[h] = __ldg(Zd + (ka + 4 * h) * ld + row);
+        }
+      } else if (op.kind == kCSR) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          y[h] = csr_col(op, Zd + (ka + 4 * h) * ld, row);
+          zc[h] = __ldg(Zd + (ka + 4 * h) * ld + row);
+        }
+      } else {
+        const Coord q = coords(op, (uint32_t)row);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) y[h] = stencil_col(op, Zd + (ka + 4 * h) * ld, (uint32_t)row, q, zc[h]);
+      }
+    }
+    double D[2] = {0.0, 0.0};
+    dmma(D, y[0], bR[0]);
+    dmma(D, y[1], bR[1]);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (i < nwin) {
+        double z0, z1;
+        if (i == nwin - 1) {
+          z0 = zc[0];
+          z1 = zc[1];
+        } else {
+          z0 = valid ? __ldg(win.p[i] + ka * ld + row) : 0.0;
+          z1 = valid ? __ldg(win.p[i] + (ka + 4) * ld + row) : 0.0;
+        }
+        dmma(D, z0, bK[i][0]);
+        dmma(D, z1, bK[i][1]);
+      }
+    }
+    // D: lane holds W'[row0 + ra][2*ka + e]
+    const int64_t orow = t * 8 + ra;
+    if (orow < op.n) {
+      Wout[(2 * ka) * ld + orow] = D[0];
+      Wout[(2 * ka + 1) * ld + orow] = D[1];
+    }
+    if (GRAM) {
+      // Gram: A = B = element (row0 + 4q + (lane&3), col lane>>2), held by lane 4r + (col>>1), reg col&1
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        const int r = 4 * qq + (lane & 3);
+        const int col = lane >> 2;
+        const int src = 4 * r + (col >> 1);
+        const double v0 = __shfl_sync(SYLV_FULL_MASK, D[0], src);
+        const double v1 = __shfl_sync(SYLV_FULL_MASK, D[1], src);
+        const double v = (col & 1) ? v1 : v0;
+        dmma(G, v, v);
+      }
+    }
+  }
+  if (GRAM) {
+    sm[warp * 64 + ra * 8 + 2 * ka] = G[0];
+    sm[warp * 64 + ra * 8 + 2 * ka + 1] = G[1];
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64; e += kThreads) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += sm[w * 64 + e];
+      partial[(int64_t)blockIdx.x * 64 + e] = s;
+    }
+  }
+}
+
+// =====================================================================================
+// Sparse-sign sketch of an SoA block, shared-memory privatised (a4)
+// =====================================================================================
+// grid (nchunk, R).  CTA (chunk, c) accumulates column c of S X for the rows of its chunk
+// in shared memory (s doubles); warp w owns bucket(s) t = w, w + 8, ... so warps never
+// write the same address; within a warp the 32 rows of a group hit 32 distinct, cyclically
+// consecutive slots, so the read-modify-write is conflict-free.  Group
+// hashes are computed 32 groups at a time (one per lane) and broadcast with shuffles.
+// Output: partial[(chunk*R + c)*s + q].
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_sketch_cols(int64_t n, const double* __restrict__ X, int64_t ld,
+                                                          SketchParams sp, int64_t groups_per_chunk,
+                                                          double* __restrict__ partial) {
+  extern __shared__ double skm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.y;
+  const uint32_t b = sp.b;
+  const int64_t s = (int64_t)b * sp.zeta;
+  for (int64_t e = threadIdx.x; e < s; e += kThreads) skm[e] = 0.0;
+  __syncthreads();
+  const int64_t ngroups = (n + 31) >> 5;
+  const int64_t g0 = (int64_t)blockIdx.x * groups_per_chunk;
+  const int64_t g1 = min(ngroups, g0 + groups_per_chunk);
+  const double* __restrict__ xc = X + c * ld;
+  for (uint32_t t = warp; t < sp.zeta; t += kWarps) {
+    double* bucket = skm + (int64_t)t * b;
+    for (int64_t gb = g0; gb < g1; gb += 32) {
+      // lane computes the three group hashes of group gb + lane
+      const uint32_t m = (uint32_t)(gb + lane);
+      const uint32_t h0 = group_hash(sp, m, t, 0);
+      const uint32_t h1 = group_hash(sp, m, t, 1);
+      const uint32_t h2 = group_hash(sp, m, t, 2);
+      const uint32_t base = __umulhi(h0, b);
+      const uint32_t ng = (uint32_t)(g1 - gb < 32 ? g1 - gb : 32);
+      for (uint32_t k0 = 0; k0 < ng; k0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t row = ((gb + k0 + u) << 5) + lane;
+          v[u] = (k0 + u < ng && row < n) ? __ldg(xc + row) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t kk = k0 + u;
+          const uint32_t bs = __shfl_sync(SYLV_FULL_MASK, base, kk & 31);
+          const uint32_t p1 = __shfl_sync(SYLV_FULL_MASK, h1, kk & 31);
+          const uint32_t sg = __shfl_sync(SYLV_FULL_MASK, h2, kk & 31);
+          if (kk < ng) {
+            const uint32_t a = 2u * (p1 & 15u) + 1u;
+            const uint32_t cc = (p1 >> 4) & 31u;
+            uint32_t slot = bs + ((a * (uint32_t)lane + cc) & 31u);
+            const double val = ((sg >> lane) & 1u) ? -v[u] : v[u];
+            if (b >= 32u) {
+              slot = slot >= b ? slot - b : slot;
+              bucket[slot] += val;
+              __syncwarp();
+            } else {
+              atomicAdd(bucket + (slot % b), val);   // tiny buckets: slots of a group collide
+            }
+          }
         }
       }
     }
   }
-  if (GRAM_SKETCH) {
-    __shared__ double sm[kWarps][R * R];
-#pragma unroll
-    for (int a = 0; a < R; ++a) {
-      const double v = warp_sum_same_col<R>(g[a]);
-      if (lane < R) sm[warp][a * R + lane] = v;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < R * R; e += kThreads) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) s += sm[w][e];
-      partial[(int64_t)blockIdx.x * R * R + e] = s;
-    }
-  }
+  __syncthreads();
+  double* out = partial + ((int64_t)blockIdx.x * R + c) * s;
+  for (int64_t e = threadIdx.x; e < s; e += kThreads) out[e] = skm[e] * sp.scale;
 }
 
-// ---------------------------------------------------------------------------------
-// Standalone sketch of an n x R block (init: S C; test entry apply_sketch), and the
-// Gram partial of the same block (init: C^T C).  out must be zeroed.
-// ---------------------------------------------------------------------------------
+// w[q*R + c] = sum_a (sum_chunk partial[(chunk*R + a)*s + q]) M[a*R + c]  (M = identity if null)
 template <int R>
-__global__ void __launch_bounds__(kThreads) k_sketch_gram(int64_t n, const double* __restrict__ X,
-                                                          SketchParams sp, double* __restrict__ out,
-                                                          double* __restrict__ partial) {
-  constexpr int RPW = 32 / R;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = lane % R, rl = lane / R;
-  double g[R];
-#pragma unroll
-  for (int a = 0; a < R; ++a) g[a] = 0.0;
-  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  for (int64_t rg = (int64_t)blockIdx.x * kWarps + warp; rg * RPW < n; rg += nwarps) {
-    const int64_t row = rg * RPW + rl;
-    const bool valid = row < n;
-    const double x = valid ? X[row * R + c] : 0.0;
+__global__ void k_sketch_reduce(const double* __restrict__ partial, int nchunk, int64_t s,
+                                const double* __restrict__ M, double* __restrict__ w) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < s; q += (int64_t)gridDim.x * blockDim.x) {
+    double v[R];
 #pragma unroll
     for (int a = 0; a < R; ++a) {
-      const double xa = (R == 1) ? x : __shfl_sync(SYLV_FULL_MASK, x, rl * R + a);
-      g[a] = fma(xa, x, g[a]);
+      double acc = 0.0;
+      for (int ch = 0; ch < nchunk; ++ch) acc += partial[((int64_t)ch * R + a) * s + q];
+      v[a] = acc;
     }
-    if (valid && out) {
-      const uint32_t m = (uint32_t)(row >> 5), l = (uint32_t)(row & 31);
-      for (uint32_t t = 0; t < sp.zeta; ++t) {
-        const SkEntry e = sk_entry(sp, m, l, t);
-        atomicAdd(out + (int64_t)e.row * R + c, e.val * x);
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      double o;
+      if (M) {
+        o = 0.0;
+#pragma unroll
+        for (int a = 0; a < R; ++a) o = fma(v[a], __ldg(M + a * R + c), o);
+      } else {
+        o = v[c];
       }
-    }
-  }
-  if (partial) {
-    __shared__ double sm[kWarps][R * R];
-#pragma unroll
-    for (int a = 0; a < R; ++a) {
-      const double v = warp_sum_same_col<R>(g[a]);
-      if (lane < R) sm[warp][a * R + lane] = v;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < R * R; e += kThreads) {
-      double s = 0.0;
-      for (int w = 0; w < kWarps; ++w) s += sm[w][e];
-      partial[(int64_t)blockIdx.x * R * R + e] = s;
+      w[q * R + c] = o;
     }
   }
 }
 
-// ---------------------------------------------------------------------------------
+// Gram partial of an SoA block (init: C^T C), one thread per row.
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_gram_soa(int64_t n, const double* __restrict__ X, int64_t ld,
+                                                       double* __restrict__ partial) {
+  __shared__ double sm[kWarps * R * R];
+  double g[R * R];
+#pragma unroll
+  for (int e = 0; e < R * R; ++e) g[e] = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * kThreads + threadIdx.x; row < n; row += (int64_t)gridDim.x * kThreads) {
+    double x[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) x[c] = __ldg(X + c * ld + row);
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int c = 0; c < R; ++c) g[a * R + c] = fma(x[a], x[c], g[a * R + c]);
+  }
+  cta_reduce_store<R * R>(g, partial, sm);
+}
+
+// Gram partial of a row-major rows x R block (sketch space CholQR2), one thread per row.
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_gram_rowmajor(int64_t rows, const double* __restrict__ X,
+                                                            double* __restrict__ partial) {
+  __shared__ double sm[kWarps * R * R];
+  double g[R * R];
+#pragma unroll
+  for (int e = 0; e < R * R; ++e) g[e] = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * kThreads + threadIdx.x; row < rows; row += (int64_t)gridDim.x * kThreads) {
+    double x[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) x[c] = __ldg(X + row * R + c);
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int c = 0; c < R; ++c) g[a * R + c] = fma(x[a], x[c], g[a * R + c]);
+  }
+  cta_reduce_store<R * R>(g, partial, sm);
+}
+
+// Row-major (n x R, ld_in) <-> SoA (R columns, ld).
+template <int R>
+__global__ void k_to_soa(int64_t n, const double* __restrict__ in, double* __restrict__ out, int64_t ld) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * R; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / R;
+    const int c = (int)(e - row * R);
+    out[c * ld + row] = in[e];
+  }
+}
+
+// out (row-major n x R) = Z (SoA) M  (get_block: U_j = Z_j R_j)
+template <int R>
+__global__ void k_soa_mul_rowmajor(int64_t n, const double* __restrict__ Z, int64_t ld,
+                                   const double* __restrict__ M, double* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * R; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / R;
+    const int c = (int)(e - row * R);
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; ++a) s = fma(Z[a * ld + row], M[a * R + c], s);
+    out[e] = s;
+  }
+}
+
+// =====================================================================================
 // Second pass accumulation X[row, l] += sum_b sum_a Z_b[row, a] M[(b*R + a)*ell + l]
-// for a chunk of nb blocks (a7).  One thread per (row, l).
-// ---------------------------------------------------------------------------------
+// (a7), one thread per (row, l); X row-major with leading dimension ldx.
+// =====================================================================================
 constexpr int kMaxChunk = 16;
 struct ChunkPtrs {
   const double* p[kMaxChunk];
 };
 
 template <int R>
-__global__ void __launch_bounds__(kThreads) k_xacc(int64_t n, ChunkPtrs zb, int nb,
+__global__ void __launch_bounds__(kThreads) k_xacc(int64_t n, ChunkPtrs zb, int nb, int64_t ld,
                                                    const double* __restrict__ M, int ell,
                                                    double* __restrict__ X, int64_t ldx) {
   const int64_t total = n * (int64_t)ell;
@@ -229,26 +563,11 @@ __global__ void __launch_bounds__(kThreads) k_xacc(int64_t n, ChunkPtrs zb, int 
     const int l = (int)(e - row * ell);
     double acc = X[row * ldx + l];
     for (int b = 0; b < nb; ++b) {
-      const double* z = zb.p[b] + row * R;
 #pragma unroll
-      for (int a = 0; a < R; ++a) acc = fma(__ldg(z + a), __ldg(M + (int64_t)(b * R + a) * ell + l), acc);
+      for (int a = 0; a < R; ++a)
+        acc = fma(__ldg(zb.p[b] + a * ld + row), __ldg(M + (int64_t)(b * R + a) * ell + l), acc);
     }
     X[row * ldx + l] = acc;
-  }
-}
-
-// Normalised block out = Z R (introspection entry get_block).
-template <int R>
-__global__ void k_zr(int64_t n, const double* __restrict__ Z, const double* __restrict__ Rm,
-                     double* __restrict__ out) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * R;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = e / R;
-    const int c = (int)(e - row * R);
-    double s = 0.0;
-#pragma unroll
-    for (int a = 0; a < R; ++a) s = fma(Z[row * R + a], Rm[a * R + c], s);
-    out[e] = s;
   }
 }
 
