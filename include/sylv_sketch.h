@@ -97,8 +97,11 @@ typedef struct {
   double rank_tol;       /* Y ~ Y1 Y2^T keeps sigma_i > rank_tol * sigma_1     */
   int32_t chunk;         /* second pass: blocks per X accumulation (0 = k+1)   */
   int32_t flags;         /* bit 0: time the n-space passes with CUDA events;
-                            bit 1: run both sequences on one stream (isolated
-                            kernel timings; default overlaps U and V on two streams) */
+                            bit 1: run everything on one stream (isolated kernel
+                            timings; default: U and V passes on two streams, each
+                            sequence's sketch-space work on its own side stream);
+                            bit 2: disable the 2.5-D TMA passes (3-D stencil, r = 8,
+                            even N) and use the generic pass kernels */
 } sylv_config;
 
 /* Create a context and run Alg. 1 line 1: U1 ell = C1, V1 ell' = C2
@@ -164,6 +167,8 @@ typedef struct {
   int64_t n_pass1, n_pass2;  /* timed launches (flags bit 0)                      */
   double ms_skqr;            /* summed time of the sketch-space QR (flags bit 0)  */
   int64_t n_skqr;
+  double ms_sketch;          /* summed time of the sparse-sign sketch kernels (a4) */
+  int64_t n_sketch;
   double host_solve_s;       /* wall seconds spent in host projected solves       */
   int64_t host_solves;
   double kappa_T_u, kappa_T_v; /* reserved                                        */

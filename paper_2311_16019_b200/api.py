@@ -44,7 +44,8 @@ class Config(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("launches", C.c_int64), ("steps", C.c_int64), ("ms_pass1", C.c_double),
                 ("ms_pass2", C.c_double), ("n_pass1", C.c_int64), ("n_pass2", C.c_int64),
-                ("ms_skqr", C.c_double), ("n_skqr", C.c_int64), ("host_solve_s", C.c_double),
+                ("ms_skqr", C.c_double), ("n_skqr", C.c_int64), ("ms_sketch", C.c_double),
+                ("n_sketch", C.c_int64), ("host_solve_s", C.c_double),
                 ("host_solves", C.c_int64), ("kappa_T_u", C.c_double), ("kappa_T_v", C.c_double)]
 
     def as_dict(self):
@@ -159,10 +160,10 @@ class SylvSketch:
     def __init__(self, A: Operator, B: Operator, C1, C2, *, r: int, k: int, d_max: int, s: int,
                  zeta: int = 8, seed_u: int = 11, seed_v: int = 12, tol: float = 1e-6,
                  rank_tol: float = 1e-12, chunk: int = 0, timing: bool = False, stream=None,
-                 keep=None, serial: bool = False):
+                 keep=None, serial: bool = False, tma: bool = True):
         self.lib = load_library()
         self.cfg = Config(r=r, k=k, d_max=d_max, zeta=zeta, s=s, seed_u=seed_u, seed_v=seed_v, tol=tol,
-                          rank_tol=rank_tol, chunk=chunk, flags=(1 if timing else 0) | (2 if serial else 0))
+                          rank_tol=rank_tol, chunk=chunk, flags=(1 if timing else 0) | (2 if serial else 0) | (0 if tma else 4))
         self.n, self.r, self.s = int(A.n), r, s
         self._keep = [A, B, keep]
         p1, k1 = _ptr(C1)

@@ -4,12 +4,15 @@
 // seed_v).  A block step runs the n-space passes (nspace.cuh) and the sketch-space QR
 // update (sspace.cuh) for U then V on the context stream; small coefficient mirrors
 // are copied to pinned host memory for the host projected solve (host_solve.cpp).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +22,7 @@
 #include "host_solve.hpp"
 #include "nspace.cuh"
 #include "sspace.cuh"
+#include "stencil25d.cuh"
 
 using namespace sylv;
 
@@ -97,12 +101,17 @@ T* dalloc(size_t count) {
 
 struct TimedPair {
   cudaEvent_t a, b;
-  int kind;  // 0 pass1, 1 pass2, 2 skqr
+  int kind;  // 0 pass1, 1 pass2, 2 skqr (sketch included), 3 sketch alone
 };
 
 }  // namespace
 
 struct Sequence {
+  // 2.5-D TMA passes (3-D stencil, r = 8, even N): tensor maps of the ring slots
+  CUtensorMap mapH[kMaxK + 1];   // halo boxes
+  CUtensorMap mapW[kMaxK + 1];   // window boxes
+  bool tma = false;
+  St25 st25{};
   int which = 0;
   int R = 1, K = 1, dmax = 0;
   int64_t n = 0, s = 0, ldT = 0, ld = 0;   // ld: SoA column stride (n rounded up to 64)
@@ -124,7 +133,8 @@ struct Sequence {
   double* hn2 = nullptr;      // (dmax+1)
   int* flags = nullptr;       // (dmax+2)
   double* part1 = nullptr;    // G x K R^2
-  double* part2 = nullptr;    // G x R^2
+  double* part2 = nullptr;    // G x R^2   (main stream: pass-2 Gram)
+  double* part_s = nullptr;   // G x R^2   (side stream: CholQR2 Grams)
   double* cpart = nullptr;    // RT x ldT x R
   double* csum = nullptr;     // ldT x R
   double* c2 = nullptr;       // ldT x R
@@ -138,6 +148,9 @@ struct Sequence {
   double* Th = nullptr;       // ldT x ldT col-major
   double* Rh = nullptr;       // (dmax+2) R^2 (filled on demand)
   int* flags_h = nullptr;
+  // per-step events (ring of K+2): coef2 of step j done (main -> side) and the sketch of
+  // step j done reading ring slot j+1 (side -> main, before pass 2 of step j+K+1 rewrites it)
+  std::vector<cudaEvent_t> ev_c2, ev_sk;
   double beta[kMaxR * kMaxR];
   double ell[kMaxR * kMaxR];
 
@@ -152,14 +165,18 @@ struct sylv_ctx {
   double tol = 1e-6, rank_tol = 1e-12;
   int sm = 148;
   int G = 0;          // grid of the n-space passes
+  int G25 = 0;        // grid of the 2.5-D TMA passes (0: not used)
+  size_t smem25_1 = 0, smem25_2 = 0;
   int RT = 1;         // row tiles of Q^T w
   int64_t tileQ = 0;
   int CC = 1;         // column chunks of Q c
   int nchunk = 1;     // row chunks of the sketch kernel (grid nchunk x R)
   int64_t gpc = 32;   // 32-row groups per sketch chunk
   size_t sk_smem = 0; // dynamic shared memory of the sketch kernel
-  cudaStream_t st2 = nullptr;  // second stream: the V sequence runs concurrently with U
-  cudaEvent_t fork = nullptr, join = nullptr;
+  // streams: main[0] = st (U passes), main[1] = st2 (V passes); side[q] = sketch + sketch-space
+  // QR of sequence q, which overlaps the next step's n-space passes (all = st in serial mode)
+  cudaStream_t st2 = nullptr, st3 = nullptr, st4 = nullptr;
+  cudaEvent_t fork = nullptr, join[3] = {nullptr, nullptr, nullptr};
   Sequence seq[2];
   int d_done = 0;
   bool broken = false;
@@ -196,7 +213,8 @@ void ev_collect(sylv_ctx* c) {
     CK(cudaEventElapsedTime(&ms, p.a, p.b));
     if (p.kind == 0) { c->stats.ms_pass1 += ms; c->stats.n_pass1++; }
     else if (p.kind == 1) { c->stats.ms_pass2 += ms; c->stats.n_pass2++; }
-    else { c->stats.ms_skqr += ms; c->stats.n_skqr++; }
+    else if (p.kind == 2) { c->stats.ms_skqr += ms; c->stats.n_skqr++; }
+    else { c->stats.ms_sketch += ms; c->stats.n_sketch++; }
     c->free_events.push_back(p);
   }
   c->timed.clear();
@@ -273,8 +291,10 @@ void upload_csr(Sequence& q, const sylv_operator* A, bool transpose, cudaStream_
 }
 
 void free_seq(Sequence& q) {
+  for (cudaEvent_t e : q.ev_c2) cudaEventDestroy(e);
+  for (cudaEvent_t e : q.ev_sk) cudaEventDestroy(e);
   double* dp[] = {q.ring, q.Cdev, q.Yt, q.sk, q.skpart, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
-                  q.part1, q.part2, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv};
+                  q.part1, q.part2, q.part_s, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv};
   for (double* p : dp)
     if (p) cudaFree(p);
   if (q.flags) cudaFree(q.flags);
@@ -297,21 +317,123 @@ void cholqr2(sylv_ctx* c, Sequence& q, double* in, int64_t col0, double* tau_out
   double* tai = q.small + 64;      // R^2
   double* tbi = q.small + 128;     // R^2
   SYLV_DISPATCH_R(R, {
-    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, in, q.part2);
-    k_chol_small<R_><<<1, 64, 0, st>>>(q.part2, gs, ta, tai, nullptr, q.flags, flag_slot);
+    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, in, q.part_s);
+    k_chol_small<R_><<<1, kThreads, 0, st>>>(q.part_s, gs, ta, tai, nullptr, q.flags, flag_slot);
     k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, in, tai, q.w2, 0);
-    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, q.w2, q.part2);
-    k_chol_small<R_><<<1, 64, 0, st>>>(q.part2, gs, tau_out, tbi, ta, q.flags, flag_slot);
+    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, q.w2, q.part_s);
+    k_chol_small<R_><<<1, kThreads, 0, st>>>(q.part_s, gs, tau_out, tbi, ta, q.flags, flag_slot);
     k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, q.w2, tbi, q.Q + col0 * q.s, q.s);
   });
   count(c, 6);
   CK(cudaGetLastError());
 }
 
-// n-space pass launchers (R <= 4: thread-per-row FMA kernels; R = 8: DMMA warp tiles)
-void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, cudaStream_t st) {
+// ---- 2.5-D TMA passes ------------------------------------------------------------------
+constexpr int kTY25 = 4;   // tile height (lines) = warps per CTA
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// SoA block (R columns of an N^3 grid, column stride ld) as an (x, y, z, column) tensor.
+bool encode_block_map(CUtensorMap* m, const double* base, int N, int64_t ld, int R, int bx, int by) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)R};
+  cuuint64_t strides[3] = {(cuuint64_t)N * 8, (cuuint64_t)N * N * 8, (cuuint64_t)ld * 8};
+  cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, 1, (cuuint32_t)R};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int K>
+size_t smem25_bytes() {
+  using Gm = Geo25<kTY25>;
+  return (size_t)kNS * (Gm::HCOL * 8 + (K - 1) * Gm::WCOL * 8) * 8 + kNS * 8;
+}
+
+template <int K>
+void set_smem25(sylv_ctx* c) {
+  c->smem25_1 = c->smem25_2 = smem25_bytes<K>();
+  CK(cudaFuncSetAttribute(k_st3d_r8<kTY25, K, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_1));
+  CK(cudaFuncSetAttribute(k_st3d_r8<kTY25, K, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_2));
+  CK(cudaFuncSetAttribute(k_st3d_r8<kTY25, K, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_2));
+}
+
+// Set up the TMA path for sequence q if eligible: 3-D stencil, r = 8, even N.
+void setup_tma(sylv_ctx* c, Sequence& q) {
+  q.tma = false;
+  if ((c->cflags & 4) || q.op.kind != kStencil3D || c->R != 8 || (q.op.N & 1) || q.op.N < 2) return;
+  const int N = q.op.N;
+  for (int j = 0; j <= c->K; ++j) {
+    const double* base = q.ring + (int64_t)j * q.ld * c->R;
+    if (!encode_block_map(&q.mapH[j], base, N, q.ld, c->R, Geo25<kTY25>::HX, Geo25<kTY25>::HY)) return;
+    if (!encode_block_map(&q.mapW[j], base, N, q.ld, c->R, Geo25<kTY25>::WX, kTY25)) return;
+  }
+  St25& p = q.st25;
+  p.N = N;
+  p.ld = q.ld;
+  p.tiles_x = (N + kTx - 1) / kTx;
+  p.tiles_y = (N + kTY25 - 1) / kTY25;
+  const int64_t tiles = (int64_t)p.tiles_x * p.tiles_y;
+  const int grid = 2 * c->sm;
+  int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, N / 16), (8 * grid + tiles - 1) / tiles));
+  p.zseg = (N + nseg - 1) / nseg;
+  p.nseg = (N + p.zseg - 1) / p.zseg;
+  p.items = tiles * p.nseg;
+  p.cd = q.op.cd;
+  p.cxm = q.op.cxm; p.cxp = q.op.cxp;
+  p.cym = q.op.cym; p.cyp = q.op.cyp;
+  p.czm = q.op.czm; p.czp = q.op.czp;
+  p.dbg = getenv("SYLV_DBG") ? atoi(getenv("SYLV_DBG")) : 0;
+  c->G25 = (int)std::min<int64_t>(p.items, grid);
+  switch (c->K) {
+    case 1: set_smem25<1>(c); break;
+    case 2: set_smem25<2>(c); break;
+    case 3: set_smem25<3>(c); break;
+    case 4: set_smem25<4>(c); break;
+  }
+  q.tma = true;
+}
+
+Tma25 tma_args(const Sequence& q, int j, int nwin) {
+  Tma25 tm;
+  const int ns = q.K + 1;
+  tm.zd = q.mapH[j % ns];
+  for (int i = 0; i < nwin - 1; ++i) tm.win[i] = q.mapW[(j - nwin + 1 + i) % ns];
+  return tm;
+}
+
+// Partials written by the pass kernels of sequence q (the coefficient kernels' nparts)
+int pass_parts(const sylv_ctx* c, const Sequence& q) { return q.tma ? c->G25 : c->G; }
+
+// n-space pass launchers (2.5-D TMA kernels when eligible; else R <= 4: thread-per-row FMA
+// kernels, R = 8: DMMA warp tiles).  j = step (1-based): Z_j is the newest window block.
+void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cudaStream_t st) {
   const int R = c->R, K = c->K;
-  if (R == 8) {
+  if (q.tma) {
+    const Tma25 tm = tma_args(q, j, nwin);
+    switch (K) {
+      case 1: k_st3d_r8<kTY25, 1, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
+      case 2: k_st3d_r8<kTY25, 2, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
+      case 3: k_st3d_r8<kTY25, 3, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
+      case 4: k_st3d_r8<kTY25, 4, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
+    }
+  } else if (R == 8) {
     switch (K) {
       case 1: k_pass1_r8<1><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); break;
       case 2: k_pass1_r8<2><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); break;
@@ -325,10 +447,18 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, cudaStream
 }
 
 template <bool GRAM>
-void launch_pass2(sylv_ctx* c, Sequence& q, const Win& win, int nwin, const double* Yt, const double* coef,
-                  double* out, cudaStream_t st) {
+void launch_pass2(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, const double* Yt, const double* coef,
+                  double* out, cudaStream_t st, bool allow_tma = true) {
   const int R = c->R, K = c->K;
-  if (R == 8) {
+  if (q.tma && allow_tma) {
+    const Tma25 tm = tma_args(q, j, nwin);
+    switch (K) {
+      case 1: k_st3d_r8<kTY25, 1, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2); break;
+      case 2: k_st3d_r8<kTY25, 2, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2); break;
+      case 3: k_st3d_r8<kTY25, 3, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2); break;
+      case 4: k_st3d_r8<kTY25, 4, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2); break;
+    }
+  } else if (R == 8) {
     switch (K) {
       case 1: k_pass2_r8<1, GRAM><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, Yt, coef, out, q.part2); break;
       case 2: k_pass2_r8<2, GRAM><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, Yt, coef, out, q.part2); break;
@@ -386,14 +516,23 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.Hc = dalloc<double>((size_t)(c->dmax + 1) * (K + 1) * R * R);
   q.hn2 = dalloc<double>(c->dmax + 1);
   q.flags = dalloc<int>(c->dmax + 2);
-  q.part1 = dalloc<double>((size_t)c->G * K * R * R);
-  q.part2 = dalloc<double>((size_t)c->G * R * R);
+  const int gmax = std::max(c->G, 2 * c->sm);
+  q.part1 = dalloc<double>((size_t)gmax * K * R * R);
+  q.part2 = dalloc<double>((size_t)gmax * R * R);
+  q.part_s = dalloc<double>((size_t)c->G * R * R);
+  q.ev_c2.resize(K + 2);
+  q.ev_sk.resize(K + 2);
+  for (int i = 0; i < K + 2; ++i) {
+    CK(cudaEventCreateWithFlags(&q.ev_c2[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&q.ev_sk[i], cudaEventDisableTiming));
+  }
   q.cpart = dalloc<double>((size_t)c->RT * ldT * R);
   q.csum = dalloc<double>(ldT * R);
   q.c2 = dalloc<double>(ldT * R);
   q.qcpart = dalloc<double>((size_t)c->CC * sR);
   q.small = dalloc<double>(512);
   CK(cudaMemsetAsync(q.ring, 0, (size_t)(K + 1) * blk * sizeof(double), c->st));
+  setup_tma(c, q);
   CK(cudaMemsetAsync(q.Tdev, 0, (size_t)ldT * ldT * sizeof(double), c->st));
   CK(cudaMemsetAsync(q.flags, 0, (c->dmax + 2) * sizeof(int), c->st));
   CK(cudaMemsetAsync(q.Hc, 0, (size_t)(c->dmax + 1) * (K + 1) * R * R * sizeof(double), c->st));
@@ -422,7 +561,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   double* beta_d = q.small + 320;
   SYLV_DISPATCH_R(R, {
     k_gram_soa<R_><<<c->G, kThreads, 0, c->st>>>(c->n, q.Cdev, q.ld, q.part2);
-    k_chol_small<R_><<<1, 64, 0, c->st>>>(q.part2, c->G, ell_d, elli_d, nullptr, q.flags, 0);
+    k_chol_small<R_><<<1, kThreads, 0, c->st>>>(q.part2, c->G, ell_d, elli_d, nullptr, q.flags, 0);
   });
   count(c, 2);
   CK(cudaGetLastError());
@@ -441,34 +580,52 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   if (q.flags_h[0]) throw Status{SYLV_E_INVALID, "C1 or C2 (or its sketch) is rank deficient"};
 }
 
-// One block step j (1-based) of one sequence on stream st: Alg. 1 lines 3-9.
-void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
+// One block step j (1-based) of one sequence: Alg. 1 lines 3-9.  The n-space passes and
+// the coefficient kernels (lines 3-8) run on `st`; the sketch and the sketch-space QR
+// update (line 9) on `side`, which overlaps the next step's passes.
+void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t side) {
   const int R = c->R, K = c->K;
   const int nwin = std::min(K, j);
   Win win{};
   for (int i = 0; i < nwin; ++i) win.p[i] = q.slot(j - nwin + 1 + i);
   const bool timing = (c->cflags & 1) != 0;
-  const int G = c->G;
+  const int G = pass_parts(c, q);
   TimedPair t1{}, t2{}, t3{};
   // ---- a1 + a2 coefficients: pass 1
   if (timing) { t1 = ev_get(c, 0); CK(cudaEventRecord(t1.a, st)); }
-  launch_pass1(c, q, win, nwin, st);
+  launch_pass1(c, q, win, nwin, j, st);
   if (timing) { CK(cudaEventRecord(t1.b, st)); c->timed.push_back(t1); }
   SYLV_DISPATCH_RK(R, K, {
     k_coef1<R_, K_><<<1, kThreads, 0, st>>>(q.part1, G, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
   });
-  // ---- a2 update + a3 Gram: pass 2 (writes Z_{j+1} = W')
+  // ---- a2 update + a3 Gram: pass 2 (writes Z_{j+1} = W' into the ring slot that the
+  //      sketch of step j-K-1 read)
+  const int ne = K + 2;
+  if (j - K - 1 >= 1 && side != st) CK(cudaStreamWaitEvent(st, q.ev_sk[(j - K - 1) % ne], 0));
   if (timing) { t2 = ev_get(c, 1); CK(cudaEventRecord(t2.a, st)); }
-  launch_pass2<true>(c, q, win, nwin, q.Yt, q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1), st);
+  launch_pass2<true>(c, q, win, nwin, j, q.Yt, q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1), st);
   if (timing) { CK(cudaEventRecord(t2.b, st)); c->timed.push_back(t2); }
   SYLV_DISPATCH_RK(R, K, {
     k_coef2<R_, K_><<<1, kThreads, 0, st>>>(q.part2, G, j, q.Rall, q.Hc, q.hn2, q.flags);
   });
   count(c, 2);
   CK(cudaGetLastError());
+  // ---- H column j mirror (main stream), then hand over to the side stream
+  const size_t hb = (size_t)(K + 1) * R * R;
+  CK(cudaMemcpyAsync(q.Hh + (size_t)j * hb, q.Hc + (size_t)j * hb, hb * sizeof(double),
+                     cudaMemcpyDeviceToHost, st));
+  if (side != st) {
+    CK(cudaEventRecord(q.ev_c2[j % ne], st));
+    CK(cudaStreamWaitEvent(side, q.ev_c2[j % ne], 0));
+  }
+  st = side;
   // ---- a4: w = (S W') R_{j+1}   (a5 timing includes the sketch)
   if (timing) { t3 = ev_get(c, 2); CK(cudaEventRecord(t3.a, st)); }
+  TimedPair t4{};
+  if (timing) { t4 = ev_get(c, 3); CK(cudaEventRecord(t4.a, st)); }
   launch_sketch(c, q, q.slot(j + 1), R, q.Rall + (int64_t)(j + 1) * R * R, q.w, st);
+  if (timing) { CK(cudaEventRecord(t4.b, st)); c->timed.push_back(t4); }
+  if (side != c->st && side != c->st2) CK(cudaEventRecord(q.ev_sk[j % ne], st));
   // ---- a5: block CGS2 against Q (m = j R columns); CholQR2; T column
   const int m = j * R;
   const dim3 gq((m + kWarps - 1) / kWarps, c->RT);
@@ -502,10 +659,7 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
   count(c);
   CK(cudaGetLastError());
   if (timing) { CK(cudaEventRecord(t3.b, st)); c->timed.push_back(t3); }
-  // ---- mirrors: H column j, T columns m..m+R (rows 0..m+R)
-  const size_t hb = (size_t)(K + 1) * R * R;
-  CK(cudaMemcpyAsync(q.Hh + (size_t)j * hb, q.Hc + (size_t)j * hb, hb * sizeof(double),
-                     cudaMemcpyDeviceToHost, st));
+  // ---- mirror: T columns m..m+R (rows 0..m+R)
   CK(cudaMemcpy2DAsync(q.Th + (int64_t)m * q.ldT, q.ldT * sizeof(double), q.Tdev + (int64_t)m * q.ldT,
                        q.ldT * sizeof(double), (size_t)(m + R) * sizeof(double), R,
                        cudaMemcpyDeviceToHost, st));
@@ -574,11 +728,14 @@ const char* sylv_sketch_last_error(const sylv_ctx* ctx) { return ctx ? ctx->err.
 void sylv_sketch_destroy(sylv_ctx* ctx) {
   if (!ctx) return;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
-  if (ctx->st2) cudaStreamSynchronize(ctx->st2);
+  for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4})
+    if (s) cudaStreamSynchronize(s);
   for (auto& q : ctx->seq) free_seq(q);
-  if (ctx->st2) cudaStreamDestroy(ctx->st2);
+  for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4})
+    if (s) cudaStreamDestroy(s);
   if (ctx->fork) cudaEventDestroy(ctx->fork);
-  if (ctx->join) cudaEventDestroy(ctx->join);
+  for (cudaEvent_t e : ctx->join)
+    if (e) cudaEventDestroy(e);
   for (auto& p : ctx->free_events) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto& p : ctx->timed) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   delete ctx;
@@ -634,7 +791,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     c->tileQ = (c->s + c->RT - 1) / c->RT;
     c->CC = (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * c->sm + (c->s / 256)) / std::max<int64_t>(1, c->s / 256)));
     // sketch kernel: whole sketch column (s doubles) in shared memory per CTA
-    c->sk_smem = (size_t)c->s * sizeof(double);
+    c->sk_smem = (size_t)sketch_smem_doubles(c->s, c->zeta) * sizeof(double);
     int max_optin = 0;
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     if (c->sk_smem > (size_t)max_optin)
@@ -650,8 +807,10 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     c->gpc = (ngroups + c->nchunk - 1) / c->nchunk;
     c->nchunk = (int)((ngroups + c->gpc - 1) / c->gpc);
     CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+    for (cudaEvent_t& e : c->join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     init_sequence(c, c->seq[0], 0, A, false, C1, cfg->seed_u);
     init_sequence(c, c->seq[1], 1, B, true, C2, cfg->seed_v);
     return SYLV_OK;
@@ -666,19 +825,26 @@ sylv_status sylv_sketch_step(sylv_ctx* c, int32_t nsteps, int32_t* d_done) {
     const int first = c->d_done + 1;
     const int last = std::min(c->dmax, c->d_done + std::max(0, nsteps));
     if (last >= first) {
-      // U on the context stream, V on st2 (independent sequences; their kernels overlap)
-      CK(cudaEventRecord(c->fork, c->st));
-      CK(cudaStreamWaitEvent(c->st2, c->fork, 0));
+      // U passes on the context stream, V passes on st2 (independent sequences); each
+      // sequence's sketch-space work on its own side stream.  Serial mode: all on st.
+      const bool serial = (c->cflags & 2) != 0;
+      cudaStream_t others[3] = {c->st2, c->st3, c->st4};
+      if (!serial) {
+        CK(cudaEventRecord(c->fork, c->st));
+        for (cudaStream_t s : others) CK(cudaStreamWaitEvent(s, c->fork, 0));
+      }
       for (int j = first; j <= last; ++j) {
-        step_sequence(c, c->seq[0], j, c->st);
-        step_sequence(c, c->seq[1], j, (c->cflags & 2) ? c->st : c->st2);
+        step_sequence(c, c->seq[0], j, c->st, serial ? c->st : c->st3);
+        step_sequence(c, c->seq[1], j, serial ? c->st : c->st2, serial ? c->st : c->st4);
+      }
+      if (!serial) {
+        for (int i = 0; i < 3; ++i) {
+          CK(cudaEventRecord(c->join[i], others[i]));
+          CK(cudaStreamWaitEvent(c->st, c->join[i], 0));
+        }
       }
       CK(cudaMemcpyAsync(c->seq[1].flags_h + first, c->seq[1].flags + first, (last - first + 2) * sizeof(int),
-                         cudaMemcpyDeviceToHost, c->st2));
-      CK(cudaEventRecord(c->join, c->st2));
-      CK(cudaStreamWaitEvent(c->st, c->join, 0));
-    }
-    if (last >= first) {
+                         cudaMemcpyDeviceToHost, c->st));
       CK(cudaMemcpyAsync(c->seq[0].flags_h + first, c->seq[0].flags + first, (last - first + 2) * sizeof(int),
                          cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
@@ -820,7 +986,8 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
             const int nwin = std::min(K, jp);
             Win win{};
             for (int i = 0; i < nwin; ++i) win.p[i] = rslot(jp - nwin + 1 + i);
-            launch_pass2<false>(c, q, win, nwin, nullptr, q.Kc + (int64_t)jp * (1 + K) * r * r, rslot(j), c->st);
+            launch_pass2<false>(c, q, win, nwin, jp, nullptr, q.Kc + (int64_t)jp * (1 + K) * r * r, rslot(j), c->st,
+                                /*allow_tma=*/false);
           }
           if (j - j0 + 1 == C || j == d) {
             ChunkPtrs cp{};

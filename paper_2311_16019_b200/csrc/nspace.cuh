@@ -386,70 +386,108 @@ __global__ void __launch_bounds__(kThreads) k_pass2_r8(OpParams op, Win win, int
 // =====================================================================================
 // Sparse-sign sketch of an SoA block, shared-memory privatised (a4)
 // =====================================================================================
-// grid (nchunk, R).  CTA (chunk, c) accumulates column c of S X for the rows of its chunk
-// in shared memory (s doubles); warp w owns bucket(s) t = w, w + 8, ... so warps never
-// write the same address; within a warp the 32 rows of a group hit 32 distinct, cyclically
-// consecutive slots, so the read-modify-write is conflict-free.  Group
-// hashes are computed 32 groups at a time (one per lane) and broadcast with shuffles.
-// Output: partial[(chunk*R + c)*s + q].
+// grid (nchunk, R), one CTA per SM (the whole sketch column lives in shared memory).
+// CTA (chunk, c) accumulates column c of S X over the rows of its chunk.
+//
+// Tiles of kSkWarps x kSkG groups of 32 rows: warp w loads ITS OWN kSkG groups into
+// registers (coalesced 256-byte loads, double-buffered: the next tile is in flight while
+// this one is scattered), so every element is read from HBM exactly once.  The scatter
+// runs in P = max(zeta, 8) phases separated by __syncthreads(); in phase p warp w owns
+// bucket t = (w + p) mod P, so no two warps ever touch the same bucket at the same time
+// and no atomics are needed.  Per phase, lane 3g + q (< 3 kSkG) evaluates hash q of group
+// g; the group's slot window base .. base+31 is written WITHOUT wrapping into
+// a bucket padded to b + 32 slots (the 32 pad slots are folded back onto slots 0..31 at the
+// end), the 32 lanes hit 32 distinct consecutive slots (conflict-free), and the sign is
+// applied by flipping the sign bit.  Output: partial[(chunk*R + c)*s + q].
+constexpr int kSkWarps = 8;
+constexpr int kSkG = 8;            // groups per warp per tile (3 kSkG <= 32 hash lanes)
+
+__host__ __device__ constexpr int64_t sketch_smem_doubles(int64_t s, int zeta) { return s + 32 * (int64_t)zeta; }
+
 template <int R>
-__global__ void __launch_bounds__(kThreads) k_sketch_cols(int64_t n, const double* __restrict__ X, int64_t ld,
-                                                          SketchParams sp, int64_t groups_per_chunk,
-                                                          double* __restrict__ partial) {
+__global__ void __launch_bounds__(kSkWarps * 32, 1) k_sketch_cols(int64_t n, const double* __restrict__ X,
+                                                                  int64_t ld, SketchParams sp,
+                                                                  int64_t groups_per_chunk,
+                                                                  double* __restrict__ partial) {
   extern __shared__ double skm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.y;
-  const uint32_t b = sp.b;
+  const uint32_t b = sp.b, bp = sp.b + 32u;           // bucket height, padded height
   const int64_t s = (int64_t)b * sp.zeta;
-  for (int64_t e = threadIdx.x; e < s; e += kThreads) skm[e] = 0.0;
-  __syncthreads();
+  const int64_t sz = (int64_t)bp * sp.zeta;
+  for (int64_t e = threadIdx.x; e < sz; e += kSkWarps * 32) skm[e] = 0.0;
   const int64_t ngroups = (n + 31) >> 5;
   const int64_t g0 = (int64_t)blockIdx.x * groups_per_chunk;
   const int64_t g1 = min(ngroups, g0 + groups_per_chunk);
   const double* __restrict__ xc = X + c * ld;
-  for (uint32_t t = warp; t < sp.zeta; t += kWarps) {
-    double* bucket = skm + (int64_t)t * b;
-    for (int64_t gb = g0; gb < g1; gb += 32) {
-      // lane computes the three group hashes of group gb + lane
-      const uint32_t m = (uint32_t)(gb + lane);
-      const uint32_t h0 = group_hash(sp, m, t, 0);
-      const uint32_t h1 = group_hash(sp, m, t, 1);
-      const uint32_t h2 = group_hash(sp, m, t, 2);
-      const uint32_t base = __umulhi(h0, b);
-      const uint32_t ng = (uint32_t)(g1 - gb < 32 ? g1 - gb : 32);
-      for (uint32_t k0 = 0; k0 < ng; k0 += 8) {
-        double v[8];
+  const uint32_t P = sp.zeta > (uint32_t)kSkWarps ? sp.zeta : (uint32_t)kSkWarps;
+  constexpr int64_t kTile = (int64_t)kSkWarps * kSkG;   // groups per tile
+  const uint32_t hq = (uint32_t)lane % 3u, hg = (uint32_t)lane / 3u;   // hash lane -> (q, group)
+
+  double v[kSkG], vn[kSkG];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int64_t row = ((gb + k0 + u) << 5) + lane;
-          v[u] = (k0 + u < ng && row < n) ? __ldg(xc + row) : 0.0;
-        }
+  for (int g = 0; g < kSkG; ++g) {
+    const int64_t grp = g0 + (int64_t)warp * kSkG + g;
+    const int64_t row = (grp << 5) + lane;
+    vn[g] = (grp < g1 && row < n) ? __ldg(xc + row) : 0.0;
+  }
+  __syncthreads();
+  for (int64_t tg = g0; tg < g1; tg += kTile) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t kk = k0 + u;
-          const uint32_t bs = __shfl_sync(SYLV_FULL_MASK, base, kk & 31);
-          const uint32_t p1 = __shfl_sync(SYLV_FULL_MASK, h1, kk & 31);
-          const uint32_t sg = __shfl_sync(SYLV_FULL_MASK, h2, kk & 31);
-          if (kk < ng) {
+    for (int g = 0; g < kSkG; ++g) v[g] = vn[g];
+    if (tg + kTile < g1) {                               // prefetch the next tile
+#pragma unroll
+      for (int g = 0; g < kSkG; ++g) {
+        const int64_t grp = tg + kTile + (int64_t)warp * kSkG + g;
+        const int64_t row = (grp << 5) + lane;
+        vn[g] = (grp < g1 && row < n) ? __ldg(xc + row) : 0.0;
+      }
+    }
+    const int64_t mybase = tg + (int64_t)warp * kSkG;      // first group of this warp
+    for (uint32_t p = 0; p < P; ++p) {
+      const uint32_t t = (warp + p) % P;
+      if (t < sp.zeta && mybase < g1) {
+        const uint32_t h = group_hash(sp, (uint32_t)mybase + hg, t, hq);
+        const uint32_t hb = (hq == 0) ? __umulhi(h, b) : h;   // lane 3g: base; 3g+1: a,c; 3g+2: signs
+        double* bucket = skm + (int64_t)t * bp;
+        if (b >= 32u) {
+#pragma unroll
+          for (int g = 0; g < kSkG; ++g) {
+            const uint32_t base = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g);
+            const uint32_t p1 = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g + 1);
+            const uint32_t sg = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g + 2);
             const uint32_t a = 2u * (p1 & 15u) + 1u;
             const uint32_t cc = (p1 >> 4) & 31u;
-            uint32_t slot = bs + ((a * (uint32_t)lane + cc) & 31u);
-            const double val = ((sg >> lane) & 1u) ? -v[u] : v[u];
-            if (b >= 32u) {
-              slot = slot >= b ? slot - b : slot;
-              bucket[slot] += val;
-              __syncwarp();
-            } else {
-              atomicAdd(bucket + (slot % b), val);   // tiny buckets: slots of a group collide
-            }
+            const uint32_t slot = base + ((a * (uint32_t)lane + cc) & 31u);     // < b + 32
+            const int hi = __double2hiint(v[g]) ^ (int)((sg << (31 - lane)) & 0x80000000u);
+            bucket[slot] += __hiloint2double(hi, __double2loint(v[g]));
+          }
+        } else {
+          // tiny buckets (b < 32): the 32 rows of a group collide; shared atomics
+#pragma unroll
+          for (int g = 0; g < kSkG; ++g) {
+            const uint32_t base = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g);
+            const uint32_t p1 = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g + 1);
+            const uint32_t sg = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g + 2);
+            const uint32_t a = 2u * (p1 & 15u) + 1u;
+            const uint32_t cc = (p1 >> 4) & 31u;
+            const uint32_t sl = (base + ((a * (uint32_t)lane + cc) & 31u)) % b;
+            atomicAdd(bucket + sl, ((sg >> lane) & 1u) ? -v[g] : v[g]);
           }
         }
       }
+      __syncthreads();
     }
   }
   __syncthreads();
+  // fold the pad slots b .. b+31 of every bucket onto slots 0 .. 31, scale, write
   double* out = partial + ((int64_t)blockIdx.x * R + c) * s;
-  for (int64_t e = threadIdx.x; e < s; e += kThreads) out[e] = skm[e] * sp.scale;
+  for (int64_t q = threadIdx.x; q < s; q += kSkWarps * 32) {
+    const int64_t t = q / b, i = q - t * b;
+    double v0 = skm[t * bp + i];
+    if (i < 32 && b >= 32u) v0 += skm[t * bp + b + i];
+    out[q] = v0 * sp.scale;
+  }
 }
 
 // w[q*R + c] = sum_a (sum_chunk partial[(chunk*R + a)*s + q]) M[a*R + c]  (M = identity if null)

@@ -18,38 +18,70 @@ __device__ __forceinline__ double sum_parts(const double* __restrict__ partial, 
   return s;
 }
 
+// Block-wide deterministic sums of per-CTA partials: out[e] = sum_p partial[p*len + e] for
+// e < nelem.  Warp w reduces elements w, w + nwarps, ...; lane l adds parts l, l + 32, ...
+// and the 32 lane sums are combined by a fixed butterfly (same order on every run).
+__device__ __forceinline__ void block_sum_parts(const double* __restrict__ partial, int nparts, int64_t len,
+                                                int nelem, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = warp; e < nelem; e += nw) {
+    double s = 0.0;
+    for (int p = lane; p < nparts; p += 32) s += partial[(int64_t)p * len + e];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(SYLV_FULL_MASK, s, off);
+    if (lane == 0) out[e] = s;
+  }
+}
+
 // h_{i,j} = R_i^T P_i R_j, K_i = R_i h_{i,j}; Kc[j] = [R_j, K_0..]; Hc[j] = [h_.., 0.., h_{j+1,j}]
+// (one CTA; thread per matrix entry for the r x r products)
 template <int R, int K>
 __global__ void k_coef1(const double* __restrict__ partial, int nparts, int nwin, int j,
                         const double* __restrict__ Rall, double* __restrict__ Kc,
                         double* __restrict__ Hc, double* __restrict__ hnorm2) {
-  __shared__ double P[K * R * R];
-  for (int e = threadIdx.x; e < nwin * R * R; e += blockDim.x)
-    P[e] = sum_parts(partial, nparts, K * R * R, e);
+  constexpr int RR = R * R;
+  __shared__ double P[K * RR], T1[K * RR], Hs[K * RR];
+  block_sum_parts(partial, nparts, K * RR, nwin * RR, P);
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  const double* Rd = Rall + (int64_t)j * R * R;
-  double* Kout = Kc + (int64_t)j * (1 + K) * R * R;
-  double* Hout = Hc + (int64_t)j * (K + 1) * R * R;
-  for (int e = 0; e < R * R; ++e) Kout[e] = Rd[e];
-  double tmp[R * R], h[R * R], kk[R * R];
-  double hn = 0.0;
-  for (int i = 0; i < K; ++i) {
+  const double* Rd = Rall + (int64_t)j * RR;
+  double* Kout = Kc + (int64_t)j * (1 + K) * RR;
+  double* Hout = Hc + (int64_t)j * (K + 1) * RR;
+  for (int e = threadIdx.x; e < K * RR; e += blockDim.x) {      // T1_i = R_i^T P_i
+    const int i = e / RR, a = (e % RR) / R, c = e % R;
+    double v = 0.0;
     if (i < nwin) {
-      const double* Ri = Rall + (int64_t)(j - nwin + 1 + i) * R * R;
-      mtm<R>(Ri, P + i * R * R, tmp);
-      mm<R>(tmp, Rd, h);
-      mm<R>(Ri, h, kk);
-      for (int e = 0; e < R * R; ++e) {
-        Hout[i * R * R + e] = h[e];
-        Kout[(1 + i) * R * R + e] = kk[e];
-        hn += h[e] * h[e];
-      }
-    } else {
-      for (int e = 0; e < R * R; ++e) Hout[i * R * R + e] = 0.0;
+      const double* Ri = Rall + (int64_t)(j - nwin + 1 + i) * RR;
+      for (int p = 0; p < R; ++p) v += Ri[p * R + a] * P[i * RR + p * R + c];
     }
+    T1[e] = v;
   }
-  hnorm2[j] = hn;
+  __syncthreads();
+  for (int e = threadIdx.x; e < K * RR; e += blockDim.x) {      // h_i = T1_i R_d
+    const int i = e / RR, a = (e % RR) / R, c = e % R;
+    double v = 0.0;
+    if (i < nwin)
+      for (int p = 0; p < R; ++p) v += T1[i * RR + a * R + p] * Rd[p * R + c];
+    Hs[e] = v;
+    Hout[e] = v;
+  }
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) Kout[e] = Rd[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < K * RR; e += blockDim.x) {      // K_i = R_i h_i
+    const int i = e / RR, a = (e % RR) / R, c = e % R;
+    double v = 0.0;
+    if (i < nwin) {
+      const double* Ri = Rall + (int64_t)(j - nwin + 1 + i) * RR;
+      for (int p = 0; p < R; ++p) v += Ri[a * R + p] * Hs[i * RR + p * R + c];
+    }
+    Kout[RR + e] = v;
+  }
+  if (threadIdx.x < 32) {                                       // ||h_{.,j}||_F^2, fixed order
+    double hn = 0.0;
+    for (int e = threadIdx.x; e < nwin * RR; e += 32) hn += Hs[e] * Hs[e];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) hn += __shfl_xor_sync(SYLV_FULL_MASK, hn, off);
+    if (threadIdx.x == 0) hnorm2[j] = hn;
+  }
 }
 
 // G = W'^T W' -> h_{j+1,j} = chol(G) (upper, positive diagonal), R_{j+1} = h^{-1};
@@ -60,7 +92,7 @@ __global__ void k_coef2(const double* __restrict__ partial, int nparts, int j,
                         double* __restrict__ Rall, double* __restrict__ Hc,
                         const double* __restrict__ hnorm2, int* __restrict__ flags) {
   __shared__ double G[R * R];
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) G[e] = sum_parts(partial, nparts, R * R, e);
+  block_sum_parts(partial, nparts, R * R, R * R, G);
   __syncthreads();
   if (threadIdx.x != 0) return;
   double h[R * R], hi[R * R];
@@ -83,7 +115,7 @@ __global__ void k_coef2(const double* __restrict__ partial, int nparts, int j,
     Hout[e] = h[e];
     Rn[e] = hi[e];
   }
-  flags[j] |= fl;
+  if (fl) atomicOr(flags + j, fl);
 }
 
 // tau = chol(sum of Gram partials) (upper); tinv = tau^{-1}; if prev: tau_out = tau * prev.
@@ -93,12 +125,12 @@ __global__ void k_chol_small(const double* __restrict__ partial, int nparts,
                              double* __restrict__ tau_out, double* __restrict__ tinv_out,
                              const double* __restrict__ prev, int* __restrict__ flags, int slot) {
   __shared__ double G[R * R];
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) G[e] = sum_parts(partial, nparts, R * R, e);
+  block_sum_parts(partial, nparts, R * R, R * R, G);
   __syncthreads();
   if (threadIdx.x != 0) return;
   double t[R * R], ti[R * R];
   if (!chol_upper<R>(G, t)) {
-    flags[slot] |= 4;
+    atomicOr(flags + slot, 4);
     for (int e = 0; e < R * R; ++e) t[e] = (e % (R + 1) == 0) ? 1.0 : 0.0;
   }
   inv_upper<R>(t, ti);

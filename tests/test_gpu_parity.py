@@ -28,6 +28,10 @@ CASES = {
     "2d-r1": dict(kind="stencil2d", N=23, r=1, k=2, d_max=60),
     "2d-r4": dict(kind="stencil2d", N=37, r=4, k=2, d_max=60),
     "3d-r8k3": dict(kind="stencil3d", N=19, r=8, k=3, d_max=55),
+    # even N: the 2.5-D TMA passes (tiles 32 x 4, ragged in x and y)
+    "3d-r8k3-tma": dict(kind="stencil3d", N=34, r=8, k=3, d_max=55),
+    "3d-r8k2-tma": dict(kind="stencil3d", N=20, r=8, k=2, d_max=55),
+    "3d-r8k4-tma": dict(kind="stencil3d", N=26, r=8, k=4, d_max=55),
     "3d-r2k1": dict(kind="stencil3d", N=11, r=2, k=1, d_max=55),
     "csr-r2": dict(kind="csr", n=20011, nnz_off=20, band=300, r=2, k=2, d_max=55),
     "csr-r4k4": dict(kind="csr", n=5003, nnz_off=6, band=40, r=4, k=4, d_max=55),
@@ -103,7 +107,7 @@ def test_window_blocks(name):
             assert _rel(Ug, seq.U[j]) <= 1e-9, (which, j)
 
 
-@pytest.mark.parametrize("name", ["2d-r1", "csr-r2", "3d-r8k3"])
+@pytest.mark.parametrize("name", ["2d-r1", "csr-r2", "3d-r8k3", "3d-r8k3-tma"])
 def test_solution_and_true_residual(name):
     cfg, csr, C1, C2, orc, gpu = _setup(name)
     d = 6 if cfg.kind == "csr" else 30          # the banded CSR case converges in ~8 steps
@@ -195,3 +199,23 @@ def test_sketch_full_config_sizes(name):
         want = sparse_sign.apply_hashed(X, cfg.s, cfg.zeta, seed)
         assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
     gpu.close()
+
+
+@pytest.mark.parametrize("name", ["3d-r8k3-tma", "3d-r8k4-tma"])
+def test_tma_passes_match_generic_passes(name):
+    """The 2.5-D TMA passes and the generic DMMA passes compute the same recurrence: window
+    blocks and per-step rho agree to rounding (1e-12 relative) over 20 steps."""
+    cfg = inputs.small_config(**CASES[name])
+    C1, C2 = inputs.make_rhs(cfg)
+    st = torch.cuda.current_stream().cuda_stream
+    a = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), stream=st)
+    b = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), stream=st,
+                           tma=False)
+    for d in range(1, 21):
+        a.step(1)
+        b.step(1)
+        ra, rb = a.residual(d)[1], b.residual(d)[1]
+        assert abs(ra - rb) <= 1e-12 * rb + 1e-15, (d, ra, rb)
+    for which in (0, 1):
+        for j in range(22 - cfg.k, 22):
+            assert _rel(a.get_block(which, j), b.get_block(which, j)) <= 1e-12, (which, j)

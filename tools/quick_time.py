@@ -13,9 +13,10 @@ csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
 C1, C2 = inputs.make_rhs(cfg)
 print(f"{name}: gen {time.time()-t0:.1f}s", flush=True)
 t0 = time.time()
-serial = len(sys.argv) > 3 and sys.argv[3] == "serial"
+serial = "serial" in sys.argv[3:]
+notma = "notma" in sys.argv[3:]
 g = pkg.from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr, timing=True,
-                    stream=torch.cuda.current_stream().cuda_stream, serial=serial)
+                    stream=torch.cuda.current_stream().cuda_stream, serial=serial, tma=not notma)
 print("serial" if serial else "two streams")
 torch.cuda.synchronize(); print(f"init {time.time()-t0:.2f}s", flush=True)
 g.step(3); g.reset_stats()
@@ -26,7 +27,7 @@ ms = e0.elapsed_time(e1)
 s = g.stats()
 R, K, n = cfg.r, cfg.k, cfg.n
 print(f"{name} {steps} steps: {ms:.2f} ms total, {ms/steps:.3f} ms/step, d={d}")
-for k in ("pass1", "pass2", "skqr"):
+for k in ("pass1", "pass2", "skqr", "sketch"):
     nn = s['n_'+k]
     if nn: print(f"  {k}: {s['ms_'+k]/nn*1e3:.1f} us/launch over {nn}")
 bp1 = 8*n*R*K; bp2 = 8*n*R*(K+1)
