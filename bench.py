@@ -58,10 +58,12 @@ def algorithmic_bytes(cfg):
         mat = 12 * nnz + 4 * (n + 1)
         p1 = mat + blk * (k + 1)          # A, Z_d gathers (counted once), k-1 other window blocks, write AZ
         p2 = blk * (k + 1) + blk          # read AZ + k window blocks, write W'
-        return {"pass1": p1, "pass2": p2, "step": 2 * (p1 + p2)}
+        return {"pass1": p1, "pass2": p2, "sketch": blk, "step": 2 * (p1 + p2)}
     p1 = blk * k
     p2 = blk * (k + 1)
-    return {"pass1": p1, "pass2": p2, "step": 2 * (p1 + p2)}
+    # the sketch kernel reads the new block once (8 n r bytes); not part of SURVEY's B_n,
+    # which assumes the sketch fused into pass 2
+    return {"pass1": p1, "pass2": p2, "sketch": blk, "step": 2 * (p1 + p2)}
 
 
 class ClockSampler:
@@ -209,6 +211,14 @@ def main():
     C1d = torch.from_numpy(C1).to(dev)
     C2d = torch.from_numpy(C2).to(dev)
     solver = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, timing=True, stream=stream.cuda_stream)
+    # per-kernel attribution run (serial stream, CUDA events around each launch), untimed
+    attr = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, timing=True, stream=stream.cuda_stream, serial=True)
+    attr.step(args.warmup)
+    attr.reset_stats()
+    attr.step(min(args.steps, 10))
+    torch.cuda.synchronize()
+    attr_stats = attr.stats()
+    attr.close()
 
     def barrier():
         if ws > 1:
@@ -229,8 +239,8 @@ def main():
         torch.cuda.synchronize()
         barrier()
     ms = e0.elapsed_time(e1)
-    stats = solver.stats()
-    launches = stats["launches"] - l0
+    stats = attr_stats
+    launches = solver.stats()["launches"] - l0
     if ws > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -244,11 +254,13 @@ def main():
     peak, peak_src = _peaks()
     p2_ms = stats["ms_pass2"] / max(1, stats["n_pass2"])
     p1_ms = stats["ms_pass1"] / max(1, stats["n_pass1"])
-    # dominant kernel = the slower of the two n-space passes
-    if p2_ms >= p1_ms:
-        dom, dom_ms, dom_bytes = "pass2", p2_ms, ab["pass2"]
-    else:
-        dom, dom_ms, dom_bytes = "pass1", p1_ms, ab["pass1"]
+    sk_ms = stats["ms_sketch"] / max(1, stats["n_sketch"])
+    # dominant kernel = the largest per-launch device time among the hot-path kernels
+    # (each launches once per sequence per step); times are CUDA events on the launching
+    # stream (serial mode: no overlap inflates them)
+    cand = {"pass1": p1_ms, "pass2": p2_ms, "sketch": sk_ms}
+    dom = max(cand, key=cand.get)
+    dom_ms, dom_bytes = cand[dom], ab[dom]
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = traffic_for(cfg.name, dom)
     step_gbs = ab["step"] / (ms / args.steps * 1e-3) / 1e9
@@ -299,9 +311,14 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
-                         "pass1_ms": p1_ms, "pass2_ms": p2_ms,
-                         "skqr_ms": stats["ms_skqr"] / max(1, stats["n_skqr"])},
-            "n_space_GBps": step_gbs, "n_space_frac_of_8TBps": step_gbs / NOMINAL_HBM_GBS,
+                         "kernels": {k: {"ms": v, "GBps": ab[k] / (v * 1e-3) / 1e9,
+                                         "frac": ab[k] / (v * 1e-3) / 1e9 / peak} for k, v in cand.items()},
+                         "skqr_ms": stats["ms_skqr"] / max(1, stats["n_skqr"]),
+                         "note": ("sketch: hashed sparse-sign scatter, bounded by shared-memory "
+                                  "read-modify-write latency, not by HBM" if dom == "sketch" else "")},
+            "step_roofline": {"bytes_per_step": ab["step"], "GBps": step_gbs, "frac": step_gbs / peak,
+                              "frac_of_8TBps": step_gbs / NOMINAL_HBM_GBS,
+                              "what": "SURVEY §8(d) B_n per block step (both sequences) / device step time"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }

@@ -476,9 +476,10 @@ void launch_pass2(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, con
 // S X for an SoA block -> w (s x R row-major) = (S X) M  (M = nullptr: identity)
 void launch_sketch(sylv_ctx* c, Sequence& q, const double* X, int R, const double* M, double* w, cudaStream_t st) {
   const dim3 g(c->nchunk, R);
+  const int nchunk = c->nchunk;
   SYLV_DISPATCH_R(R, {
-    k_sketch_cols<R_><<<g, kThreads, c->sk_smem, st>>>(c->n, X, q.ld, q.sp, c->gpc, q.skpart);
-    k_sketch_reduce<R_><<<(int)std::min<int64_t>(4 * c->sm, (q.s + 255) / 256), 256, 0, st>>>(q.skpart, c->nchunk, q.s, M, w);
+    k_sketch_cols<R_><<<g, kSkWarps * 32, c->sk_smem, st>>>(c->n, X, q.ld, q.sp, c->gpc, q.skpart);
+    k_sketch_reduce<R_><<<(int)std::min<int64_t>(4 * c->sm, (q.s + 255) / 256), 256, 0, st>>>(q.skpart, nchunk, q.s, M, w);
   });
   count(c, 2);
 }

@@ -391,38 +391,49 @@ __global__ void __launch_bounds__(kThreads) k_pass2_r8(OpParams op, Win win, int
 //
 // Tiles of kSkWarps x kSkG groups of 32 rows: warp w loads ITS OWN kSkG groups into
 // registers (coalesced 256-byte loads, double-buffered: the next tile is in flight while
-// this one is scattered), so every element is read from HBM exactly once.  The scatter
-// runs in P = max(zeta, 8) phases separated by __syncthreads(); in phase p warp w owns
-// bucket t = (w + p) mod P, so no two warps ever touch the same bucket at the same time
-// and no atomics are needed.  Per phase, lane 3g + q (< 3 kSkG) evaluates hash q of group
-// g; the group's slot window base .. base+31 is written WITHOUT wrapping into
-// a bucket padded to b + 32 slots (the 32 pad slots are folded back onto slots 0..31 at the
-// end), the 32 lanes hit 32 distinct consecutive slots (conflict-free), and the sign is
-// applied by flipping the sign bit.  Output: partial[(chunk*R + c)*s + q].
+// this one is scattered), so every element is read from HBM exactly once.
+// Per tile, each warp first evaluates the three hashes of all its
+// (group, bucket) pairs (4 pairs per lane, independent chains) and stores one 16-byte
+// record per pair in its own shared-memory area: {byte offset of the slot window, a, 8c,
+// sign bits}.  The scatter then runs in
+// P = max(zeta, 8) phases separated by __syncthreads(); in phase p warp w owns bucket
+// t = (w + p) mod P, so no two warps ever touch the same bucket at the same time and no
+// atomics are needed.  A group's record is one broadcast LDS.128; its 32 rows hit the 32
+// distinct consecutive slots base .. base+31 of a bucket padded to b + 32 slots (no wrap
+// test; the pad is folded back onto slots 0..31 at the end), conflict-free; the sign is
+// applied by flipping the sign bit.  Two groups whose windows are disjoint issue their
+// read-modify-writes together.
+// Output: partial[(chunk*R + c)*s + q].
 constexpr int kSkWarps = 8;
-constexpr int kSkG = 8;            // groups per warp per tile (3 kSkG <= 32 hash lanes)
+constexpr int kSkG = 16;           // groups per warp per tile
 
-__host__ __device__ constexpr int64_t sketch_smem_doubles(int64_t s, int zeta) { return s + 32 * (int64_t)zeta; }
+__host__ __device__ constexpr int64_t sketch_smem_doubles(int64_t s, int zeta) {
+  return s + 32 * (int64_t)zeta + (int64_t)kSkWarps * kSkG * zeta * 2;   // buckets + hash records
+}
 
 template <int R>
 __global__ void __launch_bounds__(kSkWarps * 32, 1) k_sketch_cols(int64_t n, const double* __restrict__ X,
                                                                   int64_t ld, SketchParams sp,
                                                                   int64_t groups_per_chunk,
                                                                   double* __restrict__ partial) {
-  extern __shared__ double skm[];
+  extern __shared__ __align__(16) double skm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.y;
   const uint32_t b = sp.b, bp = sp.b + 32u;           // bucket height, padded height
-  const int64_t s = (int64_t)b * sp.zeta;
-  const int64_t sz = (int64_t)bp * sp.zeta;
+  const uint32_t zeta = sp.zeta;
+  const int64_t s = (int64_t)b * zeta;
+  const int64_t sz = (int64_t)bp * zeta;
+  uint4* rec = reinterpret_cast<uint4*>(skm + sz) + (size_t)warp * kSkG * zeta;   // [g][t]
   for (int64_t e = threadIdx.x; e < sz; e += kSkWarps * 32) skm[e] = 0.0;
   const int64_t ngroups = (n + 31) >> 5;
   const int64_t g0 = (int64_t)blockIdx.x * groups_per_chunk;
   const int64_t g1 = min(ngroups, g0 + groups_per_chunk);
   const double* __restrict__ xc = X + c * ld;
-  const uint32_t P = sp.zeta > (uint32_t)kSkWarps ? sp.zeta : (uint32_t)kSkWarps;
+  const uint32_t P = zeta > (uint32_t)kSkWarps ? zeta : (uint32_t)kSkWarps;
   constexpr int64_t kTile = (int64_t)kSkWarps * kSkG;   // groups per tile
-  const uint32_t hq = (uint32_t)lane % 3u, hg = (uint32_t)lane / 3u;   // hash lane -> (q, group)
+  const uint32_t l8 = 8u * (uint32_t)lane;
+  const uint32_t npairs = (uint32_t)kSkG * zeta;      // (group, bucket) pairs per warp per tile
+  char* const sb = reinterpret_cast<char*>(skm);
 
   double v[kSkG], vn[kSkG];
 #pragma unroll
@@ -444,35 +455,59 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) k_sketch_cols(int64_t n, con
       }
     }
     const int64_t mybase = tg + (int64_t)warp * kSkG;      // first group of this warp
+    // hash records of this warp's (group, bucket) pairs
+    for (uint32_t e = lane; e < npairs; e += 32) {
+      const uint32_t g = e / zeta, t = e - g * zeta;
+      const uint32_t m = (uint32_t)mybase + g;
+      const uint32_t h0 = group_hash(sp, m, t, 0);
+      const uint32_t h1 = group_hash(sp, m, t, 1);
+      const uint32_t h2 = group_hash(sp, m, t, 2);
+      rec[e] = make_uint4(8u * (t * bp + __umulhi(h0, b)),   // byte offset of the slot window
+                          2u * (h1 & 15u) + 1u,              // a
+                          ((h1 >> 4) & 31u) * 8u,            // 8 c
+                          h2);                               // sign bits
+    }
+    __syncwarp();
     for (uint32_t p = 0; p < P; ++p) {
       const uint32_t t = (warp + p) % P;
-      if (t < sp.zeta && mybase < g1) {
-        const uint32_t h = group_hash(sp, (uint32_t)mybase + hg, t, hq);
-        const uint32_t hb = (hq == 0) ? __umulhi(h, b) : h;   // lane 3g: base; 3g+1: a,c; 3g+2: signs
-        double* bucket = skm + (int64_t)t * bp;
+      if (t < zeta && mybase < g1) {
         if (b >= 32u) {
 #pragma unroll
-          for (int g = 0; g < kSkG; ++g) {
-            const uint32_t base = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g);
-            const uint32_t p1 = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g + 1);
-            const uint32_t sg = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g + 2);
-            const uint32_t a = 2u * (p1 & 15u) + 1u;
-            const uint32_t cc = (p1 >> 4) & 31u;
-            const uint32_t slot = base + ((a * (uint32_t)lane + cc) & 31u);     // < b + 32
-            const int hi = __double2hiint(v[g]) ^ (int)((sg << (31 - lane)) & 0x80000000u);
-            bucket[slot] += __hiloint2double(hi, __double2loint(v[g]));
+          for (int g8 = 0; g8 < kSkG; g8 += 8) {
+            uint32_t adr[8], wof[8];
+            double val[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {          // records first (broadcast loads, no aliasing)
+              const uint4 r4 = rec[(g8 + u) * zeta + t];
+              wof[u] = r4.x;
+              adr[u] = r4.x + ((r4.y * l8 + r4.z) & 248u);
+              val[u] = __hiloint2double(__double2hiint(v[g8 + u]) ^ (int)((r4.w << (31 - lane)) & 0x80000000u),
+                                        __double2loint(v[g8 + u]));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+              double* pa = reinterpret_cast<double*>(sb + adr[u]);
+              double* pb = reinterpret_cast<double*>(sb + adr[u + 1]);
+              const uint32_t dist = wof[u] > wof[u + 1] ? wof[u] - wof[u + 1] : wof[u + 1] - wof[u];
+              if (dist >= 256u) {                  // disjoint windows: both loads in flight
+                const double oa = *pa, ob = *pb;
+                *pa = oa + val[u];
+                *pb = ob + val[u + 1];
+              } else {
+                *pa += val[u];
+                *pb += val[u + 1];
+              }
+            }
           }
         } else {
           // tiny buckets (b < 32): the 32 rows of a group collide; shared atomics
+          double* bucket = skm + (int64_t)t * bp;
 #pragma unroll
           for (int g = 0; g < kSkG; ++g) {
-            const uint32_t base = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g);
-            const uint32_t p1 = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g + 1);
-            const uint32_t sg = __shfl_sync(SYLV_FULL_MASK, hb, 3 * g + 2);
-            const uint32_t a = 2u * (p1 & 15u) + 1u;
-            const uint32_t cc = (p1 >> 4) & 31u;
-            const uint32_t sl = (base + ((a * (uint32_t)lane + cc) & 31u)) % b;
-            atomicAdd(bucket + sl, ((sg >> lane) & 1u) ? -v[g] : v[g]);
+            const uint4 r4 = rec[g * zeta + t];
+            const uint32_t base = r4.x / 8u - t * bp;
+            const uint32_t sl = (base + ((r4.y * (uint32_t)lane + r4.z / 8u) & 31u)) % b;
+            atomicAdd(bucket + sl, ((r4.w >> lane) & 1u) ? -v[g] : v[g]);
           }
         }
       }
