@@ -21,6 +21,7 @@ struct SketchParams {
   uint32_t seed;    // seed32 = seed ^ (seed >> 32)
   uint32_t zeta;    // nonzeros per column
   uint32_t b;       // bucket height s / zeta
+  uint32_t m0;      // global index of this rank's first 32-row group (row_begin / 32)
   double scale;     // 1 / sqrt(zeta)
 };
 
@@ -81,7 +82,8 @@ enum OpKind : int { kStencil2D = 1, kStencil3D = 2, kCSR = 3 };
 
 struct OpParams {
   int kind;
-  int64_t n;
+  int64_t n;          // rows of this rank's block (stencil: whole lines/planes); blocks carry
+                      // ghost lines (2-D) / planes (3-D) before and after them
   int N;              // stencil grid size
   FastDiv divN;       // division by N
   double cd;          // diagonal 2*dim*nu/h^2

@@ -114,12 +114,13 @@ struct Sequence {
   St25 st25{};
   int which = 0;
   int R = 1, K = 1, dmax = 0;
-  int64_t n = 0, s = 0, ldT = 0, ld = 0;   // ld: SoA column stride (n rounded up to 64)
+  int64_t n = 0, s = 0, ldT = 0, ld = 0;   // n: local rows; ld: SoA column stride
+  int64_t gz = 0;                         // ghost rows before/after a column (N^2 3-D, N 2-D, 0 CSR)
   OpParams op{};
   SketchParams sp{};
   // device
   double* ring = nullptr;     // (K+1) blocks, SoA R x ld
-  double* Cdev = nullptr;     // SoA R x ld
+  double* Cdev = nullptr;     // SoA R x ld block (allocation; data at Cdev + gz)
   double* Yt = nullptr;       // CSR: A Z_d (SoA)
   double* sk = nullptr;       // s x R (row-major)
   double* skpart = nullptr;   // nchunk x R x s sketch partials
@@ -154,7 +155,9 @@ struct Sequence {
   double beta[kMaxR * kMaxR];
   double ell[kMaxR * kMaxR];
 
-  double* slot(int j) const { return ring + (int64_t)(j % (K + 1)) * ld * R; }
+  // data pointer (local row 0 of column 0) of ring slot j; block base = data - gz
+  double* slot(int j) const { return ring + (int64_t)(j % (K + 1)) * ld * R + gz; }
+  double* cdata() const { return Cdev + gz; }
 };
 
 struct sylv_ctx {
@@ -348,10 +351,10 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // SoA block (R columns of an N^3 grid, column stride ld) as an (x, y, z, column) tensor.
-bool encode_block_map(CUtensorMap* m, const double* base, int N, int64_t ld, int R, int bx, int by) {
+bool encode_block_map(CUtensorMap* m, const double* base, int N, int depth, int64_t ld, int R, int bx, int by) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)R};
+  cuuint64_t dims[4] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)depth, (cuuint64_t)R};
   cuuint64_t strides[3] = {(cuuint64_t)N * 8, (cuuint64_t)N * N * 8, (cuuint64_t)ld * 8};
   cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, 1, (cuuint32_t)R};
   cuuint32_t es[4] = {1, 1, 1, 1};
@@ -379,21 +382,23 @@ void setup_tma(sylv_ctx* c, Sequence& q) {
   q.tma = false;
   if ((c->cflags & 4) || q.op.kind != kStencil3D || c->R != 8 || (q.op.N & 1) || q.op.N < 2) return;
   const int N = q.op.N;
+  const int nz = (int)(q.n / ((int64_t)N * N));
   for (int j = 0; j <= c->K; ++j) {
-    const double* base = q.ring + (int64_t)j * q.ld * c->R;
-    if (!encode_block_map(&q.mapH[j], base, N, q.ld, c->R, Geo25<kTY25>::HX, Geo25<kTY25>::HY)) return;
-    if (!encode_block_map(&q.mapW[j], base, N, q.ld, c->R, Geo25<kTY25>::WX, kTY25)) return;
+    const double* base = q.ring + (int64_t)j * q.ld * c->R;     // ghost plane 0 of slot j
+    if (!encode_block_map(&q.mapH[j], base, N, nz + 2, q.ld, c->R, Geo25<kTY25>::HX, Geo25<kTY25>::HY)) return;
+    if (!encode_block_map(&q.mapW[j], base, N, nz + 2, q.ld, c->R, Geo25<kTY25>::WX, kTY25)) return;
   }
   St25& p = q.st25;
   p.N = N;
+  p.nz = nz;
   p.ld = q.ld;
   p.tiles_x = (N + kTx - 1) / kTx;
   p.tiles_y = (N + kTY25 - 1) / kTY25;
   const int64_t tiles = (int64_t)p.tiles_x * p.tiles_y;
   const int grid = 2 * c->sm;
-  int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, N / 16), (8 * grid + tiles - 1) / tiles));
-  p.zseg = (N + nseg - 1) / nseg;
-  p.nseg = (N + p.zseg - 1) / p.zseg;
+  int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, nz / 16), (8 * grid + tiles - 1) / tiles));
+  p.zseg = (nz + nseg - 1) / nseg;
+  p.nseg = (nz + p.zseg - 1) / p.zseg;
   p.items = tiles * p.nseg;
   p.cd = q.op.cd;
   p.cxm = q.op.cxm; p.cxp = q.op.cxp;
@@ -492,13 +497,16 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.dmax = c->dmax;
   q.n = c->n;
   q.s = c->s;
-  q.ld = (c->n + 63) / 64 * 64;
+  q.gz = (A->kind == SYLV_OP_STENCIL3D) ? (int64_t)A->grid[0] * A->grid[0]
+         : (A->kind == SYLV_OP_STENCIL2D) ? (int64_t)A->grid[0] : 0;
+  q.ld = (c->n + 2 * q.gz + 63) / 64 * 64;
   q.ldT = (int64_t)(c->dmax + 1) * c->R;
   q.op = make_op(A, transpose);
   q.sp.seed = (uint32_t)(seed ^ (seed >> 32));
   q.sp.zeta = (uint32_t)c->zeta;
   q.sp.b = (uint32_t)(c->s / c->zeta);
   q.sp.scale = 1.0 / std::sqrt((double)c->zeta);
+  q.sp.m0 = 0;
   const int R = c->R, K = c->K;
   const int64_t blk = q.ld * R, sR = c->s * R, ldT = q.ldT;
   if (A->kind == SYLV_OP_CSR) upload_csr(q, A, transpose, c->st);
@@ -550,9 +558,9 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     double* tmp = dalloc<double>((size_t)c->n * R);
     CK(cudaMemcpyAsync(tmp, C, (size_t)c->n * R * sizeof(double), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
     CK(cudaMemsetAsync(q.Cdev, 0, blk * sizeof(double), c->st));
-    SYLV_DISPATCH_R(R, { k_to_soa<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, tmp, q.Cdev, q.ld); });
+    SYLV_DISPATCH_R(R, { k_to_soa<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, tmp, q.cdata(), q.ld); });
     count(c);
-    CK(cudaMemcpyAsync(q.slot(1), q.Cdev, blk * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(q.slot(1) - q.gz, q.Cdev, blk * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     CK(cudaStreamSynchronize(c->st));
     cudaFree(tmp);
   }
@@ -561,12 +569,12 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   double* elli_d = q.small + 256;
   double* beta_d = q.small + 320;
   SYLV_DISPATCH_R(R, {
-    k_gram_soa<R_><<<c->G, kThreads, 0, c->st>>>(c->n, q.Cdev, q.ld, q.part2);
+    k_gram_soa<R_><<<c->G, kThreads, 0, c->st>>>(c->n, q.cdata(), q.ld, q.part2);
     k_chol_small<R_><<<1, kThreads, 0, c->st>>>(q.part2, c->G, ell_d, elli_d, nullptr, q.flags, 0);
   });
   count(c, 2);
   CK(cudaGetLastError());
-  launch_sketch(c, q, q.Cdev, R, nullptr, q.sk, c->st);
+  launch_sketch(c, q, q.cdata(), R, nullptr, q.sk, c->st);
   CK(cudaGetLastError());
   cholqr2(c, q, q.sk, 0, beta_d, 0, c->st);
   SYLV_DISPATCH_R(R, { k_init_tau<R_><<<1, 1, 0, c->st>>>(beta_d, ell_d, q.Tdev, ldT, q.Rall + R * R); });
@@ -977,9 +985,10 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
       if (l > 0) {
         double* Md = dalloc<double>(M.size());
         double* rbuf = dalloc<double>((size_t)(K + C) * q.ld * r);
+        CK(cudaMemsetAsync(rbuf, 0, (size_t)(K + C) * q.ld * r * sizeof(double), c->st));   // ghosts = 0
         CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
-        auto rslot = [&](int j) { return rbuf + (int64_t)(j % (K + C)) * q.ld * r; };
-        CK(cudaMemcpyAsync(rslot(1), q.Cdev, (size_t)q.ld * r * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+        auto rslot = [&](int j) { return rbuf + (int64_t)(j % (K + C)) * q.ld * r + q.gz; };
+        CK(cudaMemcpyAsync(rslot(1) - q.gz, q.Cdev, (size_t)q.ld * r * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
         int j0 = 1;
         for (int j = 1; j <= d; ++j) {
           if (j >= 2) {  // Z_j from Z_{j-nwin..j-1} with the stored pass-2 coefficients of step j-1
@@ -1094,7 +1103,7 @@ sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X
     double* Xs = dalloc<double>((size_t)q.ld * r);
     CK(cudaMemcpyAsync(Xtmp, X, (size_t)c->n * r * sizeof(double), xin ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
     CK(cudaMemsetAsync(Xs, 0, (size_t)q.ld * r * sizeof(double), c->st));
-    SYLV_DISPATCH_R(r, { k_to_soa<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, Xtmp, Xs, q.ld); });
+    SYLV_DISPATCH_R(r, { k_to_soa<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, Xtmp, Xs + q.gz, q.ld); });
     count(c);
     double* Yd = yout ? Yout : dalloc<double>((size_t)c->s * r);
     if (r != c->R) {
@@ -1106,7 +1115,7 @@ sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X
     // partials buffer is sized for nchunk x R x s; r <= R fits, larger r needs a temporary
     double* saved = q.skpart;
     if (r > c->R) q.skpart = dalloc<double>((size_t)c->nchunk * c->s * r);
-    launch_sketch(c, q, Xs, r, nullptr, Yd, c->st);
+    launch_sketch(c, q, Xs + q.gz, r, nullptr, Yd, c->st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->st));
     if (q.skpart != saved) {

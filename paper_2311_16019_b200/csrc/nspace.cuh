@@ -57,7 +57,10 @@ __device__ __forceinline__ Coord coords(const OpParams& op, uint32_t row) {
   return c;
 }
 
-// (A Z)[row] for one SoA column `z` (= Z + c*ld).  `center` returns z[row].
+// (A Z)[row] for one SoA column `z` (= Z + c*ld), row local to this rank's block.
+// `center` returns z[row].  The last grid direction (y in 2-D, z in 3-D) is read
+// unconditionally: the block's ghost lines/planes hold the neighbour rank's boundary data,
+// or zeros at the Dirichlet boundary (fma(c, 0, v) = v exactly).
 __device__ __forceinline__ double stencil_col(const OpParams& op, const double* __restrict__ z,
                                               uint32_t row, const Coord& q, double& center) {
   const uint32_t N = (uint32_t)op.N;
@@ -66,12 +69,15 @@ __device__ __forceinline__ double stencil_col(const OpParams& op, const double* 
   double v = op.cd * center;
   if (q.x > 0) v = fma(op.cxm, __ldg(p - 1), v);
   if (q.x + 1 < N) v = fma(op.cxp, __ldg(p + 1), v);
-  if (q.y > 0) v = fma(op.cym, __ldg(p - N), v);
-  if (q.y + 1 < N) v = fma(op.cyp, __ldg(p + N), v);
   if (op.kind == kStencil3D) {
+    if (q.y > 0) v = fma(op.cym, __ldg(p - N), v);
+    if (q.y + 1 < N) v = fma(op.cyp, __ldg(p + N), v);
     const uint32_t NN = N * N;
-    if (q.z > 0) v = fma(op.czm, __ldg(p - NN), v);
-    if (q.z + 1 < N) v = fma(op.czp, __ldg(p + NN), v);
+    v = fma(op.czm, __ldg(p - NN), v);
+    v = fma(op.czp, __ldg(p + NN), v);
+  } else {
+    v = fma(op.cym, __ldg(p - N), v);
+    v = fma(op.cyp, __ldg(p + N), v);
   }
   return v;
 }
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(kSkWarps * 32, 1) k_sketch_cols(int64_t n, con
     // hash records of this warp's (group, bucket) pairs
     for (uint32_t e = lane; e < npairs; e += 32) {
       const uint32_t g = e / zeta, t = e - g * zeta;
-      const uint32_t m = (uint32_t)mybase + g;
+      const uint32_t m = sp.m0 + (uint32_t)mybase + g;          // global group index
       const uint32_t h0 = group_hash(sp, m, t, 0);
       const uint32_t h1 = group_hash(sp, m, t, 1);
       const uint32_t h2 = group_hash(sp, m, t, 2);

@@ -14,8 +14,9 @@
 //    side TMA zero-fills the out-of-range part of the box; on the low side the box starts at
 //    x = 0 / y = 0 (measured on this driver: a negative box coordinate, or an innermost
 //    coordinate whose byte offset is not a multiple of 16, raises an illegal-instruction
-//    fault), the x-1 / y-1 neighbours of x = 0 / y = 0 are masked to 0, and plane -1 is
-//    never loaded (its register plane is 0).
+//    fault) and the x-1 / y-1 neighbours of x = 0 / y = 0 are masked to 0.  In z the block
+//    carries ghost planes (zeros at the domain boundary, the neighbour rank's boundary
+//    plane when sharded), so the tensor's planes 0 .. nz+1 are all real memory.
 //  * The r x r block products are fp64 tensor-core MMAs (mma.sync.m8n8k4.f64):
 //      pass 1  P_i += Z_i(plane)^T Y(plane)             (3 DMMA per 4 points for k = 3)
 //      pass 2  W'^T = R_d^T Y^T - sum_i K_i^T Z_i^T      (8 DMMA per 8 points)
@@ -46,6 +47,8 @@ struct Tma25 {
 
 struct St25 {
   int N;                         // grid size (even)
+  int nz;                        // planes of this rank's block; the TMA tensor has nz + 2 planes
+                                 // (ghost plane 0, local planes 1..nz, ghost plane nz + 1)
   int tiles_x, tiles_y, nseg, zseg;
   int64_t items;                 // tiles_x * tiles_y * nseg
   int64_t ld;                    // SoA column stride
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
     const int64_t t2 = item / p.nseg;
     const int tx = (int)(t2 % p.tiles_x), ty = (int)(t2 / p.tiles_x);
     const int x0 = tx * kTx, y0 = ty * TY;
-    const int z0 = seg * p.zseg, z1 = min(NN, z0 + p.zseg);
+    const int z0 = 1 + seg * p.zseg, z1 = min(p.nz + 1, z0 + p.zseg);   // tensor planes
     // planes z0-1 .. z1 go through the stages; plane q uses stage (q - z0 + 1) % kNS
     auto stage_of = [&](int q) { return (q - z0 + 1) % kNS; };
     if (threadIdx.x == 0) {
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
           }
         }
       } else {
-        const int64_t rowbase = ((int64_t)z * NN + (y0 + warp)) * NN + x0;
+        const int64_t rowbase = ((int64_t)(z - 1) * NN + (y0 + warp)) * NN + x0;   // local row
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           double D[2] = {0.0, 0.0};
