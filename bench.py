@@ -46,12 +46,13 @@ def _workload_desc(cfg):
             f"r={cfg.r}, k={cfg.k}, s={cfg.s}, zeta={cfg.zeta}, fp64")
 
 
-def algorithmic_bytes(cfg):
+def algorithmic_bytes(cfg, n=None):
     """Per block step (both sequences), SURVEY §8(d): stencil B_n = 2*8*n*r*(2k+1);
     CSR B_n = 2*[12 nnz + 4(n+1) + 8 n r (2k+3)].  Per launch: pass 1 reads k blocks,
     pass 2 reads k blocks and writes 1 (stencil; CSR pass 1 also reads A and writes A Z,
     pass 2 reads A Z)."""
-    n, r, k = cfg.n, cfg.r, cfg.k
+    n = cfg.n if n is None else n          # sharded: this rank's rows
+    r, k = cfg.r, cfg.k
     blk = 8 * n * r
     if cfg.kind == "csr":
         nnz = n * (cfg.csr_nnz_off + 1)
@@ -205,14 +206,24 @@ def main():
     if args.warmup + args.steps > cfg.d_max:
         raise SystemExit(f"warmup+steps must be <= d_max={cfg.d_max}")
 
-    # ---- inputs (synthetic, seeded); replicas: each rank solves its own copy of the config
+    # ---- inputs (synthetic, seeded).  N > 1: the config is row-sharded over the ranks
+    # (z-slabs / y-lines) through the NCCL transport, strong scaling;
+    # SYLV_BENCH_REPLICAS=1 runs independent replicas instead (weak scaling).
     csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
     C1, C2 = inputs.make_rhs(cfg)
+    sharded = ws > 1 and not os.environ.get("SYLV_BENCH_REPLICAS") and cfg.kind.startswith("stencil")
+    shard_kw = {}
+    if sharded:
+        comm = pkg.nccl_comm()
+        rb, re_ = pkg.partition(cfg, ws, rank)
+        C1, C2 = np.ascontiguousarray(C1[rb:re_]), np.ascontiguousarray(C2[rb:re_])
+        shard_kw = dict(comm=comm, row_range=(rb, re_))
     C1d = torch.from_numpy(C1).to(dev)
     C2d = torch.from_numpy(C2).to(dev)
-    solver = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, timing=True, stream=stream.cuda_stream)
+    solver = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, timing=True, stream=stream.cuda_stream, **shard_kw)
     # per-kernel attribution run (serial stream, CUDA events around each launch), untimed
-    attr = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, timing=True, stream=stream.cuda_stream, serial=True)
+    attr = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, timing=True, stream=stream.cuda_stream, serial=True,
+                           **shard_kw)
     attr.step(args.warmup)
     attr.reset_stats()
     attr.step(min(args.steps, 10))
@@ -249,8 +260,11 @@ def main():
     del C1d, C2d
     torch.cuda.empty_cache()
 
-    value = ws * args.steps / (ms * 1e-3)
-    ab = algorithmic_bytes(cfg)
+    # whole-job block steps/s: sharded ranks advance ONE problem together (strong scaling);
+    # replicas each advance their own copy (weak scaling)
+    value = (1 if sharded else ws) * args.steps / (ms * 1e-3)
+    ab = algorithmic_bytes(cfg, C1.shape[0])     # per rank (= whole problem unless sharded)
+    ab_job = algorithmic_bytes(cfg)
     peak, peak_src = _peaks()
     p2_ms = stats["ms_pass2"] / max(1, stats["n_pass2"])
     p1_ms = stats["ms_pass1"] / max(1, stats["n_pass1"])
@@ -263,7 +277,8 @@ def main():
     dom_ms, dom_bytes = cand[dom], ab[dom]
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = traffic_for(cfg.name, dom)
-    step_gbs = ab["step"] / (ms / args.steps * 1e-3) / 1e9
+    # aggregate over the job's GPUs, against the aggregate peak
+    step_gbs = (ab_job["step"] if sharded else ab["step"] * ws) / (ms / args.steps * 1e-3) / 1e9
 
     # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the region
     e2e = None
@@ -273,7 +288,7 @@ def main():
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        s2 = pkg.from_config(cfg, C1=C1h, C2=C2h, csr_pair=csr, stream=stream.cuda_stream)
+        s2 = pkg.from_config(cfg, C1=C1h, C2=C2h, csr_pair=csr, stream=stream.cuda_stream, **shard_kw)
         s2.step(args.warmup + args.steps)
         rho, rr = s2.residual(args.warmup + args.steps)          # D2H of the step's result (host solve)
         torch.cuda.synchronize()
@@ -285,8 +300,8 @@ def main():
             el = float(t.item())
         nst = args.warmup + args.steps
         mirror = 2 * 8 * ((cfg.k + 1) * cfg.r ** 2 + cfg.r * ((nst // 2 + 1) * cfg.r + cfg.r))
-        e2e = {"value": ws * nst / el, "unit": UNIT,
-               "h2d_bytes_per_step": int(2 * 8 * cfg.n * cfg.r / nst),
+        e2e = {"value": (1 if sharded else ws) * nst / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(2 * 8 * C1.shape[0] * cfg.r * (1 if sharded else ws) / nst),
                "d2h_bytes_per_step": int(mirror),
                "region": f"init(host C1,C2 pinned; H2D) + {nst} steps + residual(d) host solve; wall clock, "
                          f"max over ranks", "rho_rel": rr}
@@ -303,9 +318,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": _workload_desc(cfg), "d_range": [args.warmup + 1, args.warmup + args.steps],
-                       "parallelism": ("replicas" if ws > 1 else "single GPU"),
+                       "parallelism": (f"row-sharded z-slabs x{ws} (NCCL halo + allreduce)" if sharded
+                                       else "replicas" if ws > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (window of k+1 blocks per sequence >> 126 MB)"
                        if 8 * cfg.n * cfg.r * (cfg.k + 1) > 126e6 else "working set may be L2-resident"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -316,8 +332,8 @@ def main():
                          "skqr_ms": stats["ms_skqr"] / max(1, stats["n_skqr"]),
                          "note": ("sketch: hashed sparse-sign scatter, bounded by shared-memory "
                                   "read-modify-write latency, not by HBM" if dom == "sketch" else "")},
-            "step_roofline": {"bytes_per_step": ab["step"], "GBps": step_gbs, "frac": step_gbs / peak,
-                              "frac_of_8TBps": step_gbs / NOMINAL_HBM_GBS,
+            "step_roofline": {"bytes_per_step": ab_job["step"] if sharded else ab["step"] * ws, "GBps": step_gbs,
+                              "frac": step_gbs / (peak * ws), "frac_of_8TBps": step_gbs / (NOMINAL_HBM_GBS * ws),
                               "what": "SURVEY §8(d) B_n per block step (both sequences) / device step time"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),

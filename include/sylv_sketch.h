@@ -102,13 +102,23 @@ typedef struct {
                             sequence's sketch-space work on its own side stream);
                             bit 2: disable the 2.5-D TMA passes (3-D stencil, r = 8,
                             even N) and use the generic pass kernels */
+  int64_t row_begin;     /* sharded contexts: this rank's global rows [row_begin, */
+  int64_t row_end;       /* row_end); 0, 0 = sylv_partition's balanced split.     */
+                         /* Single-rank contexts: 0, 0 (or 0, n).                  */
 } sylv_config;
 
 /* Create a context and run Alg. 1 line 1: U1 ell = C1, V1 ell' = C2
  * (CholQR on the device), beta_1 = R(S_U C1), beta_2 = R(S_V C2), T_1 = tau_1 =
- * beta_1 ell^{-1} (R3).  C1, C2: n x r row-major, host or device.
- * stream: a cudaStream_t (NULL = legacy default stream).  nccl_comm must be NULL
- * in this build (single rank). */
+ * beta_1 ell^{-1} (R3).  C1, C2: n_local x r row-major (this rank's rows),
+ * host or device.  stream: a cudaStream_t (NULL = legacy default stream).
+ * nccl_comm: NULL (single rank) or a sylv_comm* (row-sharded context, SURVEY §8(e):
+ * z-slabs / y-line ranges of the 2-D/3-D stencils; every rank calls every function of
+ * the context collectively, in the same order, with identical cfg).  Each rank keeps
+ * its rows of every basis block (plus ghost planes filled by halo exchange); the
+ * Gram-Schmidt inner products, Grams and partial sketches are summed over the ranks
+ * (bit-identical on all ranks), the sketch-space QR and the projected solves are
+ * replicated.  sylv_sketch_solution / get_block / apply_sketch work on local rows
+ * (apply_sketch returns the global S X on every rank). */
 sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B,
                              const double* C1, const double* C2,
                              const sylv_config* cfg, void* nccl_comm, void* stream,
@@ -179,6 +189,35 @@ void sylv_sketch_reset_stats(sylv_ctx* ctx);
 
 const char* sylv_sketch_last_error(const sylv_ctx* ctx);
 void sylv_sketch_destroy(sylv_ctx* ctx);
+
+/* ---- Row-sharded contexts (north star: "row-sharded by grid slabs, with NCCL
+ * halo exchange ... an allreduce of the Gram-Schmidt coefficients and ... of partial
+ * sketches (S is linear in rows)") ------------------------------------------------------ */
+typedef struct sylv_comm sylv_comm; /* opaque transport handle */
+
+/* Balanced split of a stencil grid over nranks: rank gets the global rows
+ * [*row_begin, *row_end) = whole z-planes (3-D) or y-lines (2-D), every range starting at a
+ * multiple of 32 rows (the sketch hash groups rows by 32).  Host only.
+ * SYLV_E_INVALID if the grid has fewer plane groups than ranks or kind is not a stencil. */
+sylv_status sylv_partition(int32_t kind, int32_t N, int64_t n, int32_t nranks, int32_t rank,
+                           int64_t* row_begin, int64_t* row_end);
+
+/* NCCL transport (one process per GPU).  Rank 0 calls sylv_comm_nccl_unique_id and the
+ * caller broadcasts the 128 bytes (e.g. with torch.distributed); then every rank calls
+ * sylv_comm_create_nccl collectively.  libnccl.so.2 is dlopen'ed (SYLV_E_NCCL if absent). */
+sylv_status sylv_comm_nccl_unique_id(uint8_t id[128]);
+sylv_status sylv_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id[128], sylv_comm** out);
+
+/* In-process transport: nranks virtual ranks of ONE process on one GPU, one host thread per
+ * rank calling the context functions collectively (parity tests of the sharded path on a
+ * single GPU; sums and ghost copies are plain kernels/copies ordered by CUDA events and host
+ * barriers, no kernel waits on another).  The group outlives its comms. */
+sylv_status sylv_local_group_create(int32_t nranks, void** group);
+void sylv_local_group_destroy(void* group);
+sylv_status sylv_comm_create_local(void* group, int32_t rank, sylv_comm** out);
+
+/* Destroy a transport handle (after every context using it). */
+void sylv_comm_destroy(sylv_comm* comm);
 
 /* Host LAPACK (dgees/dtrsyl/dgemm/dtrsm/dgesvd with the `scipy_` symbol prefix of
  * SciPy's bundled OpenBLAS, LP64).  Must be set before the first residual call;

@@ -38,7 +38,8 @@ class Operator(C.Structure):
 class Config(C.Structure):
     _fields_ = [("r", C.c_int32), ("k", C.c_int32), ("d_max", C.c_int32), ("zeta", C.c_int32),
                 ("s", C.c_int64), ("seed_u", C.c_uint64), ("seed_v", C.c_uint64), ("tol", C.c_double),
-                ("rank_tol", C.c_double), ("chunk", C.c_int32), ("flags", C.c_int32)]
+                ("rank_tol", C.c_double), ("chunk", C.c_int32), ("flags", C.c_int32),
+                ("row_begin", C.c_int64), ("row_end", C.c_int64)]
 
 
 class Stats(C.Structure):
@@ -57,7 +58,9 @@ SYMBOLS = ["sylv_sketch_init", "sylv_sketch_step", "sylv_sketch_residual", "sylv
            "sylv_sketch_solve", "sylv_sketch_apply_sketch", "sylv_sketch_get_small",
            "sylv_sketch_get_block", "sylv_sketch_history", "sylv_sketch_stats",
            "sylv_sketch_reset_stats", "sylv_sketch_last_error", "sylv_sketch_destroy",
-           "sylv_set_lapack_path", "sylv_version", "sylv_host_projected", "sylv_host_sylvester"]
+           "sylv_set_lapack_path", "sylv_version", "sylv_host_projected", "sylv_host_sylvester",
+           "sylv_partition", "sylv_comm_nccl_unique_id", "sylv_comm_create_nccl", "sylv_local_group_create",
+           "sylv_local_group_destroy", "sylv_comm_create_local", "sylv_comm_destroy"]
 
 
 def lapack_path() -> str:
@@ -104,6 +107,21 @@ def load_library(path: str = LIB_PATH):
     lib.sylv_host_projected.restype = C.c_int
     lib.sylv_host_sylvester.argtypes = [C.c_int32, C.c_int32, P, P, P, P]
     lib.sylv_host_sylvester.restype = C.c_int
+    lib.sylv_partition.argtypes = [C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                   C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    lib.sylv_partition.restype = C.c_int
+    lib.sylv_comm_nccl_unique_id.argtypes = [P]
+    lib.sylv_comm_nccl_unique_id.restype = C.c_int
+    lib.sylv_comm_create_nccl.argtypes = [C.c_int32, C.c_int32, P, C.POINTER(P)]
+    lib.sylv_comm_create_nccl.restype = C.c_int
+    lib.sylv_local_group_create.argtypes = [C.c_int32, C.POINTER(P)]
+    lib.sylv_local_group_create.restype = C.c_int
+    lib.sylv_local_group_destroy.argtypes = [P]
+    lib.sylv_local_group_destroy.restype = None
+    lib.sylv_comm_create_local.argtypes = [P, C.c_int32, C.POINTER(P)]
+    lib.sylv_comm_create_local.restype = C.c_int
+    lib.sylv_comm_destroy.argtypes = [P]
+    lib.sylv_comm_destroy.restype = None
     for name in SYMBOLS[:11]:
         if name not in ("sylv_sketch_reset_stats",):
             getattr(lib, name).restype = C.c_int
@@ -160,18 +178,26 @@ class SylvSketch:
     def __init__(self, A: Operator, B: Operator, C1, C2, *, r: int, k: int, d_max: int, s: int,
                  zeta: int = 8, seed_u: int = 11, seed_v: int = 12, tol: float = 1e-6,
                  rank_tol: float = 1e-12, chunk: int = 0, timing: bool = False, stream=None,
-                 keep=None, serial: bool = False, tma: bool = True):
+                 keep=None, serial: bool = False, tma: bool = True, comm: "Comm" = None,
+                 row_range: Optional[Tuple[int, int]] = None):
         self.lib = load_library()
         self.cfg = Config(r=r, k=k, d_max=d_max, zeta=zeta, s=s, seed_u=seed_u, seed_v=seed_v, tol=tol,
-                          rank_tol=rank_tol, chunk=chunk, flags=(1 if timing else 0) | (2 if serial else 0) | (0 if tma else 4))
-        self.n, self.r, self.s = int(A.n), r, s
+                          rank_tol=rank_tol, chunk=chunk, flags=(1 if timing else 0) | (2 if serial else 0) | (0 if tma else 4),
+                          row_begin=row_range[0] if row_range else 0, row_end=row_range[1] if row_range else 0)
+        self.n, self.r, self.s = int(A.n), r, s     # n: this context's (local) rows, set below
         self._keep = [A, B, keep]
         p1, k1 = _ptr(C1)
         p2, k2 = _ptr(C2)
         self._ctx = C.c_void_p()
         st = C.c_void_p(stream) if stream is not None else None
-        status = self.lib.sylv_sketch_init(C.byref(A), C.byref(B), p1, p2, C.byref(self.cfg), None, st,
-                                           C.byref(self._ctx))
+        self._comm = comm
+        if comm is not None and row_range is None:
+            raise ValueError("a sharded context needs row_range=(begin, end) (see partition())")
+        self.n_global = int(A.n)
+        if row_range:
+            self.n = int(row_range[1] - row_range[0])
+        status = self.lib.sylv_sketch_init(C.byref(A), C.byref(B), p1, p2, C.byref(self.cfg),
+                                           comm.handle if comm is not None else None, st, C.byref(self._ctx))
         if status != OK:
             msg = self._err()
             self.close()
@@ -278,6 +304,87 @@ def operators_for(cfg, csr_pair=None):
     A, ka = csr_operator(cfg.n, ra, ca, va)
     B, kb = csr_operator(cfg.n, rb, cb, vb)
     return A, B, (ka, kb)
+
+
+def partition(cfg, nranks: int, rank: int) -> Tuple[int, int]:
+    """sylv_partition: this rank's global rows [begin, end) of a stencil config."""
+    lib = load_library()
+    kind = {"stencil2d": OP_STENCIL2D, "stencil3d": OP_STENCIL3D}.get(cfg.kind)
+    if kind is None:
+        raise SylvError(1, "sharded contexts support the stencil configs")
+    b, e = C.c_int64(), C.c_int64()
+    st = lib.sylv_partition(kind, cfg.N, cfg.n, nranks, rank, C.byref(b), C.byref(e))
+    if st != OK:
+        raise SylvError(st, f"cannot split {cfg.name} over {nranks} ranks")
+    return b.value, e.value
+
+
+class Comm:
+    """A sylv_comm* transport handle (NCCL, or one virtual rank of a LocalGroup)."""
+
+    def __init__(self, handle, keep=None):
+        self.handle = handle
+        self._keep = keep
+
+    def close(self):
+        if getattr(self, "handle", None):
+            load_library().sylv_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LocalGroup:
+    """nranks virtual ranks in this process on one GPU (sylv_local_group_create); drive
+    rank i's context from its own host thread (the C calls release the GIL)."""
+
+    def __init__(self, nranks: int):
+        self.lib = load_library()
+        self.nranks = nranks
+        self.handle = C.c_void_p()
+        st = self.lib.sylv_local_group_create(nranks, C.byref(self.handle))
+        if st != OK:
+            raise SylvError(st, "sylv_local_group_create")
+
+    def comm(self, rank: int) -> Comm:
+        h = C.c_void_p()
+        st = self.lib.sylv_comm_create_local(self.handle, rank, C.byref(h))
+        if st != OK:
+            raise SylvError(st, "sylv_comm_create_local")
+        return Comm(h, keep=self)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.sylv_local_group_destroy(self.handle)
+            self.handle = None
+
+
+def nccl_comm(group=None) -> Comm:
+    """NCCL transport for the calling rank of a torch.distributed group: rank 0 draws the
+    unique id (sylv_comm_nccl_unique_id), torch broadcasts the 128 bytes, every rank joins."""
+    import torch
+    import torch.distributed as dist
+    lib = load_library()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = (C.c_uint8 * 128)()
+    if rank == 0:
+        st = lib.sylv_comm_nccl_unique_id(uid)
+        if st != OK:
+            raise SylvError(st, "sylv_comm_nccl_unique_id (libnccl.so.2 not loadable?)")
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+    dist.broadcast(t, src=0, group=group)
+    raw = bytes(t.cpu().tolist())
+    uid2 = (C.c_uint8 * 128).from_buffer_copy(raw)
+    h = C.c_void_p()
+    st = lib.sylv_comm_create_nccl(world, rank, uid2, C.byref(h))
+    if st != OK:
+        raise SylvError(st, "sylv_comm_create_nccl")
+    return Comm(h)
 
 
 def from_config(cfg, C1=None, C2=None, csr_pair=None, timing=False, stream=None, **kw) -> SylvSketch:

@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsylvsketch.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "host_solve.cpp")]
-HEADERS = [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "nspace.cuh", "sspace.cuh", "host_solve.hpp")]
+HEADERS = sorted(os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
+                 if f.endswith((".cuh", ".hpp", ".h")))
 HEADERS.append(os.path.join(ROOT, "include", "sylv_sketch.h"))
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr",

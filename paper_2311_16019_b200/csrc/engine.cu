@@ -23,6 +23,7 @@
 #include "nspace.cuh"
 #include "sspace.cuh"
 #include "stencil25d.cuh"
+#include "comm.cuh"
 
 using namespace sylv;
 
@@ -160,9 +161,17 @@ struct Sequence {
   double* cdata() const { return Cdev + gz; }
 };
 
+// Opaque transport handle of the C ABI (comm.cuh)
+struct sylv_comm {
+  Comm* impl = nullptr;
+};
+
 struct sylv_ctx {
   std::string err;
   cudaStream_t st = nullptr;
+  Comm* comm = nullptr;         // non-null: row-sharded context; not owned
+  int64_t n_global = 0, row_begin = 0, row_end = 0;
+  double* red = nullptr;        // multi-rank: reduced partials (k r^2 + r^2 per sequence)
   int R = 1, K = 1, dmax = 0, zeta = 8, chunk = 0, cflags = 0;
   int64_t n = 0, s = 0;
   double tol = 1e-6, rank_tol = 1e-12;
@@ -426,6 +435,28 @@ Tma25 tma_args(const Sequence& q, int j, int nwin) {
 // Partials written by the pass kernels of sequence q (the coefficient kernels' nparts)
 int pass_parts(const sylv_ctx* c, const Sequence& q) { return q.tma ? c->G25 : c->G; }
 
+// out[e] = sum of the nparts per-CTA partials (block_sum_parts order), one CTA
+__global__ void k_sum_partials(const double* __restrict__ partial, int nparts, int len, double* __restrict__ out) {
+  block_sum_parts(partial, nparts, len, len, out);
+}
+
+// Multi-rank: reduce this rank's per-CTA partials to one vector of `len` values, sum it
+// over the ranks (bit-identical on every rank), and return it as a single "partial" for
+// the coefficient kernels (nparts = 1).  Single rank: the partials are used directly.
+const double* reduce_partials(sylv_ctx* c, const double* partial, int nparts, int len, double* out,
+                              cudaStream_t st, int chan, int* nparts_out) {
+  if (!c->comm) {
+    *nparts_out = nparts;
+    return partial;
+  }
+  k_sum_partials<<<1, kThreads, 0, st>>>(partial, nparts, len, out);
+  count(c);
+  CK(cudaGetLastError());
+  c->comm->allreduce(out, (size_t)len, st, chan);
+  *nparts_out = 1;
+  return out;
+}
+
 // n-space pass launchers (2.5-D TMA kernels when eligible; else R <= 4: thread-per-row FMA
 // kernels, R = 8: DMMA warp tiles).  j = step (1-based): Z_j is the newest window block.
 void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cudaStream_t st) {
@@ -502,11 +533,12 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.ld = (c->n + 2 * q.gz + 63) / 64 * 64;
   q.ldT = (int64_t)(c->dmax + 1) * c->R;
   q.op = make_op(A, transpose);
+  q.op.n = c->n;   // this rank's rows
   q.sp.seed = (uint32_t)(seed ^ (seed >> 32));
   q.sp.zeta = (uint32_t)c->zeta;
   q.sp.b = (uint32_t)(c->s / c->zeta);
   q.sp.scale = 1.0 / std::sqrt((double)c->zeta);
-  q.sp.m0 = 0;
+  q.sp.m0 = (uint32_t)(c->row_begin >> 5);   // global group index of local row 0
   const int R = c->R, K = c->K;
   const int64_t blk = q.ld * R, sR = c->s * R, ldT = q.ldT;
   if (A->kind == SYLV_OP_CSR) upload_csr(q, A, transpose, c->st);
@@ -560,6 +592,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     CK(cudaMemsetAsync(q.Cdev, 0, blk * sizeof(double), c->st));
     SYLV_DISPATCH_R(R, { k_to_soa<R_><<<c->sm * 4, 256, 0, c->st>>>(c->n, tmp, q.cdata(), q.ld); });
     count(c);
+    if (c->comm) c->comm->halo(q.cdata(), R, q.ld, q.gz, c->st, kChanSetup);   // ghosts of Z_1 = C
     CK(cudaMemcpyAsync(q.slot(1) - q.gz, q.Cdev, blk * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     CK(cudaStreamSynchronize(c->st));
     cudaFree(tmp);
@@ -570,11 +603,17 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   double* beta_d = q.small + 320;
   SYLV_DISPATCH_R(R, {
     k_gram_soa<R_><<<c->G, kThreads, 0, c->st>>>(c->n, q.cdata(), q.ld, q.part2);
-    k_chol_small<R_><<<1, kThreads, 0, c->st>>>(q.part2, c->G, ell_d, elli_d, nullptr, q.flags, 0);
   });
+  {
+    int npc = c->G;
+    const double* pc = reduce_partials(c, q.part2, c->G, R * R, c->red ? c->red + (int64_t)q.which * (K + 1) * R * R : nullptr,
+                                       c->st, kChanSetup, &npc);
+    SYLV_DISPATCH_R(R, { k_chol_small<R_><<<1, kThreads, 0, c->st>>>(pc, npc, ell_d, elli_d, nullptr, q.flags, 0); });
+  }
   count(c, 2);
   CK(cudaGetLastError());
   launch_sketch(c, q, q.cdata(), R, nullptr, q.sk, c->st);
+  if (c->comm) c->comm->allreduce(q.sk, (size_t)q.s * R, c->st, kChanSetup);
   CK(cudaGetLastError());
   cholqr2(c, q, q.sk, 0, beta_d, 0, c->st);
   SYLV_DISPATCH_R(R, { k_init_tau<R_><<<1, 1, 0, c->st>>>(beta_d, ell_d, q.Tdev, ldT, q.Rall + R * R); });
@@ -604,8 +643,13 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_
   if (timing) { t1 = ev_get(c, 0); CK(cudaEventRecord(t1.a, st)); }
   launch_pass1(c, q, win, nwin, j, st);
   if (timing) { CK(cudaEventRecord(t1.b, st)); c->timed.push_back(t1); }
+  const int chan_main = q.which == 0 ? kChanUMain : kChanVMain;
+  const int chan_side = q.which == 0 ? kChanUSide : kChanVSide;
+  double* red = c->red ? c->red + (int64_t)q.which * (K + 1) * R * R : nullptr;
+  int np1 = G;
+  const double* p1 = reduce_partials(c, q.part1, G, K * R * R, red, st, chan_main, &np1);
   SYLV_DISPATCH_RK(R, K, {
-    k_coef1<R_, K_><<<1, kThreads, 0, st>>>(q.part1, G, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
+    k_coef1<R_, K_><<<1, kThreads, 0, st>>>(p1, np1, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
   });
   // ---- a2 update + a3 Gram: pass 2 (writes Z_{j+1} = W' into the ring slot that the
   //      sketch of step j-K-1 read)
@@ -614,9 +658,13 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_
   if (timing) { t2 = ev_get(c, 1); CK(cudaEventRecord(t2.a, st)); }
   launch_pass2<true>(c, q, win, nwin, j, q.Yt, q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1), st);
   if (timing) { CK(cudaEventRecord(t2.b, st)); c->timed.push_back(t2); }
+  int np2 = G;
+  const double* p2 = reduce_partials(c, q.part2, G, R * R, red ? red + K * R * R : nullptr, st, chan_main, &np2);
   SYLV_DISPATCH_RK(R, K, {
-    k_coef2<R_, K_><<<1, kThreads, 0, st>>>(q.part2, G, j, q.Rall, q.Hc, q.hn2, q.flags);
+    k_coef2<R_, K_><<<1, kThreads, 0, st>>>(p2, np2, j, q.Rall, q.Hc, q.hn2, q.flags);
   });
+  // ghost planes/lines of the new block for the next step's stencil (sharded contexts)
+  if (c->comm) c->comm->halo(q.slot(j + 1), R, q.ld, q.gz, st, chan_main);
   count(c, 2);
   CK(cudaGetLastError());
   // ---- H column j mirror (main stream), then hand over to the side stream
@@ -633,6 +681,7 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_
   TimedPair t4{};
   if (timing) { t4 = ev_get(c, 3); CK(cudaEventRecord(t4.a, st)); }
   launch_sketch(c, q, q.slot(j + 1), R, q.Rall + (int64_t)(j + 1) * R * R, q.w, st);
+  if (c->comm) c->comm->allreduce(q.w, (size_t)q.s * R, st, chan_side);   // S linear in rows
   if (timing) { CK(cudaEventRecord(t4.b, st)); c->timed.push_back(t4); }
   if (side != c->st && side != c->st2) CK(cudaEventRecord(q.ev_sk[j % ne], st));
   // ---- a5: block CGS2 against Q (m = j R columns); CholQR2; T column
@@ -683,12 +732,20 @@ template <typename F>
 sylv_status guard(sylv_ctx* c, F&& f) {
   try {
     return f();
-  } catch (const CudaError& e) {
-    return fail(c, SYLV_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
-  } catch (const Status& s) {
-    return fail(c, s.s, s.msg);
-  } catch (const std::bad_alloc&) {
-    return fail(c, SYLV_E_NOMEM, "host allocation failed");
+  } catch (...) {
+    // a rank that fails inside a collective sequence releases its peers (LocalComm)
+    if (c && c->comm) c->comm->abort();
+    try {
+      throw;
+    } catch (const CudaError& e) {
+      return fail(c, SYLV_E_CUDA, std::string(e.what) + ": " + cudaGetErrorString(e.e));
+    } catch (const Status& s) {
+      return fail(c, s.s, s.msg);
+    } catch (const std::bad_alloc&) {
+      return fail(c, SYLV_E_NOMEM, "host allocation failed");
+    } catch (const CommError& e) {
+      return fail(c, SYLV_E_NCCL, e.what);
+    }
   }
 }
 
@@ -734,12 +791,82 @@ sylv_status sylv_set_lapack_path(const char* path) {
 
 const char* sylv_sketch_last_error(const sylv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+sylv_status sylv_partition(int32_t kind, int32_t N, int64_t n, int32_t nranks, int32_t rank, int64_t* row_begin,
+                           int64_t* row_end) {
+  if (!row_begin || !row_end || nranks < 1 || rank < 0 || rank >= nranks || N < 1) return SYLV_E_INVALID;
+  int64_t unit;
+  if (kind == SYLV_OP_STENCIL3D && n == (int64_t)N * N * N) unit = (int64_t)N * N;
+  else if (kind == SYLV_OP_STENCIL2D && n == (int64_t)N * N) unit = N;
+  else return SYLV_E_INVALID;
+  // planes/lines in groups of g so that every range starts at a multiple of 32 rows
+  int64_t g = 1;
+  while ((g * unit) % 32) ++g;
+  const int64_t ngrp = (N + g - 1) / g;
+  if (ngrp < nranks) return SYLV_E_INVALID;
+  const int64_t gb = ngrp * rank / nranks, ge = ngrp * (rank + 1) / nranks;
+  *row_begin = std::min<int64_t>(N, gb * g) * unit;
+  *row_end = std::min<int64_t>(N, ge * g) * unit;
+  return *row_end > *row_begin ? SYLV_OK : SYLV_E_INVALID;
+}
+
+sylv_status sylv_comm_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return SYLV_E_INVALID;
+  NcclApi& a = nccl_api();
+  if (!a.GetUniqueId) return SYLV_E_NCCL;
+  ncclUniqueId u;
+  if (a.GetUniqueId(&u) != ncclSuccess) return SYLV_E_NCCL;
+  static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, &u, 128);
+  return SYLV_OK;
+}
+
+sylv_status sylv_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id[128], sylv_comm** out) {
+  if (!out || !id || nranks < 1 || rank < 0 || rank >= nranks) return SYLV_E_INVALID;
+  *out = nullptr;
+  try {
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    sylv_comm* c = new sylv_comm();
+    c->impl = new NcclComm(nranks, rank, u);
+    *out = c;
+    return SYLV_OK;
+  } catch (const CommError& e) {
+    std::fprintf(stderr, "sylv_comm_create_nccl: %s\n", e.what.c_str());
+    return SYLV_E_NCCL;
+  }
+}
+
+sylv_status sylv_local_group_create(int32_t nranks, void** group) {
+  if (!group || nranks < 1 || nranks > kMaxLocalRanks) return SYLV_E_INVALID;
+  *group = new LocalGroup(nranks);
+  return SYLV_OK;
+}
+
+void sylv_local_group_destroy(void* group) { delete static_cast<LocalGroup*>(group); }
+
+sylv_status sylv_comm_create_local(void* group, int32_t rank, sylv_comm** out) {
+  if (!out || !group) return SYLV_E_INVALID;
+  LocalGroup* g = static_cast<LocalGroup*>(group);
+  if (rank < 0 || rank >= g->P) return SYLV_E_INVALID;
+  sylv_comm* c = new sylv_comm();
+  c->impl = new LocalComm(g, rank);
+  *out = c;
+  return SYLV_OK;
+}
+
+void sylv_comm_destroy(sylv_comm* comm) {
+  if (!comm) return;
+  delete comm->impl;
+  delete comm;
+}
+
 void sylv_sketch_destroy(sylv_ctx* ctx) {
   if (!ctx) return;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4})
     if (s) cudaStreamSynchronize(s);
   for (auto& q : ctx->seq) free_seq(q);
+  if (ctx->red) cudaFree(ctx->red);
   for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4})
     if (s) cudaStreamDestroy(s);
   if (ctx->fork) cudaEventDestroy(ctx->fork);
@@ -764,8 +891,11 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
   if (cfg->d_max < 1) return fail(c, SYLV_E_INVALID, "d_max must be >= 1");
   if (cfg->zeta < 1 || cfg->s <= 0 || cfg->s % cfg->zeta) return fail(c, SYLV_E_INVALID, "s must be a positive multiple of zeta");
   if (cfg->s < (int64_t)(cfg->d_max + 1) * r) return fail(c, SYLV_E_INVALID, "s must be >= (d_max+1) r");
-  if (nccl_comm) return fail(c, SYLV_E_NCCL, "multi-rank contexts are not part of this build");
   if (A->n != B->n || A->n <= 0) return fail(c, SYLV_E_INVALID, "A and B must be n x n with equal n");
+  Comm* comm = nccl_comm ? static_cast<sylv_comm*>(nccl_comm)->impl : nullptr;
+  if (comm && (A->kind != B->kind || A->grid[0] != B->grid[0] ||
+               !(A->kind == SYLV_OP_STENCIL2D || A->kind == SYLV_OP_STENCIL3D)))
+    return fail(c, SYLV_E_INVALID, "sharded contexts support the 2-D/3-D stencil operators (same grid for A and B)");
   if ((uint64_t)A->n * cfg->zeta >= (1ull << 32)) return fail(c, SYLV_E_INVALID, "n*zeta must be < 2^32");
   for (const sylv_operator* o : {A, B}) {
     if (o->kind == SYLV_OP_STENCIL2D || o->kind == SYLV_OP_STENCIL3D) {
@@ -784,7 +914,33 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     c->K = cfg->k;
     c->dmax = cfg->d_max;
     c->zeta = cfg->zeta;
-    c->n = A->n;
+    c->n_global = A->n;
+    c->row_begin = 0;
+    c->row_end = A->n;
+    if (comm) {
+      // this rank's rows: given, or the balanced partition of sylv_partition
+      int64_t rb = cfg->row_begin, re = cfg->row_end;
+      if (rb == 0 && re == 0 &&
+          sylv_partition(A->kind, A->grid[0], A->n, comm->nranks, comm->rank, &rb, &re) != SYLV_OK)
+        throw Status{SYLV_E_INVALID, "cannot partition the grid over this many ranks"};
+      comm->gather_ranges(rb, re);                                    // collective
+      const int64_t unit = (A->kind == SYLV_OP_STENCIL3D) ? (int64_t)A->grid[0] * A->grid[0] : A->grid[0];
+      for (int q = 0; q < comm->nranks; ++q) {
+        const int64_t b = comm->rb[q], e = comm->re[q];
+        if ((q == 0 && b != 0) || (q > 0 && b != comm->re[q - 1]) || (q == comm->nranks - 1 && e != A->n))
+          throw Status{SYLV_E_INVALID, "row ranges must tile [0, n) in rank order"};
+        if (e <= b || b % unit || e % unit || b % 32)
+          throw Status{SYLV_E_INVALID, "row ranges must be whole, non-empty sets of grid planes (3-D) / lines (2-D) "
+                                       "starting at multiples of 32"};
+      }
+      c->comm = comm;
+      c->row_begin = rb;
+      c->row_end = re;
+      CK(cudaMalloc(&c->red, (size_t)2 * (cfg->k + 1) * r * r * sizeof(double)));
+    } else if (!(cfg->row_begin == 0 && (cfg->row_end == 0 || cfg->row_end == A->n))) {
+      throw Status{SYLV_E_INVALID, "a row range needs a communicator"};
+    }
+    c->n = c->row_end - c->row_begin;
     c->s = cfg->s;
     c->tol = cfg->tol;
     c->rank_tol = cfg->rank_tol > 0 ? cfg->rank_tol : 1e-12;
@@ -998,6 +1154,7 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
             for (int i = 0; i < nwin; ++i) win.p[i] = rslot(jp - nwin + 1 + i);
             launch_pass2<false>(c, q, win, nwin, jp, nullptr, q.Kc + (int64_t)jp * (1 + K) * r * r, rslot(j), c->st,
                                 /*allow_tma=*/false);
+            if (c->comm) c->comm->halo(rslot(j), r, q.ld, q.gz, c->st, kChanUMain);
           }
           if (j - j0 + 1 == C || j == d) {
             ChunkPtrs cp{};
@@ -1116,6 +1273,7 @@ sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X
     double* saved = q.skpart;
     if (r > c->R) q.skpart = dalloc<double>((size_t)c->nchunk * c->s * r);
     launch_sketch(c, q, Xs + q.gz, r, nullptr, Yd, c->st);
+    if (c->comm) c->comm->allreduce(Yd, (size_t)c->s * r, c->st, kChanSetup);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->st));
     if (q.skpart != saved) {

@@ -1,0 +1,168 @@
+"""Row-sharded contexts on one GPU.
+
+P virtual ranks of ONE process (sylv_local_group_create; one host thread per rank, every
+rank's kernels on its own streams, transports = plain device sums/copies ordered by CUDA
+events, no kernel waits on another) run the same code path as NCCL ranks: halo exchange of
+each new block's boundary planes/lines, allreduce of the Gram-Schmidt inner products and
+Grams, allreduce of the partial sketches (S hashed on GLOBAL rows).  The sharded run must
+reproduce the unsharded GPU run up to reduction order (1e-10 relative on rho and on the
+basis blocks) and the CPU oracle to the parity tolerance (rho 1e-8 relative, d <= 50).
+The NCCL transport itself is exercised at world size 1 (one GPU per gpurun call).
+"""
+import ctypes as C
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(1200)]
+
+torch = pytest.importorskip("torch")
+
+from oracle import alg1  # noqa: E402
+from synth import inputs  # noqa: E402
+
+
+def _pkg():
+    import paper_2311_16019_b200 as pkg
+    return pkg
+
+
+CASES = {
+    # (config, ranks, tma)
+    "3d-r8k3-tma-P2": (dict(kind="stencil3d", N=34, r=8, k=3, d_max=40), 2, True),
+    "3d-r8k3-tma-P3": (dict(kind="stencil3d", N=34, r=8, k=3, d_max=40), 3, True),
+    "3d-r8k2-generic-P2": (dict(kind="stencil3d", N=32, r=8, k=2, d_max=40), 2, False),
+    "3d-r4k2-P4": (dict(kind="stencil3d", N=32, r=4, k=2, d_max=40), 4, True),
+    "2d-r4k2-P3": (dict(kind="stencil2d", N=64, r=4, k=2, d_max=40), 3, True),
+    "2d-r1k2-P2": (dict(kind="stencil2d", N=64, r=1, k=2, d_max=40), 2, True),
+}
+NSTEPS = 16
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _unsharded(cfg, C1, C2, tma, nsteps):
+    g = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(),
+                           stream=torch.cuda.current_stream().cuda_stream, tma=tma)
+    rho = []
+    for d in range(1, nsteps + 1):
+        g.step(1)
+        rho.append(g.residual(d)[1])
+    blocks = {w: [g.get_block(w, j) for j in range(nsteps + 2 - cfg.k, nsteps + 2)] for w in (0, 1)}
+    sk = g.apply_sketch(0, torch.from_numpy(C1).cuda())
+    g.close()
+    return rho, blocks, sk
+
+
+def _sharded(cfg, C1, C2, P, tma, nsteps, solution_rank=0):
+    pkg = _pkg()
+    grp = pkg.LocalGroup(P)
+    out = [None] * P
+    errs = []
+
+    def worker(rank):
+        try:
+            torch.cuda.set_device(0)
+            b, e = pkg.partition(cfg, P, rank)
+            comm = grp.comm(rank)
+            st = torch.cuda.Stream()
+            g = pkg.from_config(cfg, C1=torch.from_numpy(C1[b:e]).cuda(), C2=torch.from_numpy(C2[b:e]).cuda(),
+                                stream=st.cuda_stream, comm=comm, row_range=(b, e), tma=tma)
+            rho = []
+            for d in range(1, nsteps + 1):
+                g.step(1)
+                rho.append(g.residual(d)[1])
+            blocks = {w: [g.get_block(w, j) for j in range(nsteps + 2 - cfg.k, nsteps + 2)] for w in (0, 1)}
+            sk = g.apply_sketch(0, torch.from_numpy(C1[b:e]).cuda())
+            H, T, beta = g.get_small(0, nsteps)
+            X1, X2, rk = g.solution(nsteps, solution_rank) if solution_rank else (None, None, 0)
+            out[rank] = dict(rows=(b, e), rho=rho, blocks=blocks, sk=sk, H=H, T=T, X1=X1, X2=X2, rank=rk)
+            g.close()
+            comm.close()
+        except Exception as ex:  # surfaced below
+            errs.append((rank, ex))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    grp.close()
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_sharded_equals_unsharded(name):
+    kw, P, tma = CASES[name]
+    cfg = inputs.small_config(**kw)
+    C1, C2 = inputs.make_rhs(cfg)
+    rho1, blocks1, sk1 = _unsharded(cfg, C1, C2, tma, NSTEPS)
+    shards = _sharded(cfg, C1, C2, P, tma, NSTEPS)
+    # row ranges tile [0, n) in rank order
+    assert shards[0]["rows"][0] == 0 and shards[-1]["rows"][1] == cfg.n
+    assert all(shards[i]["rows"][1] == shards[i + 1]["rows"][0] for i in range(P - 1))
+    for sh in shards:
+        # every rank reaches the same (replicated) projected quantities
+        np.testing.assert_array_equal(sh["rho"], shards[0]["rho"])
+        np.testing.assert_array_equal(sh["T"], shards[0]["T"])
+        for d, (a, b) in enumerate(zip(sh["rho"], rho1), 1):
+            assert abs(a - b) <= 1e-10 * b, (name, d, a, b)
+        assert _rel(sh["sk"], sk1) <= 1e-12
+    for w in (0, 1):
+        for i in range(cfg.k):
+            full = np.concatenate([sh["blocks"][w][i] for sh in shards])
+            assert _rel(full, blocks1[w][i]) <= 1e-10, (name, w, i)
+
+
+def test_sharded_matches_oracle_and_solution():
+    kw, P, tma = CASES["3d-r8k3-tma-P3"]
+    cfg = inputs.small_config(**kw)
+    C1, C2 = inputs.make_rhs(cfg)
+    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2)
+    ro = []
+    for d in range(1, NSTEPS + 1):
+        orc.step(1)
+        ro.append(orc.residual(d).rho_rel)
+    shards = _sharded(cfg, C1, C2, P, tma, NSTEPS, solution_rank=48)
+    for d, (a, b) in enumerate(zip(shards[0]["rho"], ro), 1):
+        assert abs(a - b) <= 1e-8 * b, (d, a, b)
+    # the factored solution, assembled from the ranks' rows, equals the unsharded one
+    g = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(),
+                           stream=torch.cuda.current_stream().cuda_stream)
+    g.step(NSTEPS)
+    g.residual(NSTEPS)
+    X1, X2, rk = g.solution(NSTEPS, 48)
+    g.close()
+    assert all(sh["rank"] == rk for sh in shards)
+    Xs1 = np.concatenate([np.asarray(sh["X1"]) for sh in shards])
+    Xs2 = np.concatenate([np.asarray(sh["X2"]) for sh in shards])
+    assert _rel(Xs1 @ Xs2.T, np.asarray(X1) @ np.asarray(X2).T) <= 1e-9
+
+
+def test_nccl_transport_world_size_one():
+    """The NCCL transport (communicator split per channel, allreduce, halo with no
+    neighbours) at world size 1 reproduces the unsharded context bit for bit."""
+    pkg = _pkg()
+    lib = pkg.load_library()
+    uid = (C.c_uint8 * 128)()
+    assert lib.sylv_comm_nccl_unique_id(uid) == 0
+    h = C.c_void_p()
+    assert lib.sylv_comm_create_nccl(1, 0, uid, C.byref(h)) == 0
+    comm = pkg.Comm(h)
+    cfg = inputs.small_config(kind="stencil3d", N=34, r=8, k=3, d_max=40)
+    C1, C2 = inputs.make_rhs(cfg)
+    st = torch.cuda.current_stream().cuda_stream
+    a = pkg.from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), stream=st, comm=comm,
+                        row_range=(0, cfg.n))
+    b = pkg.from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), stream=st)
+    for d in range(1, 11):
+        a.step(1)
+        b.step(1)
+        assert a.residual(d)[1] == b.residual(d)[1]
+    a.close()
+    b.close()
+    comm.close()
