@@ -181,6 +181,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance solve")
     args = ap.parse_args()
 
     from synth import inputs
@@ -257,7 +258,6 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     solver.close()
-    del C1d, C2d
     torch.cuda.empty_cache()
 
     # whole-job block steps/s: sharded ranks advance ONE problem together (strong scaling);
@@ -306,6 +306,30 @@ def main():
                "region": f"init(host C1,C2 pinned; H2D) + {nst} steps + residual(d) host solve; wall clock, "
                          f"max over ranks", "rho_rel": rr}
 
+    # ---- time to tolerance (BASELINE metric's first part): full solve with the canonical
+    # check schedule (R9): init from device C + steps + projected solves + bisection
+    ttt = None
+    if not args.no_ttt:
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s3 = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, stream=stream.cuda_stream, **shard_kw)
+        d_star, rr_star, st_star = s3.solve()
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        st3 = s3.stats()
+        s3.close()
+        if ws > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        ttt = {"seconds": el, "d_star": d_star, "rho_rel": rr_star, "converged": st_star == 0,
+               "block_steps": st3["steps"], "host_solves": st3["host_solves"], "host_solve_s": st3["host_solve_s"],
+               "gpu_solves": st3["gpu_solves"], "gpu_solve_s": st3["gpu_solve_s"],
+               "region": "wall clock: context init from device-resident C1, C2 + sylv_sketch_solve (steps, "
+                         "canonical check schedule, projected solves: host Bartels-Stewart for d r < 512, device "
+                         "sign-function iteration above, bisection); max over ranks"}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         budget = float(os.environ.get("SYLV_CPU_BUDGET_S", "30"))
@@ -335,6 +359,7 @@ def main():
             "step_roofline": {"bytes_per_step": ab_job["step"] if sharded else ab["step"] * ws, "GBps": step_gbs,
                               "frac": step_gbs / (peak * ws), "frac_of_8TBps": step_gbs / (NOMINAL_HBM_GBS * ws),
                               "what": "SURVEY §8(d) B_n per block step (both sequences) / device step time"},
+            "time_to_tolerance": ttt,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }

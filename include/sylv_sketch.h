@@ -101,7 +101,10 @@ typedef struct {
                             timings; default: U and V passes on two streams, each
                             sequence's sketch-space work on its own side stream);
                             bit 2: disable the 2.5-D TMA passes (3-D stencil, r = 8,
-                            even N) and use the generic pass kernels */
+                            even N) and use the generic pass kernels;
+                            bit 3: projected solves on the device for every d;
+                            bit 4: projected solves on the host for every d
+                            (default: device when d r >= 512, host below) */
   int64_t row_begin;     /* sharded contexts: this rank's global rows [row_begin, */
   int64_t row_end;       /* row_end); 0, 0 = sylv_partition's balanced split.     */
                          /* Single-rank contexts: 0, 0 (or 0, n).                  */
@@ -182,6 +185,9 @@ typedef struct {
   double host_solve_s;       /* wall seconds spent in host projected solves       */
   int64_t host_solves;
   double kappa_T_u, kappa_T_v; /* reserved                                        */
+  int64_t gpu_solves;        /* projected solves done on the device (sign iteration) */
+  double gpu_solve_s;        /* wall seconds in them                               */
+  int64_t gpu_solve_fallbacks; /* device solves that did not converge -> host BS   */
 } sylv_stats;
 
 sylv_status sylv_sketch_stats(sylv_ctx* ctx, sylv_stats* out);

@@ -47,7 +47,8 @@ class Stats(C.Structure):
                 ("ms_pass2", C.c_double), ("n_pass1", C.c_int64), ("n_pass2", C.c_int64),
                 ("ms_skqr", C.c_double), ("n_skqr", C.c_int64), ("ms_sketch", C.c_double),
                 ("n_sketch", C.c_int64), ("host_solve_s", C.c_double),
-                ("host_solves", C.c_int64), ("kappa_T_u", C.c_double), ("kappa_T_v", C.c_double)]
+                ("host_solves", C.c_int64), ("kappa_T_u", C.c_double), ("kappa_T_v", C.c_double),
+                ("gpu_solves", C.c_int64), ("gpu_solve_s", C.c_double), ("gpu_solve_fallbacks", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -179,10 +180,12 @@ class SylvSketch:
                  zeta: int = 8, seed_u: int = 11, seed_v: int = 12, tol: float = 1e-6,
                  rank_tol: float = 1e-12, chunk: int = 0, timing: bool = False, stream=None,
                  keep=None, serial: bool = False, tma: bool = True, comm: "Comm" = None,
+                 proj: str = "auto",
                  row_range: Optional[Tuple[int, int]] = None):
         self.lib = load_library()
         self.cfg = Config(r=r, k=k, d_max=d_max, zeta=zeta, s=s, seed_u=seed_u, seed_v=seed_v, tol=tol,
-                          rank_tol=rank_tol, chunk=chunk, flags=(1 if timing else 0) | (2 if serial else 0) | (0 if tma else 4),
+                          rank_tol=rank_tol, chunk=chunk, flags=(1 if timing else 0) | (2 if serial else 0) | (0 if tma else 4)
+                          | {"auto": 0, "gpu": 8, "host": 16}[proj],
                           row_begin=row_range[0] if row_range else 0, row_end=row_range[1] if row_range else 0)
         self.n, self.r, self.s = int(A.n), r, s     # n: this context's (local) rows, set below
         self._keep = [A, B, keep]
@@ -202,6 +205,9 @@ class SylvSketch:
             msg = self._err()
             self.close()
             raise SylvError(status, msg)
+
+    def last_error(self) -> str:
+        return self._err()
 
     # -- helpers
     def _err(self) -> str:

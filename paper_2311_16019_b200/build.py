@@ -35,7 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-cudart", "static", "-o", tmp, *SOURCES, "-ldl"]
+    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-cudart", "static", "-o", tmp, *SOURCES, "-ldl",
+           "-L/usr/local/cuda/lib64", "-lcublas", "-lcusolver", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=HERE)

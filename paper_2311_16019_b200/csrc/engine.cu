@@ -24,6 +24,7 @@
 #include "sspace.cuh"
 #include "stencil25d.cuh"
 #include "comm.cuh"
+#include "proj_gpu.cuh"
 
 using namespace sylv;
 
@@ -193,9 +194,11 @@ struct sylv_ctx {
   int d_done = 0;
   bool broken = false;
   int breakdown_d = -1;
-  // last projected solution
+  // last projected solution (host vector, or the device solver's C when y_dev)
   int y_d = -1;
+  bool y_dev = false;
   std::vector<double> Y;
+  GpuSylv* gsolve = nullptr;    // device projected solver (created on first use)
   std::vector<std::pair<int, double>> hist;
   sylv_stats stats{};
   std::vector<TimedPair> timed;
@@ -867,6 +870,7 @@ void sylv_sketch_destroy(sylv_ctx* ctx) {
     if (s) cudaStreamSynchronize(s);
   for (auto& q : ctx->seq) free_seq(q);
   if (ctx->red) cudaFree(ctx->red);
+  delete ctx->gsolve;
   for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4})
     if (s) cudaStreamDestroy(s);
   if (ctx->fork) cudaEventDestroy(ctx->fork);
@@ -1051,9 +1055,6 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
     const int r = c->R, m = d * r;
     Sequence& U = c->seq[0];
     Sequence& V = c->seq[1];
-    std::vector<double> MU, MV;
-    build_projected(d, r, c->K, U.Th, U.ldT, U.Hh, MU);
-    build_projected(d, r, c->K, V.Th, V.ldT, V.Hh, MV);
     double hhat[kMaxR * kMaxR], ghat[kMaxR * kMaxR], Bm[kMaxR * kMaxR];
     hat_coefficient(d, r, c->K, U.Th, U.ldT, U.Hh, hhat);
     hat_coefficient(d, r, c->K, V.Th, V.ldT, V.Hh, ghat);
@@ -1066,30 +1067,75 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
         bn += s * s;
       }
     bn = std::sqrt(bn);
-    std::string err;
-    const int info = sylvester_bs(m, r, MU, MV, Bm, c->Y, err);
-    c->stats.host_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    c->stats.host_solves++;
-    if (info < 0) return fail(c, SYLV_E_LAPACK, err);
-    if (info > 0) {
-      c->y_d = -1;
-      if (rho) *rho = NAN;
-      if (rho_rel) *rho_rel = NAN;
-      return fail(c, SYLV_E_SINGULAR, err);
+    // Y's last r rows (lrow[col * r + p] = Y[m-r+p, col]) and last r columns
+    // (lcol[p * m + row] = Y[row, m-r+p]) are all the residual needs
+    std::vector<double> lrow((size_t)m * r), lcol((size_t)m * r);
+    bool done = false;
+    const bool want_gpu = (c->cflags & 8) || (!(c->cflags & 16) && m >= 512);
+    if (want_gpu) {
+      // f1: device sign-function solve; falls back to the host on non-convergence
+      try {
+        if (!c->gsolve) {
+          c->gsolve = new GpuSylv();
+          c->gsolve->mcap = (c->dmax + 1) * r;
+        }
+        GpuSylv& gs = *c->gsolve;
+        if (gs.solve(U.Tdev, U.Hc, V.Tdev, V.Hc, U.ldT, d, r, c->K, Bm, c->st)) {
+          CK(cudaMemcpy2DAsync(lrow.data(), (size_t)r * sizeof(double), gs.C + (m - r), (size_t)m * sizeof(double),
+                               (size_t)r * sizeof(double), m, cudaMemcpyDeviceToHost, c->st));
+          CK(cudaMemcpyAsync(lcol.data(), gs.C + (size_t)(m - r) * m, (size_t)m * r * sizeof(double),
+                             cudaMemcpyDeviceToHost, c->st));
+          CK(cudaStreamSynchronize(c->st));
+          done = true;
+          c->y_dev = true;
+          c->stats.gpu_solves++;
+          c->stats.gpu_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        } else {
+          c->stats.gpu_solve_fallbacks++;
+          c->err = "device projected solve did not converge at d = " + std::to_string(d) + " (" +
+                   std::to_string(c->gsolve->iterations) + " iterations); host fallback";
+        }
+      } catch (const ProjError& e) {
+        c->stats.gpu_solve_fallbacks++;
+        c->err = "device projected solve failed at d = " + std::to_string(d) + ": " + e.what + "; host fallback";
+        cudaGetLastError();
+      }
+    }
+    if (!done) {
+      std::vector<double> MU, MV;
+      build_projected(d, r, c->K, U.Th, U.ldT, U.Hh, MU);
+      build_projected(d, r, c->K, V.Th, V.ldT, V.Hh, MV);
+      std::string err;
+      const int info = sylvester_bs(m, r, MU, MV, Bm, c->Y, err);
+      c->stats.host_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      c->stats.host_solves++;
+      if (info < 0) return fail(c, SYLV_E_LAPACK, err);
+      if (info > 0) {
+        c->y_d = -1;
+        if (rho) *rho = NAN;
+        if (rho_rel) *rho_rel = NAN;
+        return fail(c, SYLV_E_SINGULAR, err);
+      }
+      c->y_dev = false;
+      for (int col = 0; col < m; ++col)
+        for (int p = 0; p < r; ++p) {
+          lrow[(size_t)col * r + p] = c->Y[(size_t)col * m + (m - r + p)];
+          lcol[(size_t)p * m + col] = c->Y[(size_t)(m - r + p) * m + col];
+        }
     }
     c->y_d = d;
-    // rho^2 = ||hhat E_d^T Y||^2 + ||Y E_d ghat^T||^2 (Y col-major m x m)
+    // rho^2 = ||hhat E_d^T Y||^2 + ||Y E_d ghat^T||^2
     double s1 = 0.0, s2 = 0.0;
     for (int col = 0; col < m; ++col)
       for (int a = 0; a < r; ++a) {
         double v = 0.0;
-        for (int p = 0; p < r; ++p) v += hhat[a * r + p] * c->Y[(size_t)col * m + (m - r + p)];
+        for (int p = 0; p < r; ++p) v += hhat[a * r + p] * lrow[(size_t)col * r + p];
         s1 += v * v;
       }
     for (int row = 0; row < m; ++row)
       for (int a = 0; a < r; ++a) {
         double v = 0.0;
-        for (int p = 0; p < r; ++p) v += c->Y[(size_t)(m - r + p) * m + row] * ghat[a * r + p];
+        for (int p = 0; p < r; ++p) v += lcol[(size_t)p * m + row] * ghat[a * r + p];
         s2 += v * v;
       }
     const double rh = std::sqrt(s1 + s2);
@@ -1112,6 +1158,12 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
   }
   return guard(c, [&]() -> sylv_status {
     const int r = c->R, m = d * r, K = c->K;
+    if (c->y_dev) {                                   // Y of the last (device) solve
+      c->Y.resize((size_t)m * m);
+      CK(cudaMemcpyAsync(c->Y.data(), c->gsolve->C, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      c->y_dev = false;
+    }
     std::vector<double> Y1, Y2;
     std::string err;
     const int l = svd_truncate(m, c->Y, c->rank_tol, max_rank, Y1, Y2, err);

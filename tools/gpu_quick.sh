@@ -1,2 +1,5 @@
-for a in "32 8 3 2 6 notma" "32 8 2 2 6 tma" "34 8 3 3 6 tma"; do echo "== $a"; timeout 60 python tools/sharded_probe.py $a 2>&1 | grep "rank 0 step"; done > gpurun_out/probe2.log 2>&1
-for i in 1 2; do timeout 600 python -m pytest tests/test_gpu_sharded.py -q -p no:cacheprovider >> gpurun_out/gputest.log 2>&1; echo tests $?; done
+set -x
+timeout 120 python tools/proj_probe.py > gpurun_out/proj.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "device_projected or with_device" > gpurun_out/gputest.log 2>&1; echo tests $?
+for c in c2 c4; do timeout 300 python tools/ttt.py $c >> gpurun_out/ttt.log 2>&1; done
+timeout 900 python tools/ttt.py c3 >> gpurun_out/ttt.log 2>&1; echo c3 $?

@@ -1,6 +1,5 @@
-# round measurement: tests, bench (c3), launch list, ncu full of the steady-state hot kernels
+# round measurement: tests, bench (c3), launch list
 set -x
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; echo tests $?
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gputest.log 2>&1; echo tests $?
 timeout 900 python bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo bench $?
-timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu.log 2>&1; echo ncu $?
-timeout 300 python tools/quick_time.py c3 4 serial > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_st3d_r8|k_sketch_cols" -s 20 -c 3 -o gpurun_out/prof_c3 python tools/quick_time.py c3 4 serial > gpurun_out/ncu2.log 2>&1; echo ncufull $?
+for c in c2 c1; do timeout 600 python tools/ttt.py $c >> gpurun_out/ttt.log 2>&1; done
