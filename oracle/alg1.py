@@ -232,22 +232,22 @@ class SylvesterSketchedKrylov:
 
 
 def check_schedule(r: int, d_max: int) -> List[int]:
-    """Canonical check schedule (R9; p of Alg. 1 line 11 made explicit):
-    every step while d <= 50; then every 10 while d*r <= 800; then
-    d_next = 10*ceil(1.15*d_prev/10); d_max always included."""
-    out, d = [], 1
-    while d <= min(50, d_max):
+    """Canonical check schedule (R9; the p of Alg. 1 line 11 made explicit).  The paper
+    solves the projected equation every p iterations, p = 10 in its experiments
+    (P:979): every 10 steps while d*r <= 800; then
+    d_next = 10*ceil(1.15*d_prev/10); d_max always included.  The bisection of solve()
+    then recovers the smallest passing d inside the last bracket."""
+    out, d = [], 10
+    while d <= d_max and d * r <= 800:
         out.append(d)
-        d += 1
-    d = 50
+        d += 10
+    d = out[-1] if out else 10
     while True:
-        if (d + 10) * r <= 800:
-            d = d + 10
-        else:
-            d = 10 * math.ceil(1.15 * d / 10)
+        d = 10 * math.ceil(1.15 * d / 10)
         if d >= d_max:
             break
-        out.append(d)
+        if not out or d > out[-1]:
+            out.append(d)
     if not out or out[-1] != d_max:
         out.append(d_max)
     return [x for x in out if x <= d_max]

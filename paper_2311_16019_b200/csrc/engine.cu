@@ -1238,16 +1238,16 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
 
 sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
   if (!c) return SYLV_E_INVALID;
-  // canonical schedule (R9): every step to 50, every 10 while d r <= 800,
-  // then d_next = 10 ceil(1.15 d_prev / 10); d_max included; bisection after a pass.
+  // canonical schedule (R9; the paper's p = 10): every 10
+  // steps while d r <= 800, then d_next = 10 ceil(1.15 d_prev / 10); d_max included;
+  // bisection on the last bracket after the first pass.
   std::vector<int> sched;
-  for (int d = 1; d <= std::min(50, c->dmax); ++d) sched.push_back(d);
-  int d = 50;
+  for (int d = 10; d <= c->dmax && d * c->R <= 800; d += 10) sched.push_back(d);
+  int d = sched.empty() ? 10 : sched.back();
   while (true) {
-    if ((d + 10) * c->R <= 800) d += 10;
-    else d = 10 * (int)std::ceil(1.15 * d / 10.0);
+    d = 10 * (int)std::ceil(1.15 * d / 10.0);
     if (d >= c->dmax) break;
-    sched.push_back(d);
+    if (sched.empty() || d > sched.back()) sched.push_back(d);
   }
   if (sched.empty() || sched.back() != c->dmax) sched.push_back(c->dmax);
   int d_fail = 0, d_pass = -1, skips = 0;

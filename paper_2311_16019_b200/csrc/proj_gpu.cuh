@@ -59,6 +59,10 @@ __global__ void k_eye(double* __restrict__ X, int m) {
     X[e] = (e % (m + 1) == 0) ? 1.0 : 0.0;
 }
 
+__global__ void k_add_diag(double* __restrict__ X, int m, double v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) X[(int64_t)i * (m + 1)] += v;
+}
+
 // out[0] = sum_i log|LU_ii|  (one CTA, fixed order)
 __global__ void k_logdet(const double* __restrict__ LU, int m, double* __restrict__ out) {
   __shared__ double sm[256];
@@ -78,6 +82,7 @@ struct GpuSylv {
   cusolverDnHandle_t hs = nullptr;
   int cap = 0, capr = 0, lwork = 0;
   int mcap = 1 << 30;            // largest m ever needed ((d_max + 1) r)
+  cudaStream_t cur = nullptr;    // stream of the current solve
   double *A = nullptr, *B = nullptr, *C = nullptr, *Ai = nullptr, *Bi = nullptr, *W = nullptr, *LU = nullptr;
   double *Hb = nullptr, *work = nullptr, *dlog = nullptr;
   int *ipiv = nullptr, *info = nullptr;
@@ -108,6 +113,7 @@ struct GpuSylv {
   }
 
   void ensure(int m, int r, cudaStream_t st) {
+    cur = st;
     if (!hb) {
       ckb(cublasCreate(&hb), "cublasCreate");
       cks(cusolverDnCreate(&hs), "cusolverDnCreate");
@@ -162,6 +168,13 @@ struct GpuSylv {
     return ld;
   }
 
+  // the sign iteration must end at A = B = I (sign of matrices with spectra in Re > 0)
+  bool near_identity(const double* X, int m, cudaStream_t st) {
+    ck(cudaMemcpyAsync(LU, X, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy");
+    k_add_diag<<<(m + 255) / 256, 256, 0, st>>>(LU, m, -1.0);
+    return fro(LU, (int64_t)m * m) <= 1e-8 * std::sqrt((double)m);
+  }
+
   double fro(const double* X, int64_t n) {
     double v = 0.0;
     ckb(cublasDnrm2(hb, (int)n, X, 1, &v), "dnrm2");
@@ -172,6 +185,20 @@ struct GpuSylv {
   // On success Y (= C/2) is left in `C`; returns false if the iteration did not converge.
   bool solve(const double* TU, const double* HcU, const double* TV, const double* HcV, int64_t ldT, int d, int r,
              int K, const double* Bm, cudaStream_t st) {
+    if (solve_once(TU, HcU, TV, HcV, ldT, d, r, K, Bm, st, true)) return true;
+    return solve_once(TU, HcU, TV, HcV, ldT, d, r, K, Bm, st, false);   // pure Newton retry
+  }
+
+  // ||X^2 - I||_F / sqrt(m) (Newton-Schulz converges when this is < 1)
+  double sq_dev(const double* X, int m) {
+    const double one = 1.0, zero = 0.0;
+    ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, X, m, X, m, &zero, LU, m), "dgemm (X^2)");
+    k_add_diag<<<(m + 255) / 256, 256, 0, cur>>>(LU, m, -1.0);
+    return fro(LU, (int64_t)m * m) / std::sqrt((double)m);
+  }
+
+  bool solve_once(const double* TU, const double* HcU, const double* TV, const double* HcV, int64_t ldT, int d, int r,
+                  int K, const double* Bm, cudaStream_t st, bool allow_ns) {
     const int m = d * r;
     ensure(m, r, st);
     build_M(TU, ldT, HcU, d, r, K, A, st);
@@ -186,35 +213,66 @@ struct GpuSylv {
                          (size_t)r * sizeof(double), r, cudaMemcpyHostToDevice, st),
        "H2D (rhs)");
     const int64_t mm = (int64_t)m * m;
-    bool scale = true, last = false;
+    const double mone = -1.0, half = 0.5, c15 = 1.5, cm05 = -0.5;
+    bool scale = true, last = false, ns = false;
     for (iterations = 1; iterations <= 60; ++iterations) {
-      const double la = invert(A, Ai, m, st);
-      const double lb = invert(B, Bi, m, st);
-      const double mu = scale ? std::exp(-(la + lb) / (2.0 * m)) : 1.0;
-      // C <- (mu C + Ai C Bi / mu) / 2
-      ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, Ai, m, C, m, &zero, W, m), "dgemm (Ai C)");
-      const double a1 = 0.5 / mu, b1 = 0.5 * mu;
-      ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &a1, W, m, Bi, m, &b1, C, m), "dgemm (Ai C Bi)");
-      // A <- (mu A + Ai / mu) / 2; measure the change
-      const double h1 = 0.5 * mu, h2 = 0.5 / mu;
-      ckb(cublasDgeam(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, &h1, A, m, &h2, Ai, m, W, m), "geam (A)");
-      const double mone = -1.0;
-      ckb(cublasDaxpy(hb, (int)mm, &mone, W, 1, A, 1), "daxpy");          // A <- A_old - A_new
-      const double dA = fro(A, mm), nA = fro(W, mm);
-      std::swap(A, W);                                                     // A <- A_new
-      ckb(cublasDgeam(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, &h1, B, m, &h2, Bi, m, W, m), "geam (B)");
-      ckb(cublasDaxpy(hb, (int)mm, &mone, W, 1, B, 1), "daxpy");
-      const double dB = fro(B, mm), nB = fro(W, mm);
-      std::swap(B, W);
+      double dA, nA, dB, nB;
+      if (!ns) {
+        // scaled Newton step (needs A^{-1}, B^{-1}: LU)
+        const double la = invert(A, Ai, m, st);
+        const double lb = invert(B, Bi, m, st);
+        const double mu = scale ? std::exp(-(la + lb) / (2.0 * m)) : 1.0;
+        const double a1 = 0.5 / mu, b1 = 0.5 * mu;
+        // C <- (mu C + Ai C Bi / mu) / 2
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, Ai, m, C, m, &zero, W, m), "dgemm (Ai C)");
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &a1, W, m, Bi, m, &b1, C, m), "dgemm (Ai C Bi)");
+        // A <- (mu A + Ai / mu) / 2, B likewise (W = new, old - new kept for the change)
+        ckb(cublasDgeam(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, &b1, A, m, &a1, Ai, m, W, m), "geam (A)");
+        ckb(cublasDaxpy(hb, (int)mm, &mone, W, 1, A, 1), "daxpy");
+        dA = fro(A, mm);
+        nA = fro(W, mm);
+        std::swap(A, W);
+        ckb(cublasDgeam(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, &b1, B, m, &a1, Bi, m, W, m), "geam (B)");
+        ckb(cublasDaxpy(hb, (int)mm, &mone, W, 1, B, 1), "daxpy");
+        dB = fro(B, mm);
+        nB = fro(W, mm);
+        std::swap(B, W);
+      } else {
+        // Newton-Schulz step, inverse-free (valid once ||I - H^2|| < 1): H <- H (3I - H^2) / 2,
+        //   C <- (3C - C B^2 - A^2 C + A (C B)) / 2,  A <- (3A - A^3) / 2,  B <- (3B - B^3) / 2
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, A, m, A, m, &zero, Ai, m), "dgemm (A^2)");
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, B, m, B, m, &zero, Bi, m), "dgemm (B^2)");
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, C, m, B, m, &zero, W, m), "dgemm (C B)");
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, A, m, W, m, &zero, LU, m), "dgemm (A C B)");
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &mone, C, m, Bi, m, &one, LU, m), "dgemm (C B^2)");
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &mone, Ai, m, C, m, &one, LU, m), "dgemm (A^2 C)");
+        ckb(cublasDgeam(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, &c15, C, m, &half, LU, m, W, m), "geam (C)");
+        std::swap(C, W);
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, A, m, Ai, m, &zero, LU, m), "dgemm (A^3)");
+        ckb(cublasDgeam(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, &c15, A, m, &cm05, LU, m, W, m), "geam (A)");
+        ckb(cublasDaxpy(hb, (int)mm, &mone, W, 1, A, 1), "daxpy");
+        dA = fro(A, mm);
+        nA = fro(W, mm);
+        std::swap(A, W);
+        ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, B, m, Bi, m, &zero, LU, m), "dgemm (B^3)");
+        ckb(cublasDgeam(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, &c15, B, m, &cm05, LU, m, W, m), "geam (B)");
+        ckb(cublasDaxpy(hb, (int)mm, &mone, W, 1, B, 1), "daxpy");
+        dB = fro(B, mm);
+        nB = fro(W, mm);
+        std::swap(B, W);
+      }
       const double rel = std::max(dA / nA, dB / nB);
       if (!std::isfinite(rel)) return false;
-      if (rel < 1e-2) scale = false;                      // quadratic phase: unscaled Newton
+      if (rel < 1e-2) scale = false;                      // quadratic phase: unscaled
       if (last || rel < 1e-14) {                          // one step after rel < 1e-7: error ~ rel^2
-        const double half = 0.5;
+        if (!near_identity(A, m, st) || !near_identity(B, m, st)) return false;   // wrong fixed point
         ckb(cublasDscal(hb, (int)mm, &half, C, 1), "dscal (Y = C/2)");
         return true;
       }
       if (rel < 1e-7) last = true;
+      // Newton-Schulz once inside its basin: ||A^2 - I||, ||B^2 - I|| well below 1 (checked,
+      // not inferred from the step size: the projected matrices can be far from normal)
+      if (allow_ns && !ns && rel < 5e-2 && sq_dev(A, m) < 0.3 && sq_dev(B, m) < 0.3) ns = true;
     }
     return false;
   }

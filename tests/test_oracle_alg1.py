@@ -191,13 +191,14 @@ def test_true_residual_matches_dense():
 
 def test_check_schedule():
     s8 = alg1.check_schedule(8, 600)
-    assert s8[:50] == list(range(1, 51))
-    assert s8[50:] == [60, 70, 80, 90, 100, 120, 140, 170, 200, 230, 270, 320, 370, 430, 500, 580, 600]
+    assert s8 == [10, 20, 30, 40, 50, 60, 70, 80, 90, 100, 120, 140, 170, 200, 230, 270, 320, 370, 430, 500,
+                  580, 600]
     s4 = alg1.check_schedule(4, 1500)
-    assert s4[50:66] == list(range(60, 201, 10)) + [230]
+    assert s4[:20] == list(range(10, 201, 10)) and s4[20] == 230
     assert s4[-1] == 1500
     s1 = alg1.check_schedule(1, 300)
-    assert s1[50:] == list(range(60, 301, 10))
+    assert s1 == list(range(10, 301, 10))
+    assert alg1.check_schedule(8, 7) == [7]
 
 
 def test_c0_regression_expectation():
