@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../../include/sylv_sketch.h"
 #include "common.cuh"
 #include "host_solve.hpp"
@@ -260,45 +262,68 @@ OpParams make_op(const sylv_operator* A, bool transpose) {
   return op;
 }
 
-// Host CSR (possibly transposed) upload.
+// ---- CSR upload; B^T by a stable device sort of the nonzeros by column -------------------
+__global__ void k_row_of(const int64_t* __restrict__ rp, int64_t n, int32_t* __restrict__ row_of) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) row_of[p] = (int32_t)i;
+}
+__global__ void k_iota32(int32_t* __restrict__ x, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = (int32_t)i;
+}
+// B^T in CSR = B in CSC: nonzero k of the sorted order is (col key[k], row row_of[perm[k]])
+__global__ void k_csr_transpose_fill(const int32_t* __restrict__ key, const int32_t* __restrict__ perm,
+                                     const int32_t* __restrict__ row_of, const double* __restrict__ cv, int64_t nnz,
+                                     int64_t n, int32_t* __restrict__ tci, double* __restrict__ tcv,
+                                     int64_t* __restrict__ tp) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t pk = perm[k];
+    tci[k] = row_of[pk];
+    tcv[k] = cv[pk];
+    // row pointers of B^T: every column c in (key[k-1], key[k]] starts at k
+    for (int64_t c = (k == 0 ? 0 : (int64_t)key[k - 1] + 1); c <= key[k]; ++c) tp[c] = k;
+    if (k == nnz - 1)
+      for (int64_t c = (int64_t)key[k] + 1; c <= n; ++c) tp[c] = nnz;
+  }
+}
+
+// CSR of A (or B^T when transpose): host or device input arrays, uploaded as they are; the
+// transpose is a stable radix sort of the nonzeros by column on the device (rows stay
+// ascending inside each column, so B^T's rows are sorted and the result is deterministic).
 void upload_csr(Sequence& q, const sylv_operator* A, bool transpose, cudaStream_t st) {
   const int64_t n = A->n, nnz = A->nnz;
-  std::vector<int64_t> rp(n + 1);
-  std::vector<int32_t> ci(nnz);
-  std::vector<double> cv(nnz);
   const bool dev = is_device_ptr(A->row_ptr);
-  if (dev) {
-    CK(cudaMemcpy(rp.data(), A->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(ci.data(), A->col_idx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(cv.data(), A->val, nnz * sizeof(double), cudaMemcpyDeviceToHost));
-  } else {
-    std::memcpy(rp.data(), A->row_ptr, (n + 1) * sizeof(int64_t));
-    std::memcpy(ci.data(), A->col_idx, nnz * sizeof(int32_t));
-    std::memcpy(cv.data(), A->val, nnz * sizeof(double));
-  }
-  if (transpose) {  // counting-sort transpose: B^T in CSR = B in CSC (rows sorted by construction)
-    std::vector<int64_t> tp(n + 1, 0);
-    for (int64_t p = 0; p < nnz; ++p) tp[ci[p] + 1]++;
-    for (int64_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
-    std::vector<int64_t> pos(tp.begin(), tp.end() - 1);
-    std::vector<int32_t> tci(nnz);
-    std::vector<double> tcv(nnz);
-    for (int64_t i = 0; i < n; ++i)
-      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-        const int64_t dst = pos[ci[p]]++;
-        tci[dst] = (int32_t)i;
-        tcv[dst] = cv[p];
-      }
-    rp.swap(tp);
-    ci.swap(tci);
-    cv.swap(tcv);
-  }
+  const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   q.rp = dalloc<int64_t>(n + 1);
   q.ci = dalloc<int32_t>(nnz);
   q.cv = dalloc<double>(nnz);
-  CK(cudaMemcpyAsync(q.rp, rp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(q.ci, ci.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(q.cv, cv.data(), nnz * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (n >= (1ll << 31) || nnz >= (1ll << 31)) throw Status{SYLV_E_INVALID, "CSR n and nnz must be < 2^31"};
+  if (!transpose) {
+    CK(cudaMemcpyAsync(q.rp, A->row_ptr, (n + 1) * sizeof(int64_t), kind, st));
+    CK(cudaMemcpyAsync(q.ci, A->col_idx, nnz * sizeof(int32_t), kind, st));
+    CK(cudaMemcpyAsync(q.cv, A->val, nnz * sizeof(double), kind, st));
+  } else {
+    int64_t* rp = dalloc<int64_t>(n + 1);
+    int32_t *key = dalloc<int32_t>(nnz), *key2 = dalloc<int32_t>(nnz);
+    int32_t *perm = dalloc<int32_t>(nnz), *perm2 = dalloc<int32_t>(nnz), *row_of = dalloc<int32_t>(nnz);
+    double* cv = dalloc<double>(nnz);
+    CK(cudaMemcpyAsync(rp, A->row_ptr, (n + 1) * sizeof(int64_t), kind, st));
+    CK(cudaMemcpyAsync(key, A->col_idx, nnz * sizeof(int32_t), kind, st));
+    CK(cudaMemcpyAsync(cv, A->val, nnz * sizeof(double), kind, st));
+    k_row_of<<<1024, 256, 0, st>>>(rp, n, row_of);
+    k_iota32<<<1024, 256, 0, st>>>(perm, nnz);
+    int end_bit = 1;
+    while ((1ll << end_bit) < n) ++end_bit;
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, perm, perm2, (int)nnz, 0, end_bit, st));
+    void* tmp = dalloc<char>(tmp_bytes);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, perm, perm2, (int)nnz, 0, end_bit, st));
+    k_csr_transpose_fill<<<1024, 256, 0, st>>>(key2, perm2, row_of, cv, nnz, n, q.ci, q.cv, q.rp);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    for (void* p : {(void*)rp, (void*)key, (void*)key2, (void*)perm, (void*)perm2, (void*)row_of, (void*)cv, tmp})
+      cudaFree(p);
+  }
   CK(cudaStreamSynchronize(st));
   q.op.rp = q.rp;
   q.op.ci = q.ci;
@@ -472,6 +497,8 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cud
       case 3: k_st3d_r8<kTY25, 3, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
       case 4: k_st3d_r8<kTY25, 4, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
     }
+  } else if (q.op.kind == kCSR && R <= 4) {
+    SYLV_DISPATCH_R124_K(R, K, { k_pass1_csr<R_, K_><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); });
   } else if (R == 8) {
     switch (K) {
       case 1: k_pass1_r8<1><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); break;
@@ -1105,6 +1132,16 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
       std::vector<double> MU, MV;
       build_projected(d, r, c->K, U.Th, U.ldT, U.Hh, MU);
       build_projected(d, r, c->K, V.Th, V.ldT, V.Hh, MV);
+      // a numerically singular T_d (sketched basis lost independence) gives non-finite M;
+      // LAPACK's Schur iteration must not see it
+      for (const std::vector<double>* Mx : {&MU, &MV})
+        for (double v : *Mx)
+          if (!std::isfinite(v)) {
+            c->y_d = -1;
+            if (rho) *rho = NAN;
+            if (rho_rel) *rho_rel = NAN;
+            return fail(c, SYLV_E_SINGULAR, "projected matrix not finite at d = " + std::to_string(d));
+          }
       std::string err;
       const int info = sylvester_bs(m, r, MU, MV, Bm, c->Y, err);
       c->stats.host_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -238,6 +238,69 @@ __global__ void __launch_bounds__(kThreads) k_pass2_rows(OpParams op, Win win, i
 }
 
 // =====================================================================================
+// CSR pass 1 (a1 + a2 inner products): 8 lanes per row
+// =====================================================================================
+// Each 8-lane sub-warp owns one row at a time: lanes stride over the row's nonzeros
+// (coalesced col/val loads), accumulate all R columns of (A Z_d)[row] from ONE sweep
+// of the row (the generic kernel re-walks the row per column), and reduce with three
+// xor-shuffles.  The sub-warp's lane 0 stores Yt[row] (pass 2 streams it instead of
+// re-reading A) and accumulates P_i += Z_i[row]^T Yt[row].
+constexpr int kCsrLanes = 8;
+
+template <int R, int K>
+__global__ void __launch_bounds__(kThreads) k_pass1_csr(OpParams op, Win win, int nwin, int64_t ld,
+                                                        double* __restrict__ Yt, double* __restrict__ partial) {
+  __shared__ double sm[kWarps * K * R * R];
+  double acc[K * R * R];
+#pragma unroll
+  for (int e = 0; e < K * R * R; ++e) acc[e] = 0.0;
+  const int sub = threadIdx.x & (kCsrLanes - 1);
+  const double* __restrict__ Zd = win.p[nwin - 1];
+  const int64_t nsub = (int64_t)gridDim.x * (kThreads / kCsrLanes);
+  // warp-uniform trip count: every lane of a warp runs the same iterations (the shuffles
+  // below use the full mask); sub-warps past the last row do no work
+  const int64_t wfirst = (int64_t)blockIdx.x * (kThreads / kCsrLanes) + (threadIdx.x & ~31) / kCsrLanes;
+  for (int64_t wrow = wfirst; wrow < op.n; wrow += nsub) {
+    const int64_t row = wrow + (threadIdx.x & 31) / kCsrLanes;
+    const bool valid = row < op.n;
+    double y[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) y[c] = 0.0;
+    const int64_t p0 = valid ? __ldg(op.rp + row) : 0, p1 = valid ? __ldg(op.rp + row + 1) : 0;
+    for (int64_t p = p0 + sub; p < p1; p += kCsrLanes) {
+      const double a = __ldg(op.cv + p);
+      const int64_t col = __ldg(op.ci + p);
+#pragma unroll
+      for (int c = 0; c < R; ++c) y[c] = fma(a, __ldg(Zd + c * ld + col), y[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+#pragma unroll
+      for (int off = kCsrLanes / 2; off > 0; off >>= 1) y[c] += __shfl_xor_sync(SYLV_FULL_MASK, y[c], off);
+    }
+    if (sub == 0 && valid) {
+      if (Yt) {
+#pragma unroll
+        for (int c = 0; c < R; ++c) Yt[c * ld + row] = y[c];
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        if (i < nwin) {
+          double z[R];
+#pragma unroll
+          for (int a = 0; a < R; ++a) z[a] = __ldg(win.p[i] + a * ld + row);
+#pragma unroll
+          for (int a = 0; a < R; ++a)
+#pragma unroll
+            for (int c = 0; c < R; ++c) acc[(i * R + a) * R + c] = fma(z[a], y[c], acc[(i * R + a) * R + c]);
+        }
+      }
+    }
+  }
+  cta_reduce_store<K * R * R>(acc, partial, sm);
+}
+
+// =====================================================================================
 // r = 8: DMMA warp tiles
 // =====================================================================================
 

@@ -1,3 +1,2 @@
-timeout 900 python tools/proj_probe2.py > gpurun_out/proj2.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "device_projected or with_device or full_solve" > gpurun_out/gputest.log 2>&1; echo tests $?
-for c in c2 c3; do timeout 600 python tools/ttt.py $c >> gpurun_out/ttt.log 2>&1; done
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "csr" -o faulthandler_timeout=100 > gpurun_out/gputest.log 2>&1; echo tests $?
+timeout 200 python tools/quick_time.py c4 10 serial > gpurun_out/qt.log 2>&1; echo qt $?
