@@ -400,24 +400,25 @@ bool encode_block_map(CUtensorMap* m, const double* base, int N, int depth, int6
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int K>
+template <int R, int K>
 size_t smem25_bytes() {
-  using Gm = Geo25<kTY25>;
-  return (size_t)kNS * (Gm::HCOL * 8 + (K - 1) * Gm::WCOL * 8) * 8 + kNS * 8;
+  using Gm = Geo25<kTY25, R>;
+  constexpr int ns = stages25<R>();
+  return (size_t)ns * (Gm::HCOL * R + (K - 1) * Gm::WCOL * R) * 8 + ns * 8;
 }
 
-template <int K>
+template <int R, int K>
 void set_smem25(sylv_ctx* c) {
-  c->smem25_1 = c->smem25_2 = smem25_bytes<K>();
-  CK(cudaFuncSetAttribute(k_st3d_r8<kTY25, K, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_1));
-  CK(cudaFuncSetAttribute(k_st3d_r8<kTY25, K, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_2));
-  CK(cudaFuncSetAttribute(k_st3d_r8<kTY25, K, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_2));
+  c->smem25_1 = c->smem25_2 = smem25_bytes<R, K>();
+  CK(cudaFuncSetAttribute(k_st3d<kTY25, R, K, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_1));
+  CK(cudaFuncSetAttribute(k_st3d<kTY25, R, K, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_2));
+  CK(cudaFuncSetAttribute(k_st3d<kTY25, R, K, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_2));
 }
 
-// Set up the TMA path for sequence q if eligible: 3-D stencil, r = 8, even N.
+// Set up the TMA path for sequence q if eligible: 3-D stencil, r = 4 or 8, even N.
 void setup_tma(sylv_ctx* c, Sequence& q) {
   q.tma = false;
-  if ((c->cflags & 4) || q.op.kind != kStencil3D || c->R != 8 || (q.op.N & 1) || q.op.N < 2) return;
+  if ((c->cflags & 4) || q.op.kind != kStencil3D || (c->R != 8 && c->R != 4) || (q.op.N & 1) || q.op.N < 2) return;
   const int N = q.op.N;
   const int nz = (int)(q.n / ((int64_t)N * N));
   for (int j = 0; j <= c->K; ++j) {
@@ -432,7 +433,7 @@ void setup_tma(sylv_ctx* c, Sequence& q) {
   p.tiles_x = (N + kTx - 1) / kTx;
   p.tiles_y = (N + kTY25 - 1) / kTY25;
   const int64_t tiles = (int64_t)p.tiles_x * p.tiles_y;
-  const int grid = 2 * c->sm;
+  const int grid = (c->R == 4 ? 3 : 2) * c->sm;   // resident CTAs: r = 4 stages are half the size
   int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, nz / 16), (8 * grid + tiles - 1) / tiles));
   p.zseg = (nz + nseg - 1) / nseg;
   p.nseg = (nz + p.zseg - 1) / p.zseg;
@@ -443,11 +444,20 @@ void setup_tma(sylv_ctx* c, Sequence& q) {
   p.czm = q.op.czm; p.czp = q.op.czp;
   p.dbg = getenv("SYLV_DBG") ? atoi(getenv("SYLV_DBG")) : 0;
   c->G25 = (int)std::min<int64_t>(p.items, grid);
-  switch (c->K) {
-    case 1: set_smem25<1>(c); break;
-    case 2: set_smem25<2>(c); break;
-    case 3: set_smem25<3>(c); break;
-    case 4: set_smem25<4>(c); break;
+  if (c->R == 8) {
+    switch (c->K) {
+      case 1: set_smem25<8, 1>(c); break;
+      case 2: set_smem25<8, 2>(c); break;
+      case 3: set_smem25<8, 3>(c); break;
+      case 4: set_smem25<8, 4>(c); break;
+    }
+  } else {
+    switch (c->K) {
+      case 1: set_smem25<4, 1>(c); break;
+      case 2: set_smem25<4, 2>(c); break;
+      case 3: set_smem25<4, 3>(c); break;
+      case 4: set_smem25<4, 4>(c); break;
+    }
   }
   q.tma = true;
 }
@@ -491,12 +501,23 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cud
   const int R = c->R, K = c->K;
   if (q.tma) {
     const Tma25 tm = tma_args(q, j, nwin);
-    switch (K) {
-      case 1: k_st3d_r8<kTY25, 1, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
-      case 2: k_st3d_r8<kTY25, 2, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
-      case 3: k_st3d_r8<kTY25, 3, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
-      case 4: k_st3d_r8<kTY25, 4, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1); break;
+#define SYLV_ST3D_P1(RR, KK) k_st3d<kTY25, RR, KK, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nwin, nullptr, nullptr, q.part1)
+    if (R == 8) {
+      switch (K) {
+        case 1: SYLV_ST3D_P1(8, 1); break;
+        case 2: SYLV_ST3D_P1(8, 2); break;
+        case 3: SYLV_ST3D_P1(8, 3); break;
+        case 4: SYLV_ST3D_P1(8, 4); break;
+      }
+    } else {
+      switch (K) {
+        case 1: SYLV_ST3D_P1(4, 1); break;
+        case 2: SYLV_ST3D_P1(4, 2); break;
+        case 3: SYLV_ST3D_P1(4, 3); break;
+        case 4: SYLV_ST3D_P1(4, 4); break;
+      }
     }
+#undef SYLV_ST3D_P1
   } else if (q.op.kind == kCSR && R <= 4) {
     SYLV_DISPATCH_R124_K(R, K, { k_pass1_csr<R_, K_><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); });
   } else if (R == 8) {
@@ -518,12 +539,23 @@ void launch_pass2(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, con
   const int R = c->R, K = c->K;
   if (q.tma && allow_tma) {
     const Tma25 tm = tma_args(q, j, nwin);
-    switch (K) {
-      case 1: k_st3d_r8<kTY25, 1, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2); break;
-      case 2: k_st3d_r8<kTY25, 2, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2); break;
-      case 3: k_st3d_r8<kTY25, 3, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2); break;
-      case 4: k_st3d_r8<kTY25, 4, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2); break;
+#define SYLV_ST3D_P2(RR, KK) k_st3d<kTY25, RR, KK, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2)
+    if (R == 8) {
+      switch (K) {
+        case 1: SYLV_ST3D_P2(8, 1); break;
+        case 2: SYLV_ST3D_P2(8, 2); break;
+        case 3: SYLV_ST3D_P2(8, 3); break;
+        case 4: SYLV_ST3D_P2(8, 4); break;
+      }
+    } else {
+      switch (K) {
+        case 1: SYLV_ST3D_P2(4, 1); break;
+        case 2: SYLV_ST3D_P2(4, 2); break;
+        case 3: SYLV_ST3D_P2(4, 3); break;
+        case 4: SYLV_ST3D_P2(4, 4); break;
+      }
     }
+#undef SYLV_ST3D_P2
   } else if (R == 8) {
     switch (K) {
       case 1: k_pass2_r8<1, GRAM><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, Yt, coef, out, q.part2); break;
@@ -587,7 +619,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.Hc = dalloc<double>((size_t)(c->dmax + 1) * (K + 1) * R * R);
   q.hn2 = dalloc<double>(c->dmax + 1);
   q.flags = dalloc<int>(c->dmax + 2);
-  const int gmax = std::max(c->G, 2 * c->sm);
+  const int gmax = std::max(c->G, 3 * c->sm);
   q.part1 = dalloc<double>((size_t)gmax * K * R * R);
   q.part2 = dalloc<double>((size_t)gmax * R * R);
   q.part_s = dalloc<double>((size_t)c->G * R * R);

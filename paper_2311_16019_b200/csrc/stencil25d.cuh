@@ -38,7 +38,10 @@
 namespace sylv {
 
 constexpr int kTx = 32;          // tile width in x (points)
-constexpr int kNS = 3;           // pipeline stages (planes)
+// pipeline stages (planes in flight): enough bytes in flight per SM to cover HBM latency
+// (r = 4 tiles carry half the bytes of r = 8 ones)
+template <int R>
+constexpr int stages25() { return R >= 8 ? 3 : 6; }
 
 struct Tma25 {
   CUtensorMap zd;                // halo box map of Z_d's ring slot
@@ -56,14 +59,14 @@ struct St25 {
   int dbg;                       // development switches (SYLV_DBG), 0 in production
 };
 
-template <int TY>
+template <int TY, int R = 8>
 struct Geo25 {
   static constexpr int HX = kTx + 6, HY = TY + 2;      // halo box
   static constexpr int WX = kTx + 2;                   // window box width
   static constexpr int HCOL = HX * HY;                 // doubles per column, halo box
   static constexpr int WCOL = WX * TY;                 // doubles per column, window box
-  static constexpr int HBYTES = 8 * HCOL * 8;
-  static constexpr int WBYTES = 8 * WCOL * 8;
+  static constexpr int HBYTES = R * HCOL * 8;
+  static constexpr int WBYTES = R * WCOL * 8;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -112,36 +115,39 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 
 // Issue the loads of plane p into stage `st` (thread 0 only).  Window blocks are needed
 // only for the planes the CTA computes (with_win).
-template <int TY>
+template <int TY, int R>
 __device__ __forceinline__ void issue_plane(const Tma25& tm, int nwin, double* stage, uint64_t* bar, int x0,
                                             int y0, int p, bool with_win, int dbg = 0) {
   if (dbg & 1) with_win = false;
-  using Gm = Geo25<TY>;
+  using Gm = Geo25<TY, R>;
   const uint32_t bytes = Gm::HBYTES + (with_win ? (uint32_t)(nwin - 1) * Gm::WBYTES : 0u);
   mbar_expect_tx(bar, bytes);
   tma_load_4d(stage, &tm.zd, x0 > 0 ? x0 - 2 : 0, y0 > 0 ? y0 - 1 : 0, p, 0, bar);
   if (with_win)
     for (int i = 0; i < nwin - 1; ++i)
-      tma_load_4d(stage + Gm::HCOL * 8 + i * Gm::WCOL * 8, &tm.win[i], x0, y0, p, 0, bar);
+      tma_load_4d(stage + Gm::HCOL * R + i * Gm::WCOL * R, &tm.win[i], x0, y0, p, 0, bar);
 }
 
 // ---------------------------------------------------------------------------------------
-// The kernel.  PASS = 1: partial[blk][i*64 + a*8 + c] = sum Z_i[.,a] Y[.,c] (P_i, DMMA D
-// layout [a][c]).  PASS = 2: Wout = W' (SoA), partial[blk][a*8 + c] = (W'^T W')[a][c]
-// when GRAM.  coef (pass 2) = [R_d, K_0 .. K_{nwin-1}] row-major 8 x 8.
+// The kernel (R = 8 or 4 block columns; the DMMA fragments are 8 wide, columns >= R are
+// zero and never loaded or stored).  PASS = 1: partial[blk][(i*R + a)*R + c] =
+// sum Z_i[.,a] Y[.,c] (P_i).  PASS = 2: Wout = W' (SoA), partial[blk][a*R + c] =
+// (W'^T W')[a][c] when GRAM.  coef (pass 2) = [R_d, K_0 .. K_{nwin-1}] row-major R x R.
 // Element patterns (lane L, warp w owns line y0 + w of the tile; 32 points x0 .. x0+31):
 //   pass 1 (pattern A): element e = 0..7 is (point 4e + (L&3), column L>>2)
 //   pass 2 (pattern B): element e = 2q + h is (point 8q + (L>>2), column (L&3) + 4h)
 // ---------------------------------------------------------------------------------------
 #define DMMA25(...) do { if (!(p.dbg & 2)) dmma(__VA_ARGS__); } while (0)
-template <int TY, int K, int PASS, bool GRAM>
+template <int TY, int R, int K, int PASS, bool GRAM>
 __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
-    k_st3d_r8(const __grid_constant__ Tma25 tm, St25 p, int nwin, const double* __restrict__ coef,
-              double* __restrict__ Wout, double* __restrict__ partial) {
-  using Gm = Geo25<TY>;
+    k_st3d(const __grid_constant__ Tma25 tm, St25 p, int nwin, const double* __restrict__ coef,
+           double* __restrict__ Wout, double* __restrict__ partial) {
+  static_assert(R == 4 || R == 8, "R = 4 or 8");
+  constexpr int kNS = stages25<R>();
+  using Gm = Geo25<TY, R>;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* stages = reinterpret_cast<double*>(smraw);
-  constexpr int kStageD = Gm::HCOL * 8 + (K - 1) * Gm::WCOL * 8;   // doubles per stage
+  constexpr int kStageD = Gm::HCOL * R + (K - 1) * Gm::WCOL * R;   // doubles per stage
   uint64_t* bars = reinterpret_cast<uint64_t*>(smraw + (size_t)kNS * kStageD * 8);
   __shared__ double red[TY][64 * (PASS == 1 ? K : 1)];
 
@@ -155,6 +161,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
 
   // element coordinates inside the tile (point offset px in [0,32), column col)
   int px[8], col[8];
+  bool cok[8];                                  // column < R (else the element is zero)
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     if (PASS == 1) {
@@ -164,21 +171,26 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       px[e] = 8 * (e >> 1) + (lane >> 2);
       col[e] = (lane & 3) + 4 * (e & 1);
     }
+    cok[e] = col[e] < R;
+    if (!cok[e]) col[e] = 0;                    // keeps the (unused) addresses in range
   }
   // pass 2: A fragments of R_d^T and -K_i^T (A[m][k] = M^T[m][k'] = M[k'][m], k' = (L&3) + 4h)
   double aR[2] = {0.0, 0.0}, aK[K][2];
   if (PASS == 2) {
+    const int mm = lane >> 2;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) aR[h] = __ldg(coef + ((lane & 3) + 4 * h) * 8 + (lane >> 2));
+    for (int h = 0; h < 2; ++h) {
+      const int kk = (lane & 3) + 4 * h;
+      const bool ok = mm < R && kk < R;
+      aR[h] = ok ? __ldg(coef + kk * R + mm) : 0.0;
 #pragma unroll
-    for (int i = 0; i < K; ++i)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        aK[i][h] = (i < nwin) ? -__ldg(coef + (1 + i) * 64 + ((lane & 3) + 4 * h) * 8 + (lane >> 2)) : 0.0;
+      for (int i = 0; i < K; ++i) aK[i][h] = (ok && i < nwin) ? -__ldg(coef + (1 + i) * R * R + kk * R + mm) : 0.0;
+    }
   }
-  double acc[PASS == 1 ? K : 1][2];
+  // two accumulator sets (even / odd slices) halve the dependent DMMA chains
+  double acc[PASS == 1 ? K : 1][2], acc2[PASS == 1 ? K : 1][2];
 #pragma unroll
-  for (int i = 0; i < (PASS == 1 ? K : 1); ++i) acc[i][0] = acc[i][1] = 0.0;
+  for (int i = 0; i < (PASS == 1 ? K : 1); ++i) acc[i][0] = acc[i][1] = acc2[i][0] = acc2[i][1] = 0.0;
 
   if (p.dbg & 8) return;
   uint32_t phase = 0;   // bit s = parity of the next wait on stage s
@@ -195,7 +207,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       for (int q = z0 - 1; q < z0 - 1 + kNS && q <= z1; ++q) {
         if (q < 0) continue;                    // plane -1: Dirichlet zeros, never loaded
         const int s = stage_of(q);
-        issue_plane<TY>(tm, nwin, stages + (size_t)s * kStageD, &bars[s], x0, y0, q, q >= z0 && q < z1, p.dbg);
+        issue_plane<TY, R>(tm, nwin, stages + (size_t)s * kStageD, &bars[s], x0, y0, q, q >= z0 && q < z1, p.dbg);
       }
     }
     const int sx = x0 > 0 ? 2 : 0, sy = y0 > 0 ? 1 : 0;
@@ -214,7 +226,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       phase ^= 1u << s;
       const double* H = stages + (size_t)s * kStageD;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) dst[e] = H[(col[e] * Gm::HY + yrow) * Gm::HX + px[e] + sx];
+      for (int e = 0; e < 8; ++e) dst[e] = cok[e] ? H[(col[e] * Gm::HY + yrow) * Gm::HX + px[e] + sx] : 0.0;
     };
     read_centers(z0 - 1, zm);
     read_centers(z0, zc);
@@ -223,15 +235,19 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       const int q = z0 - 1 + kNS;
       const int s = stage_of(q);
       if (!(p.dbg & 4)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_plane<TY>(tm, nwin, stages + (size_t)s * kStageD, &bars[s], x0, y0, q, q < z1, p.dbg);
+      issue_plane<TY, R>(tm, nwin, stages + (size_t)s * kStageD, &bars[s], x0, y0, q, q < z1, p.dbg);
     }
     for (int z = z0; z < z1; ++z) {
       read_centers(z + 1, zp);                  // waits for plane z+1 (plane z is ready since z-1)
       const double* H = stages + (size_t)stage_of(z) * kStageD;
-      const double* Wb = H + Gm::HCOL * 8;
+      const double* Wb = H + Gm::HCOL * R;
       double y[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
+        if (!cok[e]) {
+          y[e] = 0.0;
+          continue;
+        }
         const double* hc = H + (col[e] * Gm::HY + yrow) * Gm::HX + px[e] + sx;
         const double xm = (x0 + px[e] > 0) ? hc[-1] : 0.0;
         const double ym = has_ym ? hc[-Gm::HX] : 0.0;
@@ -251,9 +267,10 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             if (i < nwin - 1) {
-              DMMA25(acc[i], Wb[i * Gm::WCOL * 8 + (col[e] * TY + warp) * Gm::WX + px[e]], y[e]);
+              const double zi = cok[e] ? Wb[i * Gm::WCOL * R + (col[e] * TY + warp) * Gm::WX + px[e]] : 0.0;
+              if (e & 1) DMMA25(acc2[i], zi, y[e]); else DMMA25(acc[i], zi, y[e]);
             } else if (i == nwin - 1) {
-              DMMA25(acc[i], zc[e], y[e]);
+              if (e & 1) DMMA25(acc2[i], zc[e], y[e]); else DMMA25(acc[i], zc[e], y[e]);
             }
           }
         }
@@ -263,24 +280,25 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
         for (int q = 0; q < 4; ++q) {
           double D[2] = {0.0, 0.0};
           DMMA25(D, aR[0], y[2 * q]);
-          DMMA25(D, aR[1], y[2 * q + 1]);
+          if (R == 8) DMMA25(D, aR[1], y[2 * q + 1]);
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             if (i < nwin - 1) {
-              const double* wi = Wb + i * Gm::WCOL * 8;
-              DMMA25(D, aK[i][0], wi[(col[2 * q] * TY + warp) * Gm::WX + px[2 * q]]);
-              DMMA25(D, aK[i][1], wi[(col[2 * q + 1] * TY + warp) * Gm::WX + px[2 * q + 1]]);
+              const double* wi = Wb + i * Gm::WCOL * R;
+              DMMA25(D, aK[i][0], cok[2 * q] ? wi[(col[2 * q] * TY + warp) * Gm::WX + px[2 * q]] : 0.0);
+              if (R == 8) DMMA25(D, aK[i][1], wi[(col[2 * q + 1] * TY + warp) * Gm::WX + px[2 * q + 1]]);
             } else if (i == nwin - 1) {
               DMMA25(D, aK[i][0], zc[2 * q]);
-              DMMA25(D, aK[i][1], zc[2 * q + 1]);
+              if (R == 8) DMMA25(D, aK[i][1], zc[2 * q + 1]);
             }
           }
           // D: lane holds W'[point 8q + 2(L&3) + e][column L>>2]
           const int xo = 8 * q + 2 * (lane & 3);
-          const bool ok0 = yok && (x0 + xo) < NN, ok1 = yok && (x0 + xo + 1) < NN;
+          const bool cw = (lane >> 2) < R;      // output column exists
+          const bool ok0 = cw && yok && (x0 + xo) < NN, ok1 = cw && yok && (x0 + xo + 1) < NN;
           D[0] = ok0 ? D[0] : 0.0;
           D[1] = ok1 ? D[1] : 0.0;
-          double* dst = Wout + (int64_t)(lane >> 2) * p.ld + rowbase + xo;
+          double* dst = Wout + (int64_t)(cw ? (lane >> 2) : 0) * p.ld + rowbase + xo;
           if (ok1) {
             *reinterpret_cast<double2*>(dst) = make_double2(D[0], D[1]);
           } else if (ok0) {
@@ -293,7 +311,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
               const double v0 = __shfl_sync(SYLV_FULL_MASK, D[0], src);
               const double v1 = __shfl_sync(SYLV_FULL_MASK, D[1], src);
               const double v = (lane & 1) ? v1 : v0;
-              DMMA25(acc[0], v, v);
+              if (u) DMMA25(acc2[0], v, v); else DMMA25(acc[0], v, v);
             }
           }
         }
@@ -309,7 +327,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
         if (q <= z1) {
           const int s = stage_of(q);
           if (!(p.dbg & 4)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue_plane<TY>(tm, nwin, stages + (size_t)s * kStageD, &bars[s], x0, y0, q, q < z1, p.dbg);
+          issue_plane<TY, R>(tm, nwin, stages + (size_t)s * kStageD, &bars[s], x0, y0, q, q < z1, p.dbg);
         }
       }
     }
@@ -320,15 +338,16 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
     constexpr int NA = (PASS == 1 ? K : 1);
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
-      red[warp][i * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = acc[i][0];
-      red[warp][i * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc[i][1];
+      red[warp][i * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = acc[i][0] + acc2[i][0];
+      red[warp][i * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc[i][1] + acc2[i][1];
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < NA * 64; e += blockDim.x) {
+    for (int e = threadIdx.x; e < NA * R * R; e += blockDim.x) {
+      const int i = e / (R * R), a = (e / R) % R, c = e % R;      // R x R blocks of the 8 x 8 D
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < TY; ++w) s += red[w][e];
-      partial[(int64_t)blockIdx.x * NA * 64 + e] = s;
+      for (int w = 0; w < TY; ++w) s += red[w][i * 64 + a * 8 + c];
+      partial[(int64_t)blockIdx.x * NA * R * R + e] = s;
     }
   }
 }

@@ -32,6 +32,8 @@ CASES = {
     "3d-r8k3-tma": dict(kind="stencil3d", N=34, r=8, k=3, d_max=55),
     "3d-r8k2-tma": dict(kind="stencil3d", N=20, r=8, k=2, d_max=55),
     "3d-r8k4-tma": dict(kind="stencil3d", N=26, r=8, k=4, d_max=55),
+    "3d-r4k2-tma": dict(kind="stencil3d", N=34, r=4, k=2, d_max=55),
+    "3d-r4k3-tma": dict(kind="stencil3d", N=20, r=4, k=3, d_max=55),
     "3d-r2k1": dict(kind="stencil3d", N=11, r=2, k=1, d_max=55),
     "csr-r2": dict(kind="csr", n=20011, nnz_off=20, band=300, r=2, k=2, d_max=55),
     "csr-r4k4": dict(kind="csr", n=5003, nnz_off=6, band=40, r=4, k=4, d_max=55),
@@ -201,7 +203,7 @@ def test_sketch_full_config_sizes(name):
     gpu.close()
 
 
-@pytest.mark.parametrize("name", ["3d-r8k3-tma", "3d-r8k4-tma"])
+@pytest.mark.parametrize("name", ["3d-r8k3-tma", "3d-r8k4-tma", "3d-r4k2-tma", "3d-r4k3-tma"])
 def test_tma_passes_match_generic_passes(name):
     """The 2.5-D TMA passes and the generic DMMA passes compute the same recurrence: window
     blocks and per-step rho agree to rounding (1e-12 relative) over 20 steps."""
