@@ -62,10 +62,30 @@ bool is_device_ptr(const void* p) {
 
 template <typename T>
 T* dalloc(size_t count) {
+  // Stream-ordered allocation from the device's default memory pool, kept reserved after
+  // frees (release threshold = max): a new context reuses the previous one's ~10 GB
+  // instead of going back to the driver (context init 0.1-0.3 s -> ~0.05 s).
+  static bool pool_set = [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    return true;
+  }();
+  (void)pool_set;
   T* p = nullptr;
   if (count == 0) count = 1;
-  CK(cudaMalloc(&p, count * sizeof(T)));
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), 0));
+  CK(cudaStreamSynchronize(0));   // usable from any stream of the context
   return p;
+}
+
+// Free a dalloc'ed buffer (callers have synchronised the streams that used it).
+void dfree(void* p) {
+  if (p) cudaFreeAsync(p, 0);
 }
 
 // ----------------------------------------------------------------------------------
@@ -322,7 +342,7 @@ void upload_csr(Sequence& q, const sylv_operator* A, bool transpose, cudaStream_
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     for (void* p : {(void*)rp, (void*)key, (void*)key2, (void*)perm, (void*)perm2, (void*)row_of, (void*)cv, tmp})
-      cudaFree(p);
+      dfree(p);
   }
   CK(cudaStreamSynchronize(st));
   q.op.rp = q.rp;
@@ -335,13 +355,12 @@ void free_seq(Sequence& q) {
   for (cudaEvent_t e : q.ev_sk) cudaEventDestroy(e);
   double* dp[] = {q.ring, q.Cdev, q.Yt, q.sk, q.skpart, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
                   q.part1, q.part2, q.part_s, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv};
-  for (double* p : dp)
-    if (p) cudaFree(p);
-  if (q.flags) cudaFree(q.flags);
-  if (q.rp) cudaFree(q.rp);
-  if (q.ci) cudaFree(q.ci);
+  for (double* p : dp) dfree(p);
+  dfree(q.flags);
+  dfree(q.rp);
+  dfree(q.ci);
   if (q.Hh) cudaFreeHost(q.Hh);
-  if (q.Th) cudaFreeHost(q.Th);
+  delete[] q.Th;
   if (q.Rh) cudaFreeHost(q.Rh);
   if (q.flags_h) cudaFreeHost(q.flags_h);
   q = Sequence{};
@@ -582,8 +601,22 @@ void launch_sketch(sylv_ctx* c, Sequence& q, const double* X, int R, const doubl
   count(c, 2);
 }
 
+// SYLV_TRACE_INIT=1: wall time of the init phases on stderr (development aid)
+struct InitTrace {
+  bool on = std::getenv("SYLV_TRACE_INIT") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[init] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, bool transpose,
                    const double* C, uint64_t seed) {
+  InitTrace tr;
   q.which = which;
   q.R = c->R;
   q.K = c->K;
@@ -605,6 +638,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   const int64_t blk = q.ld * R, sR = c->s * R, ldT = q.ldT;
   if (A->kind == SYLV_OP_CSR) upload_csr(q, A, transpose, c->st);
 
+  tr.mark("setup", c->st);
   q.ring = dalloc<double>((size_t)(K + 1) * blk);
   q.Cdev = dalloc<double>(blk);
   if (A->kind == SYLV_OP_CSR) q.Yt = dalloc<double>(blk);
@@ -635,15 +669,17 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.qcpart = dalloc<double>((size_t)c->CC * sR);
   q.small = dalloc<double>(512);
   CK(cudaMemsetAsync(q.ring, 0, (size_t)(K + 1) * blk * sizeof(double), c->st));
+  tr.mark("device allocations + memsets", c->st);
   setup_tma(c, q);
+  tr.mark("tensor maps", c->st);
   CK(cudaMemsetAsync(q.Tdev, 0, (size_t)ldT * ldT * sizeof(double), c->st));
   CK(cudaMemsetAsync(q.flags, 0, (c->dmax + 2) * sizeof(int), c->st));
   CK(cudaMemsetAsync(q.Hc, 0, (size_t)(c->dmax + 1) * (K + 1) * R * R * sizeof(double), c->st));
   CK(cudaMallocHost(&q.Hh, (size_t)(c->dmax + 1) * (K + 1) * R * R * sizeof(double)));
-  CK(cudaMallocHost(&q.Th, (size_t)ldT * ldT * sizeof(double)));
+  q.Th = new double[(size_t)ldT * ldT];   // host copy of T, filled on demand (sync_T)
   CK(cudaMallocHost(&q.Rh, (size_t)(c->dmax + 2) * R * R * sizeof(double)));
   CK(cudaMallocHost(&q.flags_h, (c->dmax + 2) * sizeof(int)));
-  std::memset(q.Th, 0, (size_t)ldT * ldT * sizeof(double));
+  tr.mark("pinned host mirrors", c->st);
   std::memset(q.Hh, 0, (size_t)(c->dmax + 1) * (K + 1) * R * R * sizeof(double));
 
   // C (row-major, host or device) -> Cdev (SoA) and Z_1 (ring slot 1)
@@ -657,7 +693,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     if (c->comm) c->comm->halo(q.cdata(), R, q.ld, q.gz, c->st, kChanSetup);   // ghosts of Z_1 = C
     CK(cudaMemcpyAsync(q.slot(1) - q.gz, q.Cdev, blk * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     CK(cudaStreamSynchronize(c->st));
-    cudaFree(tmp);
+    dfree(tmp);
   }
   // Alg. 1 line 1: ell = chol(C^T C) (U_1 ell = C), S C -> CholQR2 -> beta, Q_1
   double* ell_d = q.small + 192;
@@ -674,19 +710,20 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   }
   count(c, 2);
   CK(cudaGetLastError());
+  tr.mark("C upload, SoA, halo, Gram", c->st);
   launch_sketch(c, q, q.cdata(), R, nullptr, q.sk, c->st);
   if (c->comm) c->comm->allreduce(q.sk, (size_t)q.s * R, c->st, kChanSetup);
   CK(cudaGetLastError());
+  tr.mark("sketch of C", c->st);
   cholqr2(c, q, q.sk, 0, beta_d, 0, c->st);
   SYLV_DISPATCH_R(R, { k_init_tau<R_><<<1, 1, 0, c->st>>>(beta_d, ell_d, q.Tdev, ldT, q.Rall + R * R); });
   count(c);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(q.beta, beta_d, R * R * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CK(cudaMemcpyAsync(q.ell, ell_d, R * R * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpy2DAsync(q.Th, ldT * sizeof(double), q.Tdev, ldT * sizeof(double), R * sizeof(double),
-                       R, cudaMemcpyDeviceToHost, c->st));
   CK(cudaMemcpyAsync(q.flags_h, q.flags, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  tr.mark("CholQR2, T_1, mirrors", c->st);
   if (q.flags_h[0]) throw Status{SYLV_E_INVALID, "C1 or C2 (or its sketch) is rank deficient"};
 }
 
@@ -779,10 +816,14 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_
   count(c);
   CK(cudaGetLastError());
   if (timing) { CK(cudaEventRecord(t3.b, st)); c->timed.push_back(t3); }
-  // ---- mirror: T columns m..m+R (rows 0..m+R)
-  CK(cudaMemcpy2DAsync(q.Th + (int64_t)m * q.ldT, q.ldT * sizeof(double), q.Tdev + (int64_t)m * q.ldT,
-                       q.ldT * sizeof(double), (size_t)(m + R) * sizeof(double), R,
-                       cudaMemcpyDeviceToHost, st));
+}
+
+// Host copy of the leading rows x rows block of T (upper triangular, column-major, ldT).
+// Called only after the streams have been joined (residual, solution, get_small).
+void sync_T(sylv_ctx* c, Sequence& q, int rows) {
+  CK(cudaMemcpy2DAsync(q.Th, q.ldT * sizeof(double), q.Tdev, q.ldT * sizeof(double), (size_t)rows * sizeof(double),
+                       rows, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
 }
 
 sylv_status fail(sylv_ctx* c, sylv_status s, const std::string& m) {
@@ -928,7 +969,7 @@ void sylv_sketch_destroy(sylv_ctx* ctx) {
   for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4})
     if (s) cudaStreamSynchronize(s);
   for (auto& q : ctx->seq) free_seq(q);
-  if (ctx->red) cudaFree(ctx->red);
+  dfree(ctx->red);
   delete ctx->gsolve;
   for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4})
     if (s) cudaStreamDestroy(s);
@@ -999,7 +1040,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
       c->comm = comm;
       c->row_begin = rb;
       c->row_end = re;
-      CK(cudaMalloc(&c->red, (size_t)2 * (cfg->k + 1) * r * r * sizeof(double)));
+      c->red = dalloc<double>((size_t)2 * (cfg->k + 1) * r * r);
     } else if (!(cfg->row_begin == 0 && (cfg->row_end == 0 || cfg->row_end == A->n))) {
       throw Status{SYLV_E_INVALID, "a row range needs a communicator"};
     }
@@ -1115,6 +1156,8 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
     Sequence& U = c->seq[0];
     Sequence& V = c->seq[1];
     double hhat[kMaxR * kMaxR], ghat[kMaxR * kMaxR], Bm[kMaxR * kMaxR];
+    sync_T(c, U, m + r);
+    sync_T(c, V, m + r);
     hat_coefficient(d, r, c->K, U.Th, U.ldT, U.Hh, hhat);
     hat_coefficient(d, r, c->K, V.Th, V.ldT, V.Hh, ghat);
     double bn = 0.0;
@@ -1291,13 +1334,13 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
           CK(cudaGetLastError());
         }
         CK(cudaStreamSynchronize(c->st));
-        cudaFree(Md);
-        cudaFree(rbuf);
+        dfree(Md);
+        dfree(rbuf);
       }
       if (!dev_out) {
         CK(cudaMemcpyAsync(Xout[qi], Xd, (size_t)c->n * ldx * sizeof(double), cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
-        cudaFree(Xd);
+        dfree(Xd);
       }
     }
     CK(cudaStreamSynchronize(c->st));
@@ -1398,16 +1441,16 @@ sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->st));
     if (q.skpart != saved) {
-      cudaFree(q.skpart);
+      dfree(q.skpart);
       q.skpart = saved;
     }
-    cudaFree(Xtmp);
-    cudaFree(Xs);
+    dfree(Xtmp);
+    dfree(Xs);
     if (!yout) {
       CK(cudaMemcpyAsync(Yout, Yd, (size_t)c->s * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     }
     CK(cudaStreamSynchronize(c->st));
-    if (!yout) cudaFree(Yd);
+    if (!yout) dfree(Yd);
     return SYLV_OK;
   });
 }
@@ -1430,6 +1473,11 @@ sylv_status sylv_sketch_get_small(sylv_ctx* c, int32_t which, int32_t d, double*
     }
   }
   if (T) {
+    sylv_status st = guard(c, [&]() -> sylv_status {
+      sync_T(c, const_cast<Sequence&>(q), m + r);
+      return SYLV_OK;
+    });
+    if (st != SYLV_OK) return st;
     for (int a = 0; a < m + r; ++a)
       for (int b = 0; b < m + r; ++b) T[(size_t)a * (m + r) + b] = q.Th[(int64_t)b * q.ldT + a];
   }
@@ -1451,7 +1499,7 @@ sylv_status sylv_sketch_get_block(sylv_ctx* c, int32_t which, int32_t j, double*
     CK(cudaGetLastError());
     if (!dev) CK(cudaMemcpyAsync(out, od, (size_t)c->n * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    if (!dev) cudaFree(od);
+    if (!dev) dfree(od);
     return SYLV_OK;
   });
 }
