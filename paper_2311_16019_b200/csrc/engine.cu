@@ -192,6 +192,8 @@ struct sylv_comm {
 struct sylv_ctx {
   std::string err;
   cudaStream_t st = nullptr;
+  cudaStream_t rst = nullptr;       // stream of the residual computation (= st, or st_solve)
+  cudaStream_t st_solve = nullptr;  // solve driver: projected solves overlapping the next steps
   Comm* comm = nullptr;         // non-null: row-sharded context; not owned
   int64_t n_global = 0, row_begin = 0, row_end = 0;
   double* red = nullptr;        // multi-rank: reduced partials (k r^2 + r^2 per sequence)
@@ -820,10 +822,12 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_
 
 // Host copy of the leading rows x rows block of T (upper triangular, column-major, ldT).
 // Called only after the streams have been joined (residual, solution, get_small).
+// Uses the residual stream (c->rst: the context stream, or the solve driver's own stream
+// while the next steps run on the context streams; the block read is final either way).
 void sync_T(sylv_ctx* c, Sequence& q, int rows) {
   CK(cudaMemcpy2DAsync(q.Th, q.ldT * sizeof(double), q.Tdev, q.ldT * sizeof(double), (size_t)rows * sizeof(double),
-                       rows, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+                       rows, cudaMemcpyDeviceToHost, c->rst));
+  CK(cudaStreamSynchronize(c->rst));
 }
 
 sylv_status fail(sylv_ctx* c, sylv_status s, const std::string& m) {
@@ -850,6 +854,64 @@ sylv_status guard(sylv_ctx* c, F&& f) {
       return fail(c, SYLV_E_NCCL, e.what);
     }
   }
+}
+
+// Projected solve of check d on the device (sign iteration) or on the host (Bartels-Stewart)
+bool device_solve(const sylv_ctx* c, int d) {
+  return (c->cflags & 8) || (!(c->cflags & 16) && d * c->R >= 512);
+}
+
+// Enqueue block steps first..last (Alg. 1 lines 3-9 for both sequences) and the flag
+// copies; no synchronisation (sylv_sketch_step = enqueue + finish; the solve driver
+// enqueues the steps to the next check before solving the current one).
+void enqueue_steps(sylv_ctx* c, int first, int last) {
+  // U passes on the context stream, V passes on st2 (independent sequences); each
+  // sequence's sketch-space work on its own side stream.  Serial mode: all on st.
+  const bool serial = (c->cflags & 2) != 0;
+  cudaStream_t others[3] = {c->st2, c->st3, c->st4};
+  if (!serial) {
+    CK(cudaEventRecord(c->fork, c->st));
+    for (cudaStream_t s : others) CK(cudaStreamWaitEvent(s, c->fork, 0));
+  }
+  for (int j = first; j <= last; ++j) {
+    step_sequence(c, c->seq[0], j, c->st, serial ? c->st : c->st3);
+    step_sequence(c, c->seq[1], j, serial ? c->st : c->st2, serial ? c->st : c->st4);
+  }
+  if (!serial) {
+    for (int i = 0; i < 3; ++i) {
+      CK(cudaEventRecord(c->join[i], others[i]));
+      CK(cudaStreamWaitEvent(c->st, c->join[i], 0));
+    }
+  }
+  CK(cudaMemcpyAsync(c->seq[1].flags_h + first, c->seq[1].flags + first, (last - first + 2) * sizeof(int),
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->seq[0].flags_h + first, c->seq[0].flags + first, (last - first + 2) * sizeof(int),
+                     cudaMemcpyDeviceToHost, c->st));
+}
+
+// Wait for enqueued steps first..last, check breakdown / lost-independence flags, advance d_done.
+sylv_status finish_steps(sylv_ctx* c, int first, int last) {
+  CK(cudaStreamSynchronize(c->st));
+  ev_collect(c);
+  for (int j = first; j <= last; ++j) {
+    const int f = c->seq[0].flags_h[j] | c->seq[1].flags_h[j];
+    if (f & 1 || f & 2) {
+      c->d_done = j;
+      c->stats.steps += j - first + 1;
+      c->broken = true;
+      c->breakdown_d = j;
+      return fail(c, SYLV_E_BREAKDOWN, "breakdown at step " + std::to_string(j));
+    }
+    const int g = c->seq[0].flags_h[j + 1] | c->seq[1].flags_h[j + 1];
+    if (g & 4) {
+      c->d_done = j;
+      c->stats.steps += j - first + 1;
+      return fail(c, SYLV_E_LOST_INDEP, "sketched basis lost independence at step " + std::to_string(j));
+    }
+  }
+  c->stats.steps += last - first + 1;
+  c->d_done = last;
+  return SYLV_OK;
 }
 
 }  // namespace
@@ -966,12 +1028,12 @@ void sylv_comm_destroy(sylv_comm* comm) {
 void sylv_sketch_destroy(sylv_ctx* ctx) {
   if (!ctx) return;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
-  for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4})
+  for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4, ctx->st_solve})
     if (s) cudaStreamSynchronize(s);
   for (auto& q : ctx->seq) free_seq(q);
   dfree(ctx->red);
   delete ctx->gsolve;
-  for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4})
+  for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4, ctx->st_solve})
     if (s) cudaStreamDestroy(s);
   if (ctx->fork) cudaEventDestroy(ctx->fork);
   for (cudaEvent_t e : ctx->join)
@@ -1014,6 +1076,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
   }
   return guard(c, [&]() -> sylv_status {
     c->st = (cudaStream_t)stream;
+    c->rst = c->st;
     c->R = r;
     c->K = cfg->k;
     c->dmax = cfg->d_max;
@@ -1078,6 +1141,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->st_solve, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
     for (cudaEvent_t& e : c->join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     init_sequence(c, c->seq[0], 0, A, false, C1, cfg->seed_u);
@@ -1094,50 +1158,10 @@ sylv_status sylv_sketch_step(sylv_ctx* c, int32_t nsteps, int32_t* d_done) {
     const int first = c->d_done + 1;
     const int last = std::min(c->dmax, c->d_done + std::max(0, nsteps));
     if (last >= first) {
-      // U passes on the context stream, V passes on st2 (independent sequences); each
-      // sequence's sketch-space work on its own side stream.  Serial mode: all on st.
-      const bool serial = (c->cflags & 2) != 0;
-      cudaStream_t others[3] = {c->st2, c->st3, c->st4};
-      if (!serial) {
-        CK(cudaEventRecord(c->fork, c->st));
-        for (cudaStream_t s : others) CK(cudaStreamWaitEvent(s, c->fork, 0));
-      }
-      for (int j = first; j <= last; ++j) {
-        step_sequence(c, c->seq[0], j, c->st, serial ? c->st : c->st3);
-        step_sequence(c, c->seq[1], j, serial ? c->st : c->st2, serial ? c->st : c->st4);
-      }
-      if (!serial) {
-        for (int i = 0; i < 3; ++i) {
-          CK(cudaEventRecord(c->join[i], others[i]));
-          CK(cudaStreamWaitEvent(c->st, c->join[i], 0));
-        }
-      }
-      CK(cudaMemcpyAsync(c->seq[1].flags_h + first, c->seq[1].flags + first, (last - first + 2) * sizeof(int),
-                         cudaMemcpyDeviceToHost, c->st));
-      CK(cudaMemcpyAsync(c->seq[0].flags_h + first, c->seq[0].flags + first, (last - first + 2) * sizeof(int),
-                         cudaMemcpyDeviceToHost, c->st));
-      CK(cudaStreamSynchronize(c->st));
-      ev_collect(c);
-      for (int j = first; j <= last; ++j) {
-        const int f = c->seq[0].flags_h[j] | c->seq[1].flags_h[j];
-        if (f & 1 || f & 2) {
-          c->d_done = j;
-          c->stats.steps += j - first + 1;
-          c->broken = true;
-          c->breakdown_d = j;
-          if (d_done) *d_done = j;
-          return fail(c, SYLV_E_BREAKDOWN, "breakdown at step " + std::to_string(j));
-        }
-        const int g = c->seq[0].flags_h[j + 1] | c->seq[1].flags_h[j + 1];
-        if (g & 4) {
-          c->d_done = j;
-          c->stats.steps += j - first + 1;
-          if (d_done) *d_done = j;
-          return fail(c, SYLV_E_LOST_INDEP, "sketched basis lost independence at step " + std::to_string(j));
-        }
-      }
-      c->stats.steps += last - first + 1;
-      c->d_done = last;
+      enqueue_steps(c, first, last);
+      const sylv_status st = finish_steps(c, first, last);
+      if (d_done) *d_done = c->d_done;
+      if (st != SYLV_OK) return st;
     }
     if (d_done) *d_done = c->d_done;
     if (nsteps > 0 && std::max(0, last - first + 1) < nsteps)
@@ -1173,7 +1197,7 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
     // (lcol[p * m + row] = Y[row, m-r+p]) are all the residual needs
     std::vector<double> lrow((size_t)m * r), lcol((size_t)m * r);
     bool done = false;
-    const bool want_gpu = (c->cflags & 8) || (!(c->cflags & 16) && m >= 512);
+    const bool want_gpu = device_solve(c, d);
     if (want_gpu) {
       // f1: device sign-function solve; falls back to the host on non-convergence
       try {
@@ -1182,12 +1206,12 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
           c->gsolve->mcap = (c->dmax + 1) * r;
         }
         GpuSylv& gs = *c->gsolve;
-        if (gs.solve(U.Tdev, U.Hc, V.Tdev, V.Hc, U.ldT, d, r, c->K, Bm, c->st)) {
+        if (gs.solve(U.Tdev, U.Hc, V.Tdev, V.Hc, U.ldT, d, r, c->K, Bm, c->rst)) {
           CK(cudaMemcpy2DAsync(lrow.data(), (size_t)r * sizeof(double), gs.C + (m - r), (size_t)m * sizeof(double),
-                               (size_t)r * sizeof(double), m, cudaMemcpyDeviceToHost, c->st));
+                               (size_t)r * sizeof(double), m, cudaMemcpyDeviceToHost, c->rst));
           CK(cudaMemcpyAsync(lcol.data(), gs.C + (size_t)(m - r) * m, (size_t)m * r * sizeof(double),
-                             cudaMemcpyDeviceToHost, c->st));
-          CK(cudaStreamSynchronize(c->st));
+                             cudaMemcpyDeviceToHost, c->rst));
+          CK(cudaStreamSynchronize(c->rst));
           done = true;
           c->y_dev = true;
           c->stats.gpu_solves++;
@@ -1363,30 +1387,74 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
   }
   if (sched.empty() || sched.back() != c->dmax) sched.push_back(c->dmax);
   int d_fail = 0, d_pass = -1, skips = 0;
+  bool pass_by_breakdown = false;   // breakdown seen when the pass was decided (no bisection)
   double rr_pass = NAN, last_rr = NAN;
-  for (int dc : sched) {
+  // Before a check that is solved on the HOST, the steps up to the next scheduled check are
+  // enqueued first: T and H of the checked d are final, the enqueued steps only append later
+  // columns, so the CPU solve hides behind the GPU stepping (a passing check leaves at most
+  // one batch of unneeded steps).  Device solves are not overlapped: measured on c3, their
+  // GEMM/LU kernels and the pass kernels serialise on the SMs and the prefetched steps only
+  // add work.
+  int pend_first = 0, pend_last = -1;
+  auto finish_pending = [&]() -> sylv_status {
+    if (pend_last < pend_first) return SYLV_OK;
+    const int f = pend_first, l = pend_last;
+    pend_first = 0;
+    pend_last = -1;
+    return guard(c, [&]() -> sylv_status { return finish_steps(c, f, l); });
+  };
+  auto ok_step = [](sylv_status s) { return s == SYLV_OK || s == SYLV_E_BREAKDOWN || s == SYLV_E_NOT_CONVERGED; };
+  for (size_t idx = 0; idx < sched.size(); ++idx) {
+    const int dc = sched[idx];
     if (dc > c->dmax) break;
     if (c->d_done < dc && !c->broken) {
-      int dd = 0;
-      sylv_status s = sylv_sketch_step(c, dc - c->d_done, &dd);
-      if (s != SYLV_OK && s != SYLV_E_BREAKDOWN && s != SYLV_E_NOT_CONVERGED) return s;
+      sylv_status s = finish_pending();
+      if (!ok_step(s)) return s;
+      if (c->d_done < dc && !c->broken) {
+        int dd = 0;
+        s = sylv_sketch_step(c, dc - c->d_done, &dd);
+        if (!ok_step(s)) return s;
+      }
+    }
+    if (!c->broken && idx + 1 < sched.size() && !device_solve(c, std::min(dc, c->d_done))) {
+      const int nx = std::min(sched[idx + 1], c->dmax);
+      if (nx > c->d_done) {
+        const int f = c->d_done + 1;
+        const sylv_status s = guard(c, [&]() -> sylv_status {
+          enqueue_steps(c, f, nx);
+          return SYLV_OK;
+        });
+        if (s != SYLV_OK) return s;
+        pend_first = f;
+        pend_last = nx;
+      }
     }
     const int dchk = std::min(dc, c->d_done);
     double rho, rr;
+    c->rst = c->st_solve;
     sylv_status s = sylv_sketch_residual(c, dchk, &rho, &rr);
+    c->rst = c->st;
     if (s == SYLV_E_SINGULAR) {
       if (++skips >= 5) break;
       continue;
     }
-    if (s != SYLV_OK) return s;
+    if (s != SYLV_OK) {
+      finish_pending();
+      return s;
+    }
     skips = 0;
     last_rr = rr;
     if (rr < c->tol || c->broken) {
       d_pass = dchk;
       rr_pass = rr;
+      pass_by_breakdown = c->broken;
       break;
     }
     d_fail = dchk;
+  }
+  {
+    const sylv_status s = finish_pending();   // the last prefetched batch
+    if (!ok_step(s) && s != SYLV_E_LOST_INDEP) return s;
   }
   if (d_pass < 0) {
     if (d_star) *d_star = c->d_done;
@@ -1394,7 +1462,7 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     return fail(c, SYLV_E_NOT_CONVERGED, "tolerance not reached by d_max");
   }
   int lo = d_fail, hi = d_pass;
-  while (hi - lo > 1 && !c->broken) {
+  while (hi - lo > 1 && !pass_by_breakdown) {
     const int mid = (lo + hi) / 2;
     double rho, rr;
     sylv_status s = sylv_sketch_residual(c, mid, &rho, &rr);

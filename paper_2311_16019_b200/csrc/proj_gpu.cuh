@@ -22,7 +22,10 @@
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -80,6 +83,13 @@ __global__ void k_logdet(const double* __restrict__ LU, int m, double* __restric
 struct GpuSylv {
   cublasHandle_t hb = nullptr;
   cusolverDnHandle_t hs = nullptr;
+  // second lane: the B inversion of a Newton step runs concurrently with the A one
+  // (cuSOLVER getrf is latency-bound at these sizes)
+  cusolverDnHandle_t hs2 = nullptr;
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  double *LU2 = nullptr, *work2 = nullptr;
+  int *ipiv2 = nullptr, *info2 = nullptr;
   int cap = 0, capr = 0, lwork = 0;
   int mcap = 1 << 30;            // largest m ever needed ((d_max + 1) r)
   cudaStream_t cur = nullptr;    // stream of the current solve
@@ -87,20 +97,32 @@ struct GpuSylv {
   double *Hb = nullptr, *work = nullptr, *dlog = nullptr;
   int *ipiv = nullptr, *info = nullptr;
   int iterations = 0;
+  int newton_steps = 0, ns_steps = 0;
+  double t_build = 0, t_newton = 0, t_ns = 0;   // seconds (SYLV_TRACE_PROJ)
 
   ~GpuSylv() { release(); }
-  void release() {
-    for (double* p : {A, B, C, Ai, Bi, W, LU, Hb, work, dlog})
+  void free_bufs() {
+    for (double* p : {A, B, C, Ai, Bi, W, LU, Hb, work, dlog, LU2, work2})
       if (p) cudaFree(p);
-    if (ipiv) cudaFree(ipiv);
-    if (info) cudaFree(info);
-    A = B = C = Ai = Bi = W = LU = Hb = work = dlog = nullptr;
-    ipiv = info = nullptr;
+    for (int* p : {ipiv, info, ipiv2, info2})
+      if (p) cudaFree(p);
+    A = B = C = Ai = Bi = W = LU = Hb = work = dlog = LU2 = work2 = nullptr;
+    ipiv = info = ipiv2 = info2 = nullptr;
+  }
+  void release() {
+    if (st2) cudaStreamSynchronize(st2);
+    free_bufs();
     cap = 0;
     if (hb) cublasDestroy(hb);
     if (hs) cusolverDnDestroy(hs);
+    if (hs2) cusolverDnDestroy(hs2);
+    if (st2) cudaStreamDestroy(st2);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     hb = nullptr;
-    hs = nullptr;
+    hs = hs2 = nullptr;
+    st2 = nullptr;
+    ev_fork = ev_join = nullptr;
   }
   static void ck(cudaError_t e, const char* w) {
     if (e != cudaSuccess) throw ProjError{std::string(w) + ": " + cudaGetErrorString(e)};
@@ -117,23 +139,27 @@ struct GpuSylv {
     if (!hb) {
       ckb(cublasCreate(&hb), "cublasCreate");
       cks(cusolverDnCreate(&hs), "cusolverDnCreate");
+      cks(cusolverDnCreate(&hs2), "cusolverDnCreate");
+      ck(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "cudaEventCreate");
+      cks(cusolverDnSetStream(hs2, st2), "cusolverDnSetStream");
     }
     ckb(cublasSetStream(hb, st), "cublasSetStream");
     cks(cusolverDnSetStream(hs, st), "cusolverDnSetStream");
     if (m <= cap && r <= capr) return;
     if (m > cap) m = std::max(m, std::min(mcap, cap + cap / 2));   // grow geometrically (<= mcap)
-    for (double* p : {A, B, C, Ai, Bi, W, LU, Hb, work, dlog})
-      if (p) cudaFree(p);
-    if (ipiv) cudaFree(ipiv);
-    if (info) cudaFree(info);
+    ck(cudaStreamSynchronize(st), "sync");
+    free_bufs();
     const size_t mm = (size_t)m * m;
-    for (double** p : {&A, &B, &C, &Ai, &Bi, &W, &LU}) ck(cudaMalloc(p, mm * sizeof(double)), "cudaMalloc (proj)");
+    for (double** p : {&A, &B, &C, &Ai, &Bi, &W, &LU, &LU2}) ck(cudaMalloc(p, mm * sizeof(double)), "cudaMalloc (proj)");
     ck(cudaMalloc(&Hb, (size_t)(m + r) * m * sizeof(double)), "cudaMalloc (proj)");
     ck(cudaMalloc(&dlog, 2 * sizeof(double)), "cudaMalloc (proj)");
-    ck(cudaMalloc(&ipiv, (size_t)m * sizeof(int)), "cudaMalloc (proj)");
-    ck(cudaMalloc(&info, sizeof(int)), "cudaMalloc (proj)");
+    for (int** p : {&ipiv, &ipiv2}) ck(cudaMalloc(p, (size_t)m * sizeof(int)), "cudaMalloc (proj)");
+    for (int** p : {&info, &info2}) ck(cudaMalloc(p, sizeof(int)), "cudaMalloc (proj)");
     cks(cusolverDnDgetrf_bufferSize(hs, m, m, LU, m, &lwork), "getrf_bufferSize");
     ck(cudaMalloc(&work, (size_t)std::max(lwork, 1) * sizeof(double)), "cudaMalloc (proj)");
+    ck(cudaMalloc(&work2, (size_t)std::max(lwork, 1) * sizeof(double)), "cudaMalloc (proj)");
     cap = m;
     capr = r;
   }
@@ -153,19 +179,37 @@ struct GpuSylv {
   }
 
   // X (m x m, in/out of `src`) -> Xinv; returns log|det X|
-  double invert(const double* src, double* dst, int m, cudaStream_t st) {
-    ck(cudaMemcpyAsync(LU, src, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy (LU)");
-    cks(cusolverDnDgetrf(hs, m, m, LU, m, work, ipiv, info), "getrf");
-    k_logdet<<<1, 256, 0, st>>>(LU, m, dlog);
-    k_eye<<<(int)std::min<int64_t>(4096, ((int64_t)m * m + 255) / 256), 256, 0, st>>>(dst, m);
-    cks(cusolverDnDgetrs(hs, CUBLAS_OP_N, m, m, LU, m, ipiv, dst, m, info), "getrs");
-    double ld = 0.0;
-    int inf = 0;
-    ck(cudaMemcpyAsync(&ld, dlog, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaMemcpyAsync(&inf, info, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+  // Enqueue X -> X^{-1} (LU) on lane 0 (st, hs) or lane 1 (st2, hs2); log|det X| -> dlog[lane]
+  void invert_async(const double* src, double* dst, int m, int lane, cudaStream_t st) {
+    cudaStream_t s = lane ? st2 : st;
+    cusolverDnHandle_t h = lane ? hs2 : hs;
+    double* lu = lane ? LU2 : LU;
+    ck(cudaMemcpyAsync(lu, src, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy (LU)");
+    cks(cusolverDnDgetrf(h, m, m, lu, m, lane ? work2 : work, lane ? ipiv2 : ipiv, lane ? info2 : info), "getrf");
+    k_logdet<<<1, 256, 0, s>>>(lu, m, dlog + lane);
+    k_eye<<<(int)std::min<int64_t>(4096, ((int64_t)m * m + 255) / 256), 256, 0, s>>>(dst, m);
+    cks(cusolverDnDgetrs(h, CUBLAS_OP_N, m, m, lu, m, lane ? ipiv2 : ipiv, dst, m, lane ? info2 : info), "getrs");
+  }
+
+  // A^{-1} and B^{-1} concurrently; returns log|det A|, log|det B|
+  void invert_pair(const double* Am, double* Ainv, const double* Bm, double* Binv, int m, cudaStream_t st,
+                   double* la, double* lb) {
+    ck(cudaEventRecord(ev_fork, st), "event");
+    ck(cudaStreamWaitEvent(st2, ev_fork, 0), "event");
+    invert_async(Am, Ainv, m, 0, st);
+    invert_async(Bm, Binv, m, 1, st);
+    ck(cudaEventRecord(ev_join, st2), "event");
+    ck(cudaStreamWaitEvent(st, ev_join, 0), "event");
+    double ld[2] = {0.0, 0.0};
+    int inf[2] = {0, 0};
+    ck(cudaMemcpyAsync(ld, dlog, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaMemcpyAsync(&inf[0], info, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaMemcpyAsync(&inf[1], info2, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "sync");
-    if (inf != 0 || !std::isfinite(ld)) throw ProjError{"singular projected matrix"};
-    return ld;
+    if (inf[0] != 0 || inf[1] != 0 || !std::isfinite(ld[0]) || !std::isfinite(ld[1]))
+      throw ProjError{"singular projected matrix"};
+    *la = ld[0];
+    *lb = ld[1];
   }
 
   // the sign iteration must end at A = B = I (sign of matrices with spectra in Re > 0)
@@ -199,6 +243,13 @@ struct GpuSylv {
 
   bool solve_once(const double* TU, const double* HcU, const double* TV, const double* HcV, int64_t ldT, int d, int r,
                   int K, const double* Bm, cudaStream_t st, bool allow_ns) {
+    const bool trace = std::getenv("SYLV_TRACE_PROJ") != nullptr;
+    auto now = [&]() {
+      if (trace) cudaStreamSynchronize(st);
+      return std::chrono::steady_clock::now();
+    };
+    auto t0 = now();
+    newton_steps = ns_steps = 0;
     const int m = d * r;
     ensure(m, r, st);
     build_M(TU, ldT, HcU, d, r, K, A, st);
@@ -213,14 +264,19 @@ struct GpuSylv {
                          (size_t)r * sizeof(double), r, cudaMemcpyHostToDevice, st),
        "H2D (rhs)");
     const int64_t mm = (int64_t)m * m;
+    auto t1 = now();
+    t_build = std::chrono::duration<double>(t1 - t0).count();
+    t_newton = t_ns = 0.0;
     const double mone = -1.0, half = 0.5, c15 = 1.5, cm05 = -0.5;
     bool scale = true, last = false, ns = false;
     for (iterations = 1; iterations <= 60; ++iterations) {
       double dA, nA, dB, nB;
+      auto ti = now();
+      if (!ns) ++newton_steps; else ++ns_steps;
       if (!ns) {
         // scaled Newton step (needs A^{-1}, B^{-1}: LU)
-        const double la = invert(A, Ai, m, st);
-        const double lb = invert(B, Bi, m, st);
+        double la = 0.0, lb = 0.0;
+        invert_pair(A, Ai, B, Bi, m, st, &la, &lb);
         const double mu = scale ? std::exp(-(la + lb) / (2.0 * m)) : 1.0;
         const double a1 = 0.5 / mu, b1 = 0.5 * mu;
         // C <- (mu C + Ai C Bi / mu) / 2
@@ -262,11 +318,18 @@ struct GpuSylv {
         std::swap(B, W);
       }
       const double rel = std::max(dA / nA, dB / nB);
+      {
+        const double dt = std::chrono::duration<double>(now() - ti).count();
+        if (ns_steps && newton_steps + ns_steps > 0 && ns) t_ns += dt; else t_newton += dt;
+      }
       if (!std::isfinite(rel)) return false;
       if (rel < 1e-2) scale = false;                      // quadratic phase: unscaled
       if (last || rel < 1e-14) {                          // one step after rel < 1e-7: error ~ rel^2
         if (!near_identity(A, m, st) || !near_identity(B, m, st)) return false;   // wrong fixed point
         ckb(cublasDscal(hb, (int)mm, &half, C, 1), "dscal (Y = C/2)");
+        if (trace)
+          std::fprintf(stderr, "[proj] m=%d build %.1f ms, %d Newton %.1f ms, %d NS %.1f ms\n", m, 1e3 * t_build,
+                       newton_steps, 1e3 * t_newton, ns_steps, 1e3 * t_ns);
         return true;
       }
       if (rel < 1e-7) last = true;
