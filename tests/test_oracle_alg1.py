@@ -212,3 +212,35 @@ def test_c0_regression_expectation():
     A, _, B = operators.operator_pair(cfg)
     _, rel = alg1.true_residual(A, B, o.C1, o.C2, X1, X2)
     assert rel < 5e-6
+
+
+@pytest.mark.parametrize("k", [2, 20])
+def test_sketched_residual_within_embedding_bound(k):
+    """Paper P:185-188: if S_U, S_V are eps-subspace embeddings of the Krylov
+    spaces that contain the residual's column and row spaces (R = A X + X B - C1 C2^T has
+    columns in span(U_{d+1}) and rows in span(V_{d+1})), the sketched residual norm lies in
+    [(1 - eps_U)(1 - eps_V), (1 + eps_U)(1 + eps_V)] ||R||_F.  eps is measured directly from
+    the singular values of S Q (Q an orthonormal basis of the retained blocks), the true R
+    from the dense reconstruction of the oracle's X (rank_tol = 0: no truncation), so this
+    pins rho, the solution and the basis together against an independent bound."""
+    d = 10
+    cfg, A, Bt, B, C1, C2 = _small(N=10, r=1, k=k, d_max=d + 2, s=400)
+    obj = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2, keep_basis=True)
+    obj.step(d)
+    res = obj.residual(d)
+    X1, X2 = obj.solution(d, res.Y, rank_tol=0.0)
+    R = A @ (X1 @ X2.T) + (X1 @ X2.T) @ B.toarray() - C1 @ C2.T
+    nR = np.linalg.norm(R)
+    S_U = sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed_u).toarray()
+    S_V = sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed_v).toarray()
+    # the residual lives in span(U_{d+1}) (x) span(V_{d+1}) (exactly, up to rounding)
+    QU = np.linalg.qr(np.concatenate([obj.U.U[i] for i in range(1, d + 2)], axis=1))[0]
+    QV = np.linalg.qr(np.concatenate([obj.V.U[i] for i in range(1, d + 2)], axis=1))[0]
+    assert np.linalg.norm(R - QU @ (QU.T @ R) @ QV @ QV.T) <= 1e-8 * nR
+    sU = np.linalg.svd(S_U @ QU, compute_uv=False)
+    sV = np.linalg.svd(S_V @ QV, compute_uv=False)
+    eU = max(abs(sU.max() - 1), abs(1 - sU.min()))
+    eV = max(abs(sV.max() - 1), abs(1 - sV.min()))
+    assert eU < 1 and eV < 1
+    assert res.rho == pytest.approx(np.linalg.norm(S_U @ R @ S_V.T), rel=1e-9)
+    assert (1 - eU) * (1 - eV) * nR * (1 - 1e-9) <= res.rho <= (1 + eU) * (1 + eV) * nR * (1 + 1e-9)
