@@ -1,6 +1,7 @@
-# round measurement: all GPU tests, bench (c3), ncu launch list of the same command
+# round measurement: all GPU tests, bench (c3 + others), launch list, ncu full of the steady-state hot kernels
 set -x
 timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider -o faulthandler_timeout=600 > gpurun_out/gputest.log 2>&1; echo tests $?
-timeout 300 python tools/init_probe.py c3 > gpurun_out/init.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo bench $?
+for c in c2 c4 c1 c0; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-ttt > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-ttt > gpurun_out/ncu.log 2>&1; echo ncu $?
+timeout 300 python tools/quick_time.py c3 4 serial > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_st3d|k_sketch_cols" -s 20 -c 3 -o gpurun_out/prof_c3 python tools/quick_time.py c3 4 serial > gpurun_out/ncu2.log 2>&1; echo ncufull $?
