@@ -18,6 +18,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "../../include/sylv_sketch.h"
 #include "common.cuh"
@@ -25,6 +26,7 @@
 #include "nspace.cuh"
 #include "sspace.cuh"
 #include "stencil25d.cuh"
+#include "sketch_pull.cuh"
 #include "comm.cuh"
 #include "proj_gpu.cuh"
 
@@ -148,6 +150,11 @@ struct Sequence {
   double* Yt = nullptr;       // CSR: A Z_d (SoA)
   double* sk = nullptr;       // s x R (row-major)
   double* skpart = nullptr;   // nchunk x R x s sketch partials
+  // pull sketch (sketch_pull.cuh): groups sorted by (bucket, L2 chunk, window base)
+  uint32_t* pl_list = nullptr;   // zeta x ngroups local group indices
+  uint32_t* pl_off = nullptr;    // zeta x wpb + 1 per-warp segment offsets into pl_list
+  double* pl_strips = nullptr;   // zeta x wpb x R x kPullS per-warp strips
+  uint32_t pl_nch = 0, pl_wpb = 0, pl_bpw = 1;
   double* w = nullptr;        // s x R
   double* w2 = nullptr;       // s x R
   double* Q = nullptr;        // s x ldT (col-major)
@@ -173,8 +180,8 @@ struct Sequence {
   double* Th = nullptr;       // ldT x ldT col-major
   double* Rh = nullptr;       // (dmax+2) R^2 (filled on demand)
   int* flags_h = nullptr;
-  // per-step events (ring of K+2): coef2 of step j done (main -> side) and the sketch of
-  // step j done reading ring slot j+1 (side -> main, before pass 2 of step j+K+1 rewrites it)
+  // per-step events (ring of K+2): sketch of step j done (main -> side: the sketch-space QR
+  // reads w) and the QR of step j done with w (side -> main, before the next sketch writes it)
   std::vector<cudaEvent_t> ev_c2, ev_sk;
   double beta[kMaxR * kMaxR];
   double ell[kMaxR * kMaxR];
@@ -210,10 +217,12 @@ struct sylv_ctx {
   int nchunk = 1;     // row chunks of the sketch kernel (grid nchunk x R)
   int64_t gpc = 32;   // 32-row groups per sketch chunk
   size_t sk_smem = 0; // dynamic shared memory of the sketch kernel
+  bool sk_pull = false;  // large n: pull formulation of the sketch (sketch_pull.cuh)
   // streams: main[0] = st (U passes), main[1] = st2 (V passes); side[q] = sketch + sketch-space
   // QR of sequence q, which overlaps the next step's n-space passes (all = st in serial mode)
   cudaStream_t st2 = nullptr, st3 = nullptr, st4 = nullptr;
   cudaEvent_t fork = nullptr, join[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t phase[3] = {nullptr, nullptr, nullptr};   // pass/sketch phase barriers (enqueue_steps)
   Sequence seq[2];
   int d_done = 0;
   bool broken = false;
@@ -359,6 +368,9 @@ void free_seq(Sequence& q) {
                   q.part1, q.part2, q.part_s, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv};
   for (double* p : dp) dfree(p);
   dfree(q.flags);
+  dfree(q.pl_list);
+  dfree(q.pl_off);
+  dfree(q.pl_strips);
   dfree(q.rp);
   dfree(q.ci);
   if (q.Hh) cudaFreeHost(q.Hh);
@@ -594,13 +606,70 @@ void launch_pass2(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, con
 
 // S X for an SoA block -> w (s x R row-major) = (S X) M  (M = nullptr: identity)
 void launch_sketch(sylv_ctx* c, Sequence& q, const double* X, int R, const double* M, double* w, cudaStream_t st) {
+  const int red_grid = (int)std::min<int64_t>(4 * c->sm, (q.s + 255) / 256);
+  if (q.pl_list) {
+    const int nw = (int)(q.sp.zeta * q.pl_wpb);
+    SYLV_DISPATCH_R(R, {
+      k_sketch_pull<R_><<<(nw + kPullWarps - 1) / kPullWarps, kPullWarps * 32, 0, st>>>(
+          c->n, X, q.ld, q.sp, q.pl_list, q.pl_off, q.pl_wpb, q.pl_bpw, q.pl_strips);
+      k_sketch_pull_fold<R_><<<(int)std::min<int64_t>(4 * c->sm, (q.s * R + 255) / 256), 256, 0, st>>>(
+          q.pl_strips, q.sp, q.pl_wpb, q.pl_bpw, q.skpart);
+      k_sketch_reduce<R_><<<red_grid, 256, 0, st>>>(q.skpart, 1, q.s, M, w);
+    });
+    count(c, 3);
+    return;
+  }
   const dim3 g(c->nchunk, R);
   const int nchunk = c->nchunk;
   SYLV_DISPATCH_R(R, {
     k_sketch_cols<R_><<<g, kSkWarps * 32, c->sk_smem, st>>>(c->n, X, q.ld, q.sp, c->gpc, q.skpart);
-    k_sketch_reduce<R_><<<(int)std::min<int64_t>(4 * c->sm, (q.s + 255) / 256), 256, 0, st>>>(q.skpart, nchunk, q.s, M, w);
+    k_sketch_reduce<R_><<<red_grid, 256, 0, st>>>(q.skpart, nchunk, q.s, M, w);
   });
   count(c, 2);
+}
+
+// Pull-sketch lists (sketch_pull.cuh): the hash depends only on (seed, global group, bucket),
+// so the groups of each bucket are sorted once by (L2 chunk, window base) — stable, so every
+// later summation order is fixed.
+void build_pull_lists(sylv_ctx* c, Sequence& q, cudaStream_t st) {
+  const int64_t ngroups = (c->n + 31) / 32;
+  int64_t gpch = std::max<int64_t>(1, (int64_t)(32 << 20) / (256 * q.R));   // ~32 MB of W per chunk
+  if (const char* e = std::getenv("SYLV_PULL_CHUNK")) gpch = std::max<int64_t>(1, std::atoll(e));   // tests
+  const int64_t nch = (ngroups + gpch - 1) / gpch;
+  // bases per warp: as few as keep every warp resident at once (the warps sweep W's L2
+  // chunks together; a second wave would re-read W from HBM)
+  int occ = 1;
+  SYLV_DISPATCH_R(q.R, { CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sketch_pull<R_>, kPullWarps * 32, 0)); });
+  const int64_t resident = (int64_t)std::max(1, occ) * c->sm * kPullWarps;
+  int64_t bpw = std::max<int64_t>(1, std::min<int64_t>(kPullBpwMax, ((int64_t)q.sp.zeta * q.sp.b + resident - 1) / resident));
+  if (const char* e = std::getenv("SYLV_PULL_BPW")) bpw = std::max(1, std::min(kPullBpwMax, std::atoi(e)));
+  const int64_t wpb = (q.sp.b + bpw - 1) / bpw;
+  const int64_t nkeys = (int64_t)q.sp.zeta * wpb * nch * bpw;
+  const int64_t total = ngroups * q.sp.zeta;
+  if (nkeys >= (1ll << 32) || total >= (1ll << 31) || c->n >= (1ll << 32) - 64) return;   // stays on k_sketch_cols
+  q.pl_nch = (uint32_t)nch;
+  q.pl_bpw = (uint32_t)bpw;
+  q.pl_wpb = (uint32_t)wpb;
+  const int64_t nw = (int64_t)q.sp.zeta * wpb;
+  uint32_t *keys = dalloc<uint32_t>(total), *keys2 = dalloc<uint32_t>(total), *vals = dalloc<uint32_t>(total);
+  uint32_t* counts = dalloc<uint32_t>(nw + 1);
+  q.pl_list = dalloc<uint32_t>(total);
+  q.pl_off = dalloc<uint32_t>(nw + 1);
+  q.pl_strips = dalloc<double>((size_t)nw * q.R * kPullS);
+  CK(cudaMemsetAsync(counts, 0, (nw + 1) * sizeof(uint32_t), st));
+  k_pull_keys<<<4 * c->sm, 256, 0, st>>>(ngroups, q.sp, gpch, (uint32_t)nch, q.pl_bpw, q.pl_wpb, keys, vals, counts);
+  count(c);
+  int end_bit = 1;
+  while (end_bit < 32 && (1ll << end_bit) < nkeys) ++end_bit;
+  size_t sort_bytes = 0, scan_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, keys, keys2, vals, q.pl_list, (int)total, 0, end_bit, st));
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts, q.pl_off, (int)(nw + 1), st));
+  void* tmp = dalloc<char>(std::max(sort_bytes, scan_bytes));
+  CK(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, keys, keys2, vals, q.pl_list, (int)total, 0, end_bit, st));
+  CK(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, counts, q.pl_off, (int)(nw + 1), st));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  for (void* p : {(void*)keys, (void*)keys2, (void*)vals, (void*)counts, tmp}) dfree(p);
 }
 
 // SYLV_TRACE_INIT=1: wall time of the init phases on stderr (development aid)
@@ -646,6 +715,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   if (A->kind == SYLV_OP_CSR) q.Yt = dalloc<double>(blk);
   q.sk = dalloc<double>(sR);
   q.skpart = dalloc<double>((size_t)c->nchunk * sR);
+  if (c->sk_pull && q.sp.b >= 64) build_pull_lists(c, q, c->st);
   q.w = dalloc<double>(sR);
   q.w2 = dalloc<double>(sR);
   q.Q = dalloc<double>((size_t)c->s * ldT);
@@ -729,23 +799,24 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   if (q.flags_h[0]) throw Status{SYLV_E_INVALID, "C1 or C2 (or its sketch) is rank deficient"};
 }
 
-// One block step j (1-based) of one sequence: Alg. 1 lines 3-9.  The n-space passes and
-// the coefficient kernels (lines 3-8) run on `st`; the sketch and the sketch-space QR
-// update (line 9) on `side`, which overlaps the next step's passes.
-void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t side) {
+// One block step j (1-based) of one sequence: Alg. 1 lines 3-9, in two phases.
+// step_passes (lines 3-8): the n-space passes and the coefficient kernels on `st`.
+// step_sketch (line 9): the sketch of the new block on `st` (it reads the block just written
+// and the ring slot is rewritten only by a later pass on the same stream), then the sketch-space
+// QR update on `side`, which overlaps the next step's passes.
+void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
   const int R = c->R, K = c->K;
   const int nwin = std::min(K, j);
   Win win{};
   for (int i = 0; i < nwin; ++i) win.p[i] = q.slot(j - nwin + 1 + i);
   const bool timing = (c->cflags & 1) != 0;
   const int G = pass_parts(c, q);
-  TimedPair t1{}, t2{}, t3{};
+  TimedPair t1{}, t2{};
   // ---- a1 + a2 coefficients: pass 1
   if (timing) { t1 = ev_get(c, 0); CK(cudaEventRecord(t1.a, st)); }
   launch_pass1(c, q, win, nwin, j, st);
   if (timing) { CK(cudaEventRecord(t1.b, st)); c->timed.push_back(t1); }
   const int chan_main = q.which == 0 ? kChanUMain : kChanVMain;
-  const int chan_side = q.which == 0 ? kChanUSide : kChanVSide;
   double* red = c->red ? c->red + (int64_t)q.which * (K + 1) * R * R : nullptr;
   int np1 = G;
   const double* p1 = reduce_partials(c, q.part1, G, K * R * R, red, st, chan_main, &np1);
@@ -753,9 +824,7 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_
     k_coef1<R_, K_><<<1, kThreads, 0, st>>>(p1, np1, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
   });
   // ---- a2 update + a3 Gram: pass 2 (writes Z_{j+1} = W' into the ring slot that the
-  //      sketch of step j-K-1 read)
-  const int ne = K + 2;
-  if (j - K - 1 >= 1 && side != st) CK(cudaStreamWaitEvent(st, q.ev_sk[(j - K - 1) % ne], 0));
+  //      sketch of step j-K-1 read, earlier on this stream)
   if (timing) { t2 = ev_get(c, 1); CK(cudaEventRecord(t2.a, st)); }
   launch_pass2<true>(c, q, win, nwin, j, q.Yt, q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1), st);
   if (timing) { CK(cudaEventRecord(t2.b, st)); c->timed.push_back(t2); }
@@ -768,23 +837,30 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_
   if (c->comm) c->comm->halo(q.slot(j + 1), R, q.ld, q.gz, st, chan_main);
   count(c, 2);
   CK(cudaGetLastError());
-  // ---- H column j mirror (main stream), then hand over to the side stream
+  // ---- H column j mirror
   const size_t hb = (size_t)(K + 1) * R * R;
   CK(cudaMemcpyAsync(q.Hh + (size_t)j * hb, q.Hc + (size_t)j * hb, hb * sizeof(double),
                      cudaMemcpyDeviceToHost, st));
+}
+
+void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t side) {
+  const int R = c->R, K = c->K;
+  const bool timing = (c->cflags & 1) != 0;
+  const int ne = K + 2;
+  const int chan_main = q.which == 0 ? kChanUMain : kChanVMain;
+  TimedPair t3{}, t4{};
+  // ---- a4: w = (S W') R_{j+1}   (a5 timing includes the sketch)
+  if (side != st && j >= 2) CK(cudaStreamWaitEvent(st, q.ev_sk[(j - 1) % ne], 0));   // QR j-1 done with w
+  if (timing) { t3 = ev_get(c, 2); CK(cudaEventRecord(t3.a, st)); }
+  if (timing) { t4 = ev_get(c, 3); CK(cudaEventRecord(t4.a, st)); }
+  launch_sketch(c, q, q.slot(j + 1), R, q.Rall + (int64_t)(j + 1) * R * R, q.w, st);
+  if (c->comm) c->comm->allreduce(q.w, (size_t)q.s * R, st, chan_main);   // S linear in rows
+  if (timing) { CK(cudaEventRecord(t4.b, st)); c->timed.push_back(t4); }
   if (side != st) {
     CK(cudaEventRecord(q.ev_c2[j % ne], st));
     CK(cudaStreamWaitEvent(side, q.ev_c2[j % ne], 0));
   }
   st = side;
-  // ---- a4: w = (S W') R_{j+1}   (a5 timing includes the sketch)
-  if (timing) { t3 = ev_get(c, 2); CK(cudaEventRecord(t3.a, st)); }
-  TimedPair t4{};
-  if (timing) { t4 = ev_get(c, 3); CK(cudaEventRecord(t4.a, st)); }
-  launch_sketch(c, q, q.slot(j + 1), R, q.Rall + (int64_t)(j + 1) * R * R, q.w, st);
-  if (c->comm) c->comm->allreduce(q.w, (size_t)q.s * R, st, chan_side);   // S linear in rows
-  if (timing) { CK(cudaEventRecord(t4.b, st)); c->timed.push_back(t4); }
-  if (side != c->st && side != c->st2) CK(cudaEventRecord(q.ev_sk[j % ne], st));
   // ---- a5: block CGS2 against Q (m = j R columns); CholQR2; T column
   const int m = j * R;
   const dim3 gq((m + kWarps - 1) / kWarps, c->RT);
@@ -818,6 +894,7 @@ void step_sequence(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_
   count(c);
   CK(cudaGetLastError());
   if (timing) { CK(cudaEventRecord(t3.b, st)); c->timed.push_back(t3); }
+  if (st != c->st && st != c->st2) CK(cudaEventRecord(q.ev_sk[j % ne], st));
 }
 
 // Host copy of the leading rows x rows block of T (upper triangular, column-major, ldT).
@@ -873,9 +950,28 @@ void enqueue_steps(sylv_ctx* c, int first, int last) {
     CK(cudaEventRecord(c->fork, c->st));
     for (cudaStream_t s : others) CK(cudaStreamWaitEvent(s, c->fork, 0));
   }
+  // Phases per step: U and V passes concurrently (st, st2; each hides the other's small
+  // coefficient kernels), then the U sketch, then the V sketch — the L2-resident pull sketch
+  // (sketch_pull.cuh) must not share L2 with a streaming pass — then each sequence's
+  // sketch-space QR on its side stream, overlapping the next step's passes.
   for (int j = first; j <= last; ++j) {
-    step_sequence(c, c->seq[0], j, c->st, serial ? c->st : c->st3);
-    step_sequence(c, c->seq[1], j, serial ? c->st : c->st2, serial ? c->st : c->st4);
+    if (serial) {
+      step_passes(c, c->seq[0], j, c->st);
+      step_passes(c, c->seq[1], j, c->st);
+      step_sketch(c, c->seq[0], j, c->st, c->st);
+      step_sketch(c, c->seq[1], j, c->st, c->st);
+      continue;
+    }
+    step_passes(c, c->seq[0], j, c->st);
+    step_passes(c, c->seq[1], j, c->st2);
+    CK(cudaEventRecord(c->phase[0], c->st2));      // V passes done
+    CK(cudaStreamWaitEvent(c->st, c->phase[0], 0));
+    step_sketch(c, c->seq[0], j, c->st, c->st3);
+    CK(cudaEventRecord(c->phase[1], c->st));       // U sketch done
+    CK(cudaStreamWaitEvent(c->st2, c->phase[1], 0));
+    step_sketch(c, c->seq[1], j, c->st2, c->st4);
+    CK(cudaEventRecord(c->phase[2], c->st2));      // V sketch done
+    CK(cudaStreamWaitEvent(c->st, c->phase[2], 0));
   }
   if (!serial) {
     for (int i = 0; i < 3; ++i) {
@@ -1038,6 +1134,8 @@ void sylv_sketch_destroy(sylv_ctx* ctx) {
   if (ctx->fork) cudaEventDestroy(ctx->fork);
   for (cudaEvent_t e : ctx->join)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->phase)
+    if (e) cudaEventDestroy(e);
   for (auto& p : ctx->free_events) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto& p : ctx->timed) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   delete ctx;
@@ -1138,12 +1236,18 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     c->nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(ngroups, (int64_t)c->sm * per_sm / r));
     c->gpc = (ngroups + c->nchunk - 1) / c->nchunk;
     c->nchunk = (int)((ngroups + c->gpc - 1) / c->gpc);
+    {
+      // SYLV_SKETCH=cols|pull overrides the size rule (development / A-B timing)
+      const char* e = std::getenv("SYLV_SKETCH");
+      c->sk_pull = e ? std::strcmp(e, "pull") == 0 : ngroups >= kPullMinGroups;
+    }
     CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->st_solve, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
     for (cudaEvent_t& e : c->join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (cudaEvent_t& e : c->phase) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     init_sequence(c, c->seq[0], 0, A, false, C1, cfg->seed_u);
     init_sequence(c, c->seq[1], 1, B, true, C2, cfg->seed_v);
     return SYLV_OK;
@@ -1503,7 +1607,11 @@ sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X
     }
     // partials buffer is sized for nchunk x R x s; r <= R fits, larger r needs a temporary
     double* saved = q.skpart;
-    if (r > c->R) q.skpart = dalloc<double>((size_t)c->nchunk * c->s * r);
+    double* saved_strips = q.pl_strips;
+    if (r > c->R) {
+      q.skpart = dalloc<double>((size_t)c->nchunk * c->s * r);
+      if (q.pl_list) q.pl_strips = dalloc<double>((size_t)q.sp.zeta * q.pl_wpb * r * kPullS);
+    }
     launch_sketch(c, q, Xs + q.gz, r, nullptr, Yd, c->st);
     if (c->comm) c->comm->allreduce(Yd, (size_t)c->s * r, c->st, kChanSetup);
     CK(cudaGetLastError());
@@ -1511,6 +1619,10 @@ sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X
     if (q.skpart != saved) {
       dfree(q.skpart);
       q.skpart = saved;
+    }
+    if (q.pl_strips != saved_strips) {
+      dfree(q.pl_strips);
+      q.pl_strips = saved_strips;
     }
     dfree(Xtmp);
     dfree(Xs);

@@ -36,6 +36,9 @@ CASES = {
     "3d-r4k2-P4": (dict(kind="stencil3d", N=32, r=4, k=2, d_max=40), 4, True),
     "2d-r4k2-P3": (dict(kind="stencil2d", N=64, r=4, k=2, d_max=40), 3, True),
     "2d-r1k2-P2": (dict(kind="stencil2d", N=64, r=1, k=2, d_max=40), 2, True),
+    # pull sketch (sketch_pull.cuh) on shards: global group offsets m0 > 0 in the sorted lists
+    "3d-r8k3-tma-P3-pull": (dict(kind="stencil3d", N=34, r=8, k=3, d_max=40), 3, True, "pull"),
+    "2d-r4k2-P3-pull": (dict(kind="stencil2d", N=64, r=4, k=2, d_max=40), 3, True, "pull"),
 }
 NSTEPS = 16
 
@@ -96,8 +99,10 @@ def _sharded(cfg, C1, C2, P, tma, nsteps, solution_rank=0):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-def test_sharded_equals_unsharded(name):
-    kw, P, tma = CASES[name]
+def test_sharded_equals_unsharded(name, monkeypatch):
+    kw, P, tma = CASES[name][:3]
+    if len(CASES[name]) > 3:
+        monkeypatch.setenv("SYLV_SKETCH", CASES[name][3])
     cfg = inputs.small_config(**kw)
     C1, C2 = inputs.make_rhs(cfg)
     rho1, blocks1, sk1 = _unsharded(cfg, C1, C2, tma, NSTEPS)
