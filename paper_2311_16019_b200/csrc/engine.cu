@@ -636,14 +636,18 @@ void build_pull_lists(sylv_ctx* c, Sequence& q, cudaStream_t st) {
   int64_t gpch = std::max<int64_t>(1, (int64_t)(32 << 20) / (256 * q.R));   // ~32 MB of W per chunk
   if (const char* e = std::getenv("SYLV_PULL_CHUNK")) gpch = std::max<int64_t>(1, std::atoll(e));   // tests
   const int64_t nch = (ngroups + gpch - 1) / gpch;
-  // bases per warp: as few as keep every warp resident at once (the warps sweep W's L2
-  // chunks together; a second wave would re-read W from HBM)
+  // warps per bucket: exactly the resident warps of the GPU (the warps sweep W's L2 chunks
+  // together, a second wave would re-read W from HBM, and every SM gets the same load)
   int occ = 1;
   SYLV_DISPATCH_R(q.R, { CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sketch_pull<R_>, kPullWarps * 32, 0)); });
   const int64_t resident = (int64_t)std::max(1, occ) * c->sm * kPullWarps;
-  int64_t bpw = std::max<int64_t>(1, std::min<int64_t>(kPullBpwMax, ((int64_t)q.sp.zeta * q.sp.b + resident - 1) / resident));
-  if (const char* e = std::getenv("SYLV_PULL_BPW")) bpw = std::max(1, std::min(kPullBpwMax, std::atoi(e)));
-  const int64_t wpb = (q.sp.b + bpw - 1) / bpw;
+  const int64_t b = q.sp.b;
+  int64_t wpb = std::max<int64_t>((b + kPullBpwMax - 1) / kPullBpwMax, std::min<int64_t>(b, resident / q.sp.zeta));
+  if (const char* e = std::getenv("SYLV_PULL_BPW")) {   // tests: ranges of at most this many bases
+    const int64_t bw = std::max(1, std::min(kPullBpwMax, std::atoi(e)));
+    wpb = (b + bw - 1) / bw;
+  }
+  const int64_t bpw = (b + wpb - 1) / wpb;   // longest range
   const int64_t nkeys = (int64_t)q.sp.zeta * wpb * nch * bpw;
   const int64_t total = ngroups * q.sp.zeta;
   if (nkeys >= (1ll << 32) || total >= (1ll << 31) || c->n >= (1ll << 32) - 64) return;   // stays on k_sketch_cols

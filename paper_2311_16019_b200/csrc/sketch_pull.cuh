@@ -24,17 +24,27 @@
 namespace sylv {
 
 constexpr int kPullWarps = 8;
-constexpr int kPullBpwMax = 16;           // window bases per warp (runtime bpw <= this)
+constexpr int kPullBpwMax = 16;           // window bases per warp (runtime ceil(b / wpb) <= this)
 constexpr int kPullS = kPullBpwMax + 32;  // strip slots per warp and column (bpw + 31 used)
 // list entries whose R column loads are in flight together (16-32 loads of 256 B per warp)
 template <int R> constexpr int pull_u() { return R >= 4 ? 2 : 4; }
 template <int R> constexpr int pull_min_blocks() { return R >= 8 ? 2 : 3; }   // registers: 2 U R + R doubles
 constexpr int64_t kPullMinGroups = 4096;  // default: pull for n >= 131072 rows (with b >= 64)
 
-// Sort keys: entry (group g, bucket t) with window base p belongs to warp w = p / bpw of bucket
-// t; within the warp's list segment the order is (L2 chunk of g, p), and the radix sort is
-// stable, so equal keys keep increasing g.
-//   keys[t * ngroups + g] = ((t * wpb + w) * nch + g / gpch) * bpw + (p - w * bpw), vals = g,
+// Warp w of a bucket owns the window bases [q0(w), q0(w+1)), q0(w) = floor(w b / wpb): ranges of
+// floor(b/wpb) or ceil(b/wpb) = bpw bases, so wpb can be chosen to fill the resident warps of
+// the GPU exactly (every SM gets the same load).
+__host__ __device__ __forceinline__ uint32_t pull_q0(uint32_t w, uint32_t b, uint32_t wpb) {
+  return (uint32_t)(((uint64_t)w * b) / wpb);
+}
+__host__ __device__ __forceinline__ uint32_t pull_owner(uint32_t p, uint32_t b, uint32_t wpb) {
+  return (uint32_t)((((uint64_t)p + 1) * wpb - 1) / b);   // max w with q0(w) <= p
+}
+
+// Sort keys: entry (group g, bucket t) with window base p belongs to warp w = pull_owner(p) of
+// bucket t; within the warp's list segment the order is (L2 chunk of g, p), and the radix sort
+// is stable, so equal keys keep increasing g.
+//   keys[t * ngroups + g] = ((t * wpb + w) * nch + g / gpch) * bpw + (p - q0(w)), vals = g,
 //   counts[t * wpb + w] += 1 (-> exclusive scan = per-warp segment offsets)
 __global__ void k_pull_keys(int64_t ngroups, SketchParams sp, int64_t gpch, uint32_t nch, uint32_t bpw,
                             uint32_t wpb, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
@@ -44,8 +54,8 @@ __global__ void k_pull_keys(int64_t ngroups, SketchParams sp, int64_t gpch, uint
     const uint32_t t = (uint32_t)(i / ngroups);
     const int64_t g = i - (int64_t)t * ngroups;
     const uint32_t base = __umulhi(group_hash(sp, sp.m0 + (uint32_t)g, t, 0), sp.b);
-    const uint32_t w = base / bpw;
-    keys[i] = ((t * wpb + w) * nch + (uint32_t)(g / gpch)) * bpw + (base - w * bpw);
+    const uint32_t w = pull_owner(base, sp.b, wpb);
+    keys[i] = ((t * wpb + w) * nch + (uint32_t)(g / gpch)) * bpw + (base - pull_q0(w, sp.b, wpb));
     vals[i] = (uint32_t)g;
     atomicAdd(counts + t * wpb + w, 1u);
   }
@@ -130,7 +140,7 @@ __global__ void __launch_bounds__(kPullWarps * 32, pull_min_blocks<R>()) k_sketc
   const uint32_t wg = blockIdx.x * kPullWarps + warp;
   if (wg >= sp.zeta * wpb) return;               // whole warp; no block-wide barrier below
   const uint32_t t = wg / wpb;
-  const uint32_t q0 = (wg - t * wpb) * bpw;
+  const uint32_t q0 = pull_q0(wg - t * wpb, sp.b, wpb);
   const uint32_t n32 = (uint32_t)n;
   const double* xc[R];
 #pragma unroll
@@ -188,13 +198,13 @@ __global__ void k_sketch_pull_fold(const double* __restrict__ strips, SketchPara
     const int c = (int)(idx / s);
     const int64_t q = idx - (int64_t)c * s;
     const uint32_t t = (uint32_t)(q / b), p = (uint32_t)(q - (int64_t)t * b);
-    const uint32_t wl = p / bpw;
+    const uint32_t wl = pull_owner(p, b, wpb);
     double sum = 0.0;
-    // warps whose strip (bases q0 .. q0+bpw-1, slots q0 .. q0+bpw+30 mod b) covers p, nearest
-    // first; the distance (p - q0) mod b grows with k (the last warp of a bucket may be short)
+    // warps whose strip (slots q0 .. q0 + bpw + 30 mod b; zero past the warp's own bases + 30)
+    // covers p, nearest first; the distance (p - q0) mod b grows with k
     for (uint32_t k = 0; k < wpb; ++k) {
       const uint32_t w = (wl + wpb - k) % wpb;
-      const uint32_t dd = (p + b - w * bpw) % b;
+      const uint32_t dd = (p + b - pull_q0(w, b, wpb)) % b;
       if (dd >= bpw + 31u) break;
       sum += strips[((size_t)(t * wpb + w) * R + c) * kPullS + dd];
     }
