@@ -354,8 +354,13 @@ def main():
                          "kernels": {k: {"ms": v, "GBps": ab[k] / (v * 1e-3) / 1e9,
                                          "frac": ab[k] / (v * 1e-3) / 1e9 / peak} for k, v in cand.items()},
                          "skqr_ms": stats["ms_skqr"] / max(1, stats["n_skqr"]),
-                         "note": ("sketch: hashed sparse-sign scatter, bounded by shared-memory "
-                                  "read-modify-write latency, not by HBM" if dom == "sketch" else "")},
+                         "sketch_l2": {"bytes_per_launch": cfg.zeta * ab["sketch"],
+                                       "GBps": cfg.zeta * ab["sketch"] / (sk_ms * 1e-3) / 1e9,
+                                       "what": "pull sketch (sketch_pull.cuh): every element of the new block "
+                                               "is read zeta times from L2 (once per bucket); bound by L2->SM "
+                                               "bandwidth, not HBM (ncu lts__throughput, profiles/)"},
+                         "note": ("sketch: hashed sparse-sign gather, bounded by L2 bandwidth (zeta reads "
+                                  "per element), not by HBM" if dom == "sketch" else "")},
             "step_roofline": {"bytes_per_step": ab_job["step"] if sharded else ab["step"] * ws, "GBps": step_gbs,
                               "frac": step_gbs / (peak * ws), "frac_of_8TBps": step_gbs / (NOMINAL_HBM_GBS * ws),
                               "what": "SURVEY §8(d) B_n per block step (both sequences) / device step time"},

@@ -180,8 +180,11 @@ struct Sequence {
   double* Th = nullptr;       // ldT x ldT col-major
   double* Rh = nullptr;       // (dmax+2) R^2 (filled on demand)
   int* flags_h = nullptr;
-  // per-step events (ring of K+2): sketch of step j done (main -> side: the sketch-space QR
-  // reads w) and the QR of step j done with w (side -> main, before the next sketch writes it)
+  // per-step events (ring of K+2).  Sketch on the side stream (push sketch, small n): ev_c2 =
+  // step j's block ready (main -> side), ev_sk = the sketch of step j done reading ring slot
+  // j+1 (side -> main, before pass 2 of step j+K+1 rewrites it).  Sketch on the main stream
+  // (pull sketch): ev_c2 = sketch of step j done (main -> side QR), ev_sk = QR of step j done
+  // with w (side -> main, before the next sketch writes it).
   std::vector<cudaEvent_t> ev_c2, ev_sk;
   double beta[kMaxR * kMaxR];
   double ell[kMaxR * kMaxR];
@@ -808,7 +811,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
 // step_sketch (line 9): the sketch of the new block on `st` (it reads the block just written
 // and the ring slot is rewritten only by a later pass on the same stream), then the sketch-space
 // QR update on `side`, which overlaps the next step's passes.
-void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
+void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, bool sketch_on_side) {
   const int R = c->R, K = c->K;
   const int nwin = std::min(K, j);
   Win win{};
@@ -828,7 +831,8 @@ void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
     k_coef1<R_, K_><<<1, kThreads, 0, st>>>(p1, np1, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
   });
   // ---- a2 update + a3 Gram: pass 2 (writes Z_{j+1} = W' into the ring slot that the
-  //      sketch of step j-K-1 read, earlier on this stream)
+  //      sketch of step j-K-1 read: earlier on this stream, or on the side stream)
+  if (sketch_on_side && j - K - 1 >= 1) CK(cudaStreamWaitEvent(st, q.ev_sk[(j - K - 1) % (K + 2)], 0));
   if (timing) { t2 = ev_get(c, 1); CK(cudaEventRecord(t2.a, st)); }
   launch_pass2<true>(c, q, win, nwin, j, q.Yt, q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1), st);
   if (timing) { CK(cudaEventRecord(t2.b, st)); c->timed.push_back(t2); }
@@ -847,24 +851,34 @@ void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
                      cudaMemcpyDeviceToHost, st));
 }
 
-void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t side) {
+void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t side, bool sketch_on_side) {
   const int R = c->R, K = c->K;
   const bool timing = (c->cflags & 1) != 0;
   const int ne = K + 2;
-  const int chan_main = q.which == 0 ? kChanUMain : kChanVMain;
+  const int chan = q.which == 0 ? (sketch_on_side ? kChanUSide : kChanUMain) : (sketch_on_side ? kChanVSide : kChanVMain);
   TimedPair t3{}, t4{};
+  if (side != st) {
+    if (sketch_on_side) {
+      CK(cudaEventRecord(q.ev_c2[j % ne], st));               // block j+1 written
+      CK(cudaStreamWaitEvent(side, q.ev_c2[j % ne], 0));
+      st = side;
+    } else if (j >= 2) {
+      CK(cudaStreamWaitEvent(st, q.ev_sk[(j - 1) % ne], 0));   // QR j-1 done with w
+    }
+  }
   // ---- a4: w = (S W') R_{j+1}   (a5 timing includes the sketch)
-  if (side != st && j >= 2) CK(cudaStreamWaitEvent(st, q.ev_sk[(j - 1) % ne], 0));   // QR j-1 done with w
   if (timing) { t3 = ev_get(c, 2); CK(cudaEventRecord(t3.a, st)); }
   if (timing) { t4 = ev_get(c, 3); CK(cudaEventRecord(t4.a, st)); }
   launch_sketch(c, q, q.slot(j + 1), R, q.Rall + (int64_t)(j + 1) * R * R, q.w, st);
-  if (c->comm) c->comm->allreduce(q.w, (size_t)q.s * R, st, chan_main);   // S linear in rows
+  if (c->comm) c->comm->allreduce(q.w, (size_t)q.s * R, st, chan);   // S linear in rows
   if (timing) { CK(cudaEventRecord(t4.b, st)); c->timed.push_back(t4); }
-  if (side != st) {
+  if (side != st) {                                           // pull: QR on the side stream
     CK(cudaEventRecord(q.ev_c2[j % ne], st));
     CK(cudaStreamWaitEvent(side, q.ev_c2[j % ne], 0));
+    st = side;
+  } else if (sketch_on_side && st != c->st && st != c->st2) {
+    CK(cudaEventRecord(q.ev_sk[j % ne], st));                 // ring slot j+1 read
   }
-  st = side;
   // ---- a5: block CGS2 against Q (m = j R columns); CholQR2; T column
   const int m = j * R;
   const dim3 gq((m + kWarps - 1) / kWarps, c->RT);
@@ -898,7 +912,7 @@ void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t 
   count(c);
   CK(cudaGetLastError());
   if (timing) { CK(cudaEventRecord(t3.b, st)); c->timed.push_back(t3); }
-  if (st != c->st && st != c->st2) CK(cudaEventRecord(q.ev_sk[j % ne], st));
+  if (!sketch_on_side && st != c->st && st != c->st2) CK(cudaEventRecord(q.ev_sk[j % ne], st));   // w free
 }
 
 // Host copy of the leading rows x rows block of T (upper triangular, column-major, ldT).
@@ -954,28 +968,35 @@ void enqueue_steps(sylv_ctx* c, int first, int last) {
     CK(cudaEventRecord(c->fork, c->st));
     for (cudaStream_t s : others) CK(cudaStreamWaitEvent(s, c->fork, 0));
   }
-  // Phases per step: U and V passes concurrently (st, st2; each hides the other's small
-  // coefficient kernels), then the U sketch, then the V sketch — the L2-resident pull sketch
-  // (sketch_pull.cuh) must not share L2 with a streaming pass — then each sequence's
-  // sketch-space QR on its side stream, overlapping the next step's passes.
+  // Pull sketch (large n): per step, U and V passes concurrently (st, st2; each hides the
+  // other's small coefficient kernels), then the U sketch, then the V sketch — the L2-resident
+  // pull sketch (sketch_pull.cuh) must not share L2 with a streaming pass — then each
+  // sequence's sketch-space QR on its side stream, overlapping the next step's passes.
+  // Push sketch (small n): sketch + QR on the side streams, overlapping the next passes.
+  const bool on_side = !c->seq[0].pl_list;
   for (int j = first; j <= last; ++j) {
     if (serial) {
-      step_passes(c, c->seq[0], j, c->st);
-      step_passes(c, c->seq[1], j, c->st);
-      step_sketch(c, c->seq[0], j, c->st, c->st);
-      step_sketch(c, c->seq[1], j, c->st, c->st);
-      continue;
+      step_passes(c, c->seq[0], j, c->st, false);
+      step_sketch(c, c->seq[0], j, c->st, c->st, false);
+      step_passes(c, c->seq[1], j, c->st, false);
+      step_sketch(c, c->seq[1], j, c->st, c->st, false);
+    } else if (on_side) {
+      step_passes(c, c->seq[0], j, c->st, true);
+      step_sketch(c, c->seq[0], j, c->st, c->st3, true);
+      step_passes(c, c->seq[1], j, c->st2, true);
+      step_sketch(c, c->seq[1], j, c->st2, c->st4, true);
+    } else {
+      step_passes(c, c->seq[0], j, c->st, false);
+      step_passes(c, c->seq[1], j, c->st2, false);
+      CK(cudaEventRecord(c->phase[0], c->st2));      // V passes done
+      CK(cudaStreamWaitEvent(c->st, c->phase[0], 0));
+      step_sketch(c, c->seq[0], j, c->st, c->st3, false);
+      CK(cudaEventRecord(c->phase[1], c->st));       // U sketch done
+      CK(cudaStreamWaitEvent(c->st2, c->phase[1], 0));
+      step_sketch(c, c->seq[1], j, c->st2, c->st4, false);
+      CK(cudaEventRecord(c->phase[2], c->st2));      // V sketch done
+      CK(cudaStreamWaitEvent(c->st, c->phase[2], 0));
     }
-    step_passes(c, c->seq[0], j, c->st);
-    step_passes(c, c->seq[1], j, c->st2);
-    CK(cudaEventRecord(c->phase[0], c->st2));      // V passes done
-    CK(cudaStreamWaitEvent(c->st, c->phase[0], 0));
-    step_sketch(c, c->seq[0], j, c->st, c->st3);
-    CK(cudaEventRecord(c->phase[1], c->st));       // U sketch done
-    CK(cudaStreamWaitEvent(c->st2, c->phase[1], 0));
-    step_sketch(c, c->seq[1], j, c->st2, c->st4);
-    CK(cudaEventRecord(c->phase[2], c->st2));      // V sketch done
-    CK(cudaStreamWaitEvent(c->st, c->phase[2], 0));
   }
   if (!serial) {
     for (int i = 0; i < 3; ++i) {
