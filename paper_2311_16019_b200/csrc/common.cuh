@@ -14,6 +14,7 @@ namespace sylv {
 constexpr int kMaxR = 8;
 constexpr int kMaxK = 4;
 constexpr int kThreads = 256;            // CTA size of the streaming kernels
+constexpr int kSmallThreads = 1024;      // CTA size of the one-CTA coefficient kernels (sspace.cuh)
 constexpr int kWarps = kThreads / 32;
 
 // ---- hashed sparse-sign S (never stored) ------------------------------------------

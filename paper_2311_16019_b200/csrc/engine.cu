@@ -394,10 +394,10 @@ void cholqr2(sylv_ctx* c, Sequence& q, double* in, int64_t col0, double* tau_out
   double* tbi = q.small + 128;     // R^2
   SYLV_DISPATCH_R(R, {
     k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, in, q.part_s);
-    k_chol_small<R_><<<1, kThreads, 0, st>>>(q.part_s, gs, ta, tai, nullptr, q.flags, flag_slot);
+    k_chol_small<R_><<<1, kSmallThreads, 0, st>>>(q.part_s, gs, ta, tai, nullptr, q.flags, flag_slot);
     k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, in, tai, q.w2, 0);
     k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, q.w2, q.part_s);
-    k_chol_small<R_><<<1, kThreads, 0, st>>>(q.part_s, gs, tau_out, tbi, ta, q.flags, flag_slot);
+    k_chol_small<R_><<<1, kSmallThreads, 0, st>>>(q.part_s, gs, tau_out, tbi, ta, q.flags, flag_slot);
     k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, q.w2, tbi, q.Q + col0 * q.s, q.s);
   });
   count(c, 6);
@@ -510,7 +510,7 @@ Tma25 tma_args(const Sequence& q, int j, int nwin) {
 int pass_parts(const sylv_ctx* c, const Sequence& q) { return q.tma ? c->G25 : c->G; }
 
 // out[e] = sum of the nparts per-CTA partials (block_sum_parts order), one CTA
-__global__ void k_sum_partials(const double* __restrict__ partial, int nparts, int len, double* __restrict__ out) {
+__global__ void __launch_bounds__(kSmallThreads) k_sum_partials(const double* __restrict__ partial, int nparts, int len, double* __restrict__ out) {
   block_sum_parts(partial, nparts, len, len, out);
 }
 
@@ -523,7 +523,7 @@ const double* reduce_partials(sylv_ctx* c, const double* partial, int nparts, in
     *nparts_out = nparts;
     return partial;
   }
-  k_sum_partials<<<1, kThreads, 0, st>>>(partial, nparts, len, out);
+  k_sum_partials<<<1, kSmallThreads, 0, st>>>(partial, nparts, len, out);
   count(c);
   CK(cudaGetLastError());
   c->comm->allreduce(out, (size_t)len, st, chan);
@@ -785,7 +785,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     int npc = c->G;
     const double* pc = reduce_partials(c, q.part2, c->G, R * R, c->red ? c->red + (int64_t)q.which * (K + 1) * R * R : nullptr,
                                        c->st, kChanSetup, &npc);
-    SYLV_DISPATCH_R(R, { k_chol_small<R_><<<1, kThreads, 0, c->st>>>(pc, npc, ell_d, elli_d, nullptr, q.flags, 0); });
+    SYLV_DISPATCH_R(R, { k_chol_small<R_><<<1, kSmallThreads, 0, c->st>>>(pc, npc, ell_d, elli_d, nullptr, q.flags, 0); });
   }
   count(c, 2);
   CK(cudaGetLastError());
@@ -828,7 +828,7 @@ void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, bool sketch_o
   int np1 = G;
   const double* p1 = reduce_partials(c, q.part1, G, K * R * R, red, st, chan_main, &np1);
   SYLV_DISPATCH_RK(R, K, {
-    k_coef1<R_, K_><<<1, kThreads, 0, st>>>(p1, np1, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
+    k_coef1<R_, K_><<<1, kSmallThreads, 0, st>>>(p1, np1, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
   });
   // ---- a2 update + a3 Gram: pass 2 (writes Z_{j+1} = W' into the ring slot that the
   //      sketch of step j-K-1 read: earlier on this stream, or on the side stream)
@@ -839,7 +839,7 @@ void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, bool sketch_o
   int np2 = G;
   const double* p2 = reduce_partials(c, q.part2, G, R * R, red ? red + K * R * R : nullptr, st, chan_main, &np2);
   SYLV_DISPATCH_RK(R, K, {
-    k_coef2<R_, K_><<<1, kThreads, 0, st>>>(p2, np2, j, q.Rall, q.Hc, q.hn2, q.flags);
+    k_coef2<R_, K_><<<1, kSmallThreads, 0, st>>>(p2, np2, j, q.Rall, q.Hc, q.hn2, q.flags);
   });
   // ghost planes/lines of the new block for the next step's stencil (sharded contexts)
   if (c->comm) c->comm->halo(q.slot(j + 1), R, q.ld, q.gz, st, chan_main);

@@ -23,20 +23,34 @@ __device__ __forceinline__ double sum_parts(const double* __restrict__ partial, 
 // and the 32 lane sums are combined by a fixed butterfly (same order on every run).
 __device__ __forceinline__ void block_sum_parts(const double* __restrict__ partial, int nparts, int64_t len,
                                                 int nelem, double* __restrict__ out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int e = warp; e < nelem; e += nw) {
+  // nc chunks of parts per element, one thread per (element, chunk) — coalesced over the
+  // elements, 8 independent loads in flight per thread — then the chunk sums in chunk order
+  // (fixed order: deterministic).  Launched with kSmallThreads threads; nelem <= len <=
+  // kMaxK R^2.  The chunking depends on len, not nelem, so a sum over all len elements
+  // (k_sum_partials, sharded contexts) adds each element in the same order as a sum over a
+  // prefix (k_coef1 with nwin < K): bit-identical results.
+  __shared__ double acc[kSmallThreads];
+  const int nt = blockDim.x;
+  const int nc = max(1, min(nt / (len > 0 ? (int)len : 1), nparts));
+  for (int idx = threadIdx.x; idx < nelem * nc; idx += nt) {
+    const int e = idx % nelem, c = idx / nelem;
     double s = 0.0;
-    for (int p = lane; p < nparts; p += 32) s += partial[(int64_t)p * len + e];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(SYLV_FULL_MASK, s, off);
-    if (lane == 0) out[e] = s;
+#pragma unroll 8
+    for (int p = c; p < nparts; p += nc) s += partial[(int64_t)p * len + e];
+    acc[idx] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nelem; e += nt) {
+    double s = 0.0;
+    for (int c = 0; c < nc; ++c) s += acc[c * nelem + e];
+    out[e] = s;
   }
 }
 
 // h_{i,j} = R_i^T P_i R_j, K_i = R_i h_{i,j}; Kc[j] = [R_j, K_0..]; Hc[j] = [h_.., 0.., h_{j+1,j}]
 // (one CTA; thread per matrix entry for the r x r products)
 template <int R, int K>
-__global__ void k_coef1(const double* __restrict__ partial, int nparts, int nwin, int j,
+__global__ void __launch_bounds__(kSmallThreads) k_coef1(const double* __restrict__ partial, int nparts, int nwin, int j,
                         const double* __restrict__ Rall, double* __restrict__ Kc,
                         double* __restrict__ Hc, double* __restrict__ hnorm2) {
   constexpr int RR = R * R;
@@ -88,7 +102,7 @@ __global__ void k_coef1(const double* __restrict__ partial, int nparts, int nwin
 // breakdown flag (bit 0) if min diag h <= 1e-14 ||W~||_F  (R11), with
 // ||W~||_F^2 = ||W'||_F^2 + sum_i ||h_{i,j}||_F^2 (window orthonormal); bit 1 if G not PD.
 template <int R, int K>
-__global__ void k_coef2(const double* __restrict__ partial, int nparts, int j,
+__global__ void __launch_bounds__(kSmallThreads) k_coef2(const double* __restrict__ partial, int nparts, int j,
                         double* __restrict__ Rall, double* __restrict__ Hc,
                         const double* __restrict__ hnorm2, int* __restrict__ flags) {
   __shared__ double G[R * R];
@@ -121,7 +135,7 @@ __global__ void k_coef2(const double* __restrict__ partial, int nparts, int j,
 // tau = chol(sum of Gram partials) (upper); tinv = tau^{-1}; if prev: tau_out = tau * prev.
 // Sets flags[slot] bit 2 if not positive definite (lost independence).
 template <int R>
-__global__ void k_chol_small(const double* __restrict__ partial, int nparts,
+__global__ void __launch_bounds__(kSmallThreads) k_chol_small(const double* __restrict__ partial, int nparts,
                              double* __restrict__ tau_out, double* __restrict__ tinv_out,
                              const double* __restrict__ prev, int* __restrict__ flags, int slot) {
   __shared__ double G[R * R];
