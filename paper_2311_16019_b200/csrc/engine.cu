@@ -148,6 +148,7 @@ struct Sequence {
   double* ring = nullptr;     // (K+1) blocks, SoA R x ld
   double* Cdev = nullptr;     // SoA R x ld block (allocation; data at Cdev + gz)
   double* Yt = nullptr;       // CSR: A Z_d (SoA)
+  double* Zaos = nullptr;     // CSR, r even: row-interleaved copy of Z_d for the pass-1 gathers
   double* sk = nullptr;       // s x R (row-major)
   double* skpart = nullptr;   // nchunk x R x s sketch partials
   // pull sketch (sketch_pull.cuh): groups sorted by (bucket, L2 chunk, window base)
@@ -367,7 +368,7 @@ void upload_csr(Sequence& q, const sylv_operator* A, bool transpose, cudaStream_
 void free_seq(Sequence& q) {
   for (cudaEvent_t e : q.ev_c2) cudaEventDestroy(e);
   for (cudaEvent_t e : q.ev_sk) cudaEventDestroy(e);
-  double* dp[] = {q.ring, q.Cdev, q.Yt, q.sk, q.skpart, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
+  double* dp[] = {q.ring, q.Cdev, q.Yt, q.Zaos, q.sk, q.skpart, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
                   q.part1, q.part2, q.part_s, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv};
   for (double* p : dp) dfree(p);
   dfree(q.flags);
@@ -469,7 +470,10 @@ void setup_tma(sylv_ctx* c, Sequence& q) {
   p.tiles_x = (N + kTx - 1) / kTx;
   p.tiles_y = (N + kTY25 - 1) / kTY25;
   const int64_t tiles = (int64_t)p.tiles_x * p.tiles_y;
-  const int grid = (c->R == 4 ? 3 : 2) * c->sm;   // resident CTAs: r = 4 stages are half the size
+  // resident CTAs: r = 4 stages are half the size (4 stages of 11.6 KB; registers allow 4 CTAs)
+  int gmul = c->R == 4 ? 4 : 2;
+  if (const char* e = std::getenv("SYLV_G25MUL")) gmul = std::max(1, std::atoi(e));   // tuning
+  const int grid = gmul * c->sm;
   int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, nz / 16), (8 * grid + tiles - 1) / tiles));
   p.zseg = (nz + nseg - 1) / nseg;
   p.nseg = (nz + p.zseg - 1) / p.zseg;
@@ -555,7 +559,11 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cud
     }
 #undef SYLV_ST3D_P1
   } else if (q.op.kind == kCSR && R <= 4) {
-    SYLV_DISPATCH_R124_K(R, K, { k_pass1_csr<R_, K_><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); });
+    if (R % 2 == 0) {   // AoS copy of Z_d for the gathers
+      SYLV_DISPATCH_R124(R, { k_soa_to_aos<R_><<<4 * c->sm, kThreads, 0, st>>>(c->n, win.p[nwin - 1], q.ld, q.Zaos); });
+      count(c);
+    }
+    SYLV_DISPATCH_R124_K(R, K, { k_pass1_csr<R_, K_><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Zaos, q.Yt, q.part1); });
   } else if (R == 8) {
     switch (K) {
       case 1: k_pass1_r8<1><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); break;
@@ -720,6 +728,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.ring = dalloc<double>((size_t)(K + 1) * blk);
   q.Cdev = dalloc<double>(blk);
   if (A->kind == SYLV_OP_CSR) q.Yt = dalloc<double>(blk);
+  if (A->kind == SYLV_OP_CSR && R % 2 == 0) q.Zaos = dalloc<double>((size_t)c->n * R);
   q.sk = dalloc<double>(sR);
   q.skpart = dalloc<double>((size_t)c->nchunk * sR);
   if (c->sk_pull && q.sp.b >= 64) build_pull_lists(c, q, c->st);

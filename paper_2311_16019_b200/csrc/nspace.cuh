@@ -238,17 +238,40 @@ __global__ void __launch_bounds__(kThreads) k_pass2_rows(OpParams op, Win win, i
 }
 
 // =====================================================================================
-// CSR pass 1 (a1 + a2 inner products): 8 lanes per row
+// CSR pass 1 (a1 + a2 inner products): 4 lanes per row
 // =====================================================================================
-// Each 8-lane sub-warp owns one row at a time: lanes stride over the row's nonzeros
-// (coalesced col/val loads), accumulate all R columns of (A Z_d)[row] from ONE sweep
-// of the row (the generic kernel re-walks the row per column), and reduce with three
-// xor-shuffles.  The sub-warp's lane 0 stores Yt[row] (pass 2 streams it instead of
-// re-reading A) and accumulates P_i += Z_i[row]^T Yt[row].
-constexpr int kCsrLanes = 8;
+// Each 4-lane sub-warp owns one row at a time (8 rows per warp): lanes stride over the row's
+// nonzeros, issue all value/index loads of their first 6 nonzeros before the gathers, gather
+// the rows of Z_d from a row-interleaved copy (one sector per nonzero for r <= 4), accumulate
+// all R columns of (A Z_d)[row] from ONE sweep of the row, and reduce with two xor-shuffles;
+// the next row's row pointers are loaded one iteration ahead.  The sub-warp's lane 0 stores
+// Yt[row] (pass 2 streams it instead of re-reading A) and accumulates P_i += Z_i[row]^T Yt[row].
+// c4 (r = 2): 0.76 ms -> 0.48 ms per launch (8 lanes, SoA gathers -> this).
+constexpr int kCsrLanes = 4;
+
+// Row-interleaved (AoS) copy of an SoA block for the CSR gathers: Za[row*R + c] = Z[c*ld + row].
+// One gathered row is then R contiguous doubles (one 32-byte sector for R <= 4) instead of R
+// separate sectors: half (R = 2) or a quarter (R = 4) of the L1 wavefronts of pass 1.
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_soa_to_aos(int64_t n, const double* __restrict__ Z, int64_t ld,
+                                                         double* __restrict__ Za) {
+  for (int64_t row = (int64_t)blockIdx.x * kThreads + threadIdx.x; row < n; row += (int64_t)gridDim.x * kThreads) {
+    double v[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) v[c] = __ldg(Z + c * ld + row);
+    if (R % 2 == 0) {
+#pragma unroll
+      for (int c = 0; c < R; c += 2) reinterpret_cast<double2*>(Za + row * R)[c / 2] = make_double2(v[c], v[c + 1]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < R; ++c) Za[row * R + c] = v[c];
+    }
+  }
+}
 
 template <int R, int K>
 __global__ void __launch_bounds__(kThreads) k_pass1_csr(OpParams op, Win win, int nwin, int64_t ld,
+                                                        const double* __restrict__ Za,
                                                         double* __restrict__ Yt, double* __restrict__ partial) {
   __shared__ double sm[kWarps * K * R * R];
   double acc[K * R * R];
@@ -260,19 +283,51 @@ __global__ void __launch_bounds__(kThreads) k_pass1_csr(OpParams op, Win win, in
   // warp-uniform trip count: every lane of a warp runs the same iterations (the shuffles
   // below use the full mask); sub-warps past the last row do no work
   const int64_t wfirst = (int64_t)blockIdx.x * (kThreads / kCsrLanes) + (threadIdx.x & ~31) / kCsrLanes;
+  // row pointers of the next row are loaded one iteration ahead
+  const int64_t r0 = wfirst + (threadIdx.x & 31) / kCsrLanes;
+  int64_t q0 = r0 < op.n ? __ldg(op.rp + r0) : 0, q1 = r0 < op.n ? __ldg(op.rp + r0 + 1) : 0;
   for (int64_t wrow = wfirst; wrow < op.n; wrow += nsub) {
     const int64_t row = wrow + (threadIdx.x & 31) / kCsrLanes;
     const bool valid = row < op.n;
     double y[R];
 #pragma unroll
     for (int c = 0; c < R; ++c) y[c] = 0.0;
-    const int64_t p0 = valid ? __ldg(op.rp + row) : 0, p1 = valid ? __ldg(op.rp + row + 1) : 0;
-    for (int64_t p = p0 + sub; p < p1; p += kCsrLanes) {
-      const double a = __ldg(op.cv + p);
-      const int64_t col = __ldg(op.ci + p);
-#pragma unroll
-      for (int c = 0; c < R; ++c) y[c] = fma(a, __ldg(Zd + c * ld + col), y[c]);
+    const int64_t p0 = q0, p1 = q1;
+    {
+      const int64_t rn = row + nsub;
+      q0 = rn < op.n ? __ldg(op.rp + rn) : 0;
+      q1 = rn < op.n ? __ldg(op.rp + rn + 1) : 0;
     }
+    // gather of Z_d row `col` into y (AoS copy for even R)
+    auto gather = [&](double a, int64_t col) {
+      if (R % 2 == 0) {
+        const double2* zr = reinterpret_cast<const double2*>(Za + col * R);
+#pragma unroll
+        for (int c = 0; c < R; c += 2) {
+          const double2 z = __ldg(zr + c / 2);
+          y[c] = fma(a, z.x, y[c]);
+          y[c + 1] = fma(a, z.y, y[c + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < R; ++c) y[c] = fma(a, __ldg(Zd + c * ld + col), y[c]);
+      }
+    };
+    // the first kCsrU nonzeros per lane: all value/index loads issued before the gathers
+    // (rows of the BASELINE CSR have 21 nonzeros: <= 6 per lane); longer rows continue below
+    constexpr int kCsrU = 6;
+    double av[kCsrU];
+    int32_t cl[kCsrU];
+#pragma unroll
+    for (int u = 0; u < kCsrU; ++u) {
+      const int64_t p = p0 + sub + u * kCsrLanes;
+      av[u] = p < p1 ? __ldg(op.cv + p) : 0.0;
+      cl[u] = p < p1 ? __ldg(op.ci + p) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kCsrU; ++u)
+      if (cl[u] >= 0) gather(av[u], cl[u]);
+    for (int64_t p = p0 + sub + kCsrU * kCsrLanes; p < p1; p += kCsrLanes) gather(__ldg(op.cv + p), __ldg(op.ci + p));
 #pragma unroll
     for (int c = 0; c < R; ++c) {
 #pragma unroll

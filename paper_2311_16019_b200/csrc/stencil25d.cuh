@@ -41,7 +41,7 @@ constexpr int kTx = 32;          // tile width in x (points)
 // pipeline stages (planes in flight): enough bytes in flight per SM to cover HBM latency
 // (r = 4 tiles carry half the bytes of r = 8 ones)
 template <int R>
-constexpr int stages25() { return R >= 8 ? 3 : 6; }
+constexpr int stages25() { return R >= 8 ? 3 : 4; }
 
 struct Tma25 {
   CUtensorMap zd;                // halo box map of Z_d's ring slot
