@@ -115,9 +115,13 @@ typedef struct {
  * beta_1 ell^{-1} (R3).  C1, C2: n_local x r row-major (this rank's rows),
  * host or device.  stream: a cudaStream_t (NULL = legacy default stream).
  * nccl_comm: NULL (single rank) or a sylv_comm* (row-sharded context, SURVEY §8(e):
- * z-slabs / y-line ranges of the 2-D/3-D stencils; every rank calls every function of
- * the context collectively, in the same order, with identical cfg).  Each rank keeps
- * its rows of every basis block (plus ghost planes filled by halo exchange); the
+ * z-slabs / y-line ranges of the 2-D/3-D stencils, ranges of 32-row groups of a CSR matrix;
+ * every rank calls every function of the context collectively, in the same order, with
+ * identical cfg).  CSR operators of a sharded context describe the GLOBAL matrices (every
+ * rank passes the same arrays, A and B, not B^T); each rank keeps its rows of A and of B^T
+ * with local column indices, and its halo width is the band max |col - row| of the matrix
+ * (every rank must own at least band rows; c4: 4096).  Each rank keeps
+ * its rows of every basis block (plus ghost planes/rows filled by halo exchange); the
  * Gram-Schmidt inner products, Grams and partial sketches are summed over the ranks
  * (bit-identical on all ranks), the sketch-space QR and the projected solves are
  * replicated.  sylv_sketch_solution / get_block / apply_sketch work on local rows
@@ -201,10 +205,11 @@ void sylv_sketch_destroy(sylv_ctx* ctx);
  * sketches (S is linear in rows)") ------------------------------------------------------ */
 typedef struct sylv_comm sylv_comm; /* opaque transport handle */
 
-/* Balanced split of a stencil grid over nranks: rank gets the global rows
- * [*row_begin, *row_end) = whole z-planes (3-D) or y-lines (2-D), every range starting at a
- * multiple of 32 rows (the sketch hash groups rows by 32).  Host only.
- * SYLV_E_INVALID if the grid has fewer plane groups than ranks or kind is not a stencil. */
+/* Balanced split of an operator over nranks: rank gets the global rows
+ * [*row_begin, *row_end) = whole z-planes (3-D) or y-lines (2-D), or (kind = SYLV_OP_CSR; N is
+ * ignored) a range of 32-row groups; every range starts at a multiple of 32 rows (the sketch
+ * hash groups rows by 32).  Host only.  SYLV_E_INVALID if there are fewer
+ * plane/row groups than ranks. */
 sylv_status sylv_partition(int32_t kind, int32_t N, int64_t n, int32_t nranks, int32_t rank,
                            int64_t* row_begin, int64_t* row_end);
 

@@ -313,13 +313,14 @@ def operators_for(cfg, csr_pair=None):
 
 
 def partition(cfg, nranks: int, rank: int) -> Tuple[int, int]:
-    """sylv_partition: this rank's global rows [begin, end) of a stencil config."""
+    """sylv_partition: this rank's global rows [begin, end) of a config (stencil: whole
+    planes/lines; CSR: multiples of 32 rows)."""
     lib = load_library()
-    kind = {"stencil2d": OP_STENCIL2D, "stencil3d": OP_STENCIL3D}.get(cfg.kind)
+    kind = {"stencil2d": OP_STENCIL2D, "stencil3d": OP_STENCIL3D, "csr": OP_CSR}.get(cfg.kind)
     if kind is None:
-        raise SylvError(1, "sharded contexts support the stencil configs")
+        raise SylvError(1, f"unknown operator kind {cfg.kind}")
     b, e = C.c_int64(), C.c_int64()
-    st = lib.sylv_partition(kind, cfg.N, cfg.n, nranks, rank, C.byref(b), C.byref(e))
+    st = lib.sylv_partition(kind, cfg.N if kind != OP_CSR else 1, cfg.n, nranks, rank, C.byref(b), C.byref(e))
     if st != OK:
         raise SylvError(st, f"cannot split {cfg.name} over {nranks} ranks")
     return b.value, e.value

@@ -325,6 +325,28 @@ __global__ void k_csr_transpose_fill(const int32_t* __restrict__ key, const int3
 // CSR of A (or B^T when transpose): host or device input arrays, uploaded as they are; the
 // transpose is a stable radix sort of the nonzeros by column on the device (rows stay
 // ascending inside each column, so B^T's rows are sorted and the result is deterministic).
+// max |col - row| over the nonzeros (the halo width of a row-sharded CSR operator)
+__global__ void k_csr_band(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t n,
+                           int* __restrict__ band) {
+  int m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) m = max(m, abs(ci[p] - (int)i));
+  atomicMax(band, m);
+}
+
+// rows [b, e) of a CSR matrix with column indices made local (col - b; ghosts are negative
+// or >= e - b): rp_l[i] = rp[b+i] - rp[b], ci_l = ci - b, cv_l = cv
+__global__ void k_csr_slice(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ cv,
+                            int64_t b, int64_t e, int64_t p0, int64_t nnz_l, int64_t* __restrict__ rp_l,
+                            int32_t* __restrict__ ci_l, double* __restrict__ cv_l) {
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, ts = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = t0; i <= e - b; i += ts) rp_l[i] = rp[b + i] - p0;
+  for (int64_t p = t0; p < nnz_l; p += ts) {
+    ci_l[p] = ci[p0 + p] - (int32_t)b;
+    cv_l[p] = cv[p0 + p];
+  }
+}
+
 void upload_csr(Sequence& q, const sylv_operator* A, bool transpose, cudaStream_t st) {
   const int64_t n = A->n, nnz = A->nnz;
   const bool dev = is_device_ptr(A->row_ptr);
@@ -560,10 +582,11 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cud
 #undef SYLV_ST3D_P1
   } else if (q.op.kind == kCSR && R <= 4) {
     if (R % 2 == 0) {   // AoS copy of Z_d for the gathers
-      SYLV_DISPATCH_R124(R, { k_soa_to_aos<R_><<<4 * c->sm, kThreads, 0, st>>>(c->n, win.p[nwin - 1], q.ld, q.Zaos); });
+      // rows -gz .. n+gz-1 (ghost rows of a sharded CSR operator included)
+      SYLV_DISPATCH_R124(R, { k_soa_to_aos<R_><<<4 * c->sm, kThreads, 0, st>>>(c->n + 2 * q.gz, win.p[nwin - 1] - q.gz, q.ld, q.Zaos); });
       count(c);
     }
-    SYLV_DISPATCH_R124_K(R, K, { k_pass1_csr<R_, K_><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Zaos, q.Yt, q.part1); });
+    SYLV_DISPATCH_R124_K(R, K, { k_pass1_csr<R_, K_><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Zaos ? q.Zaos + q.gz * R : nullptr, q.Yt, q.part1); });
   } else if (R == 8) {
     switch (K) {
       case 1: k_pass1_r8<1><<<c->G, kThreads, 0, st>>>(q.op, win, nwin, q.ld, q.Yt, q.part1); break;
@@ -700,6 +723,48 @@ struct InitTrace {
   }
 };
 
+// Row-sharded CSR: keep rows [row_begin, row_end) of the global matrix
+// uploaded by upload_csr, with local column indices.  The halo width is the matrix band
+// max |col - row| (computed from the global matrix, hence the same on every rank); columns of
+// the local rows reach at most band rows into the neighbour ranks, whose boundary rows the
+// halo exchange copies into the ghost rows (gz = band) before and after each block column.
+void shard_csr(sylv_ctx* c, Sequence& q) {
+  cudaStream_t st = c->st;
+  const int64_t ng = c->n_global, b = c->row_begin, e = c->row_end;
+  int* band_d = dalloc<int>(1);
+  CK(cudaMemsetAsync(band_d, 0, sizeof(int), st));
+  k_csr_band<<<1024, 256, 0, st>>>(q.rp, q.ci, ng, band_d);
+  count(c);
+  int band = 0;
+  int64_t pb[2];
+  CK(cudaMemcpyAsync(&band, band_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&pb[0], q.rp + b, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&pb[1], q.rp + e, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  dfree(band_d);
+  for (int r = 0; r < c->comm->nranks; ++r)
+    if (c->comm->re[r] - c->comm->rb[r] < band)
+      throw Status{SYLV_E_INVALID, "CSR sharding: every rank needs at least band = max|col-row| rows"};
+  const int64_t nnz_l = pb[1] - pb[0];
+  int64_t* rp_l = dalloc<int64_t>(e - b + 1);
+  int32_t* ci_l = dalloc<int32_t>(nnz_l);
+  double* cv_l = dalloc<double>(nnz_l);
+  k_csr_slice<<<1024, 256, 0, st>>>(q.rp, q.ci, q.cv, b, e, pb[0], nnz_l, rp_l, ci_l, cv_l);
+  count(c);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  dfree(q.rp);
+  dfree(q.ci);
+  dfree(q.cv);
+  q.rp = rp_l;
+  q.ci = ci_l;
+  q.cv = cv_l;
+  q.op.rp = q.rp;
+  q.op.ci = q.ci;
+  q.op.cv = q.cv;
+  q.gz = band;
+}
+
 void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, bool transpose,
                    const double* C, uint64_t seed) {
   InitTrace tr;
@@ -709,12 +774,16 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.dmax = c->dmax;
   q.n = c->n;
   q.s = c->s;
-  q.gz = (A->kind == SYLV_OP_STENCIL3D) ? (int64_t)A->grid[0] * A->grid[0]
-         : (A->kind == SYLV_OP_STENCIL2D) ? (int64_t)A->grid[0] : 0;
-  q.ld = (c->n + 2 * q.gz + 63) / 64 * 64;
-  q.ldT = (int64_t)(c->dmax + 1) * c->R;
   q.op = make_op(A, transpose);
   q.op.n = c->n;   // this rank's rows
+  q.gz = (A->kind == SYLV_OP_STENCIL3D) ? (int64_t)A->grid[0] * A->grid[0]
+         : (A->kind == SYLV_OP_STENCIL2D) ? (int64_t)A->grid[0] : 0;
+  if (A->kind == SYLV_OP_CSR) {
+    upload_csr(q, A, transpose, c->st);          // the global matrix (A, or B^T); sets q.op's arrays
+    if (c->comm) shard_csr(c, q);                // this rank's rows; q.gz = band
+  }
+  q.ld = (c->n + 2 * q.gz + 63) / 64 * 64;
+  q.ldT = (int64_t)(c->dmax + 1) * c->R;
   q.sp.seed = (uint32_t)(seed ^ (seed >> 32));
   q.sp.zeta = (uint32_t)c->zeta;
   q.sp.b = (uint32_t)(c->s / c->zeta);
@@ -722,13 +791,11 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.sp.m0 = (uint32_t)(c->row_begin >> 5);   // global group index of local row 0
   const int R = c->R, K = c->K;
   const int64_t blk = q.ld * R, sR = c->s * R, ldT = q.ldT;
-  if (A->kind == SYLV_OP_CSR) upload_csr(q, A, transpose, c->st);
-
   tr.mark("setup", c->st);
   q.ring = dalloc<double>((size_t)(K + 1) * blk);
   q.Cdev = dalloc<double>(blk);
   if (A->kind == SYLV_OP_CSR) q.Yt = dalloc<double>(blk);
-  if (A->kind == SYLV_OP_CSR && R % 2 == 0) q.Zaos = dalloc<double>((size_t)c->n * R);
+  if (A->kind == SYLV_OP_CSR && R % 2 == 0) q.Zaos = dalloc<double>((size_t)(c->n + 2 * q.gz) * R);
   q.sk = dalloc<double>(sR);
   q.skpart = dalloc<double>((size_t)c->nchunk * sR);
   if (c->sk_pull && q.sp.b >= 64) build_pull_lists(c, q, c->st);
@@ -1092,7 +1159,14 @@ sylv_status sylv_partition(int32_t kind, int32_t N, int64_t n, int32_t nranks, i
   int64_t unit;
   if (kind == SYLV_OP_STENCIL3D && n == (int64_t)N * N * N) unit = (int64_t)N * N;
   else if (kind == SYLV_OP_STENCIL2D && n == (int64_t)N * N) unit = N;
-  else return SYLV_E_INVALID;
+  else if (kind == SYLV_OP_CSR && n > 0) {
+    // rows in groups of 32 (N is ignored)
+    const int64_t ngrp = (n + 31) / 32;
+    if (ngrp < nranks) return SYLV_E_INVALID;
+    *row_begin = std::min<int64_t>(n, 32 * (ngrp * rank / nranks));
+    *row_end = std::min<int64_t>(n, 32 * (ngrp * (rank + 1) / nranks));
+    return *row_end > *row_begin ? SYLV_OK : SYLV_E_INVALID;
+  } else return SYLV_E_INVALID;
   // planes/lines in groups of g so that every range starts at a multiple of 32 rows
   int64_t g = 1;
   while ((g * unit) % 32) ++g;
@@ -1191,9 +1265,8 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
   if (cfg->s < (int64_t)(cfg->d_max + 1) * r) return fail(c, SYLV_E_INVALID, "s must be >= (d_max+1) r");
   if (A->n != B->n || A->n <= 0) return fail(c, SYLV_E_INVALID, "A and B must be n x n with equal n");
   Comm* comm = nccl_comm ? static_cast<sylv_comm*>(nccl_comm)->impl : nullptr;
-  if (comm && (A->kind != B->kind || A->grid[0] != B->grid[0] ||
-               !(A->kind == SYLV_OP_STENCIL2D || A->kind == SYLV_OP_STENCIL3D)))
-    return fail(c, SYLV_E_INVALID, "sharded contexts support the 2-D/3-D stencil operators (same grid for A and B)");
+  if (comm && (A->kind != B->kind || (A->kind != SYLV_OP_CSR && A->grid[0] != B->grid[0])))
+    return fail(c, SYLV_E_INVALID, "sharded contexts need A and B of the same kind (and grid for stencils)");
   if ((uint64_t)A->n * cfg->zeta >= (1ull << 32)) return fail(c, SYLV_E_INVALID, "n*zeta must be < 2^32");
   for (const sylv_operator* o : {A, B}) {
     if (o->kind == SYLV_OP_STENCIL2D || o->kind == SYLV_OP_STENCIL3D) {
@@ -1223,14 +1296,16 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
           sylv_partition(A->kind, A->grid[0], A->n, comm->nranks, comm->rank, &rb, &re) != SYLV_OK)
         throw Status{SYLV_E_INVALID, "cannot partition the grid over this many ranks"};
       comm->gather_ranges(rb, re);                                    // collective
-      const int64_t unit = (A->kind == SYLV_OP_STENCIL3D) ? (int64_t)A->grid[0] * A->grid[0] : A->grid[0];
+      const bool csr = A->kind == SYLV_OP_CSR;
+      const int64_t unit = (A->kind == SYLV_OP_STENCIL3D) ? (int64_t)A->grid[0] * A->grid[0]
+                           : csr ? 32 : A->grid[0];
       for (int q = 0; q < comm->nranks; ++q) {
         const int64_t b = comm->rb[q], e = comm->re[q];
         if ((q == 0 && b != 0) || (q > 0 && b != comm->re[q - 1]) || (q == comm->nranks - 1 && e != A->n))
           throw Status{SYLV_E_INVALID, "row ranges must tile [0, n) in rank order"};
-        if (e <= b || b % unit || e % unit || b % 32)
+        if (e <= b || b % unit || (e % unit && e != A->n) || b % 32)
           throw Status{SYLV_E_INVALID, "row ranges must be whole, non-empty sets of grid planes (3-D) / lines (2-D) "
-                                       "starting at multiples of 32"};
+                                       "starting at multiples of 32 (CSR: multiples of 32 rows)"};
       }
       c->comm = comm;
       c->row_begin = rb;

@@ -316,17 +316,18 @@ __global__ void __launch_bounds__(kThreads) k_pass1_csr(OpParams op, Win win, in
     // the first kCsrU nonzeros per lane: all value/index loads issued before the gathers
     // (rows of the BASELINE CSR have 21 nonzeros: <= 6 per lane); longer rows continue below
     constexpr int kCsrU = 6;
+    // (column indices of a row-sharded operator are local and may be negative: ghost rows)
     double av[kCsrU];
     int32_t cl[kCsrU];
 #pragma unroll
     for (int u = 0; u < kCsrU; ++u) {
       const int64_t p = p0 + sub + u * kCsrLanes;
       av[u] = p < p1 ? __ldg(op.cv + p) : 0.0;
-      cl[u] = p < p1 ? __ldg(op.ci + p) : -1;
+      cl[u] = p < p1 ? __ldg(op.ci + p) : 0;
     }
 #pragma unroll
     for (int u = 0; u < kCsrU; ++u)
-      if (cl[u] >= 0) gather(av[u], cl[u]);
+      if (p0 + sub + u * kCsrLanes < p1) gather(av[u], cl[u]);
     for (int64_t p = p0 + sub + kCsrU * kCsrLanes; p < p1; p += kCsrLanes) gather(__ldg(op.cv + p), __ldg(op.ci + p));
 #pragma unroll
     for (int c = 0; c < R; ++c) {

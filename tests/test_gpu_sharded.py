@@ -4,7 +4,8 @@ P virtual ranks of ONE process (sylv_local_group_create; one host thread per ran
 rank's kernels on its own streams, transports = plain device sums/copies ordered by CUDA
 events, no kernel waits on another) run the same code path as NCCL ranks: halo exchange of
 each new block's boundary planes/lines, allreduce of the Gram-Schmidt inner products and
-Grams, allreduce of the partial sketches (S hashed on GLOBAL rows).  The sharded run must
+Grams, allreduce of the partial sketches (S hashed on GLOBAL rows); CSR operators are split
+into 32-row-group ranges with band-wide ghost rows.  The sharded run must
 reproduce the unsharded GPU run up to reduction order (1e-10 relative on rho and on the
 basis blocks) and the CPU oracle to the parity tolerance (rho 1e-8 relative, d <= 50).
 The NCCL transport itself is exercised at world size 1 (one GPU per gpurun call).
@@ -39,6 +40,10 @@ CASES = {
     # pull sketch (sketch_pull.cuh) on shards: global group offsets m0 > 0 in the sorted lists
     "3d-r8k3-tma-P3-pull": (dict(kind="stencil3d", N=34, r=8, k=3, d_max=40), 3, True, "pull"),
     "2d-r4k2-P3-pull": (dict(kind="stencil2d", N=64, r=4, k=2, d_max=40), 3, True, "pull"),
+    # row-sharded CSR (c4's decomposition): ghost rows = band, global CSR on every rank
+    "csr-r2k2-P2": (dict(kind="csr", n=20011, nnz_off=20, band=300, r=2, k=2, d_max=40), 2, True),
+    "csr-r4k3-P3": (dict(kind="csr", n=9001, nnz_off=6, band=500, r=4, k=3, d_max=40), 3, True),
+    "csr-r1k2-P4": (dict(kind="csr", n=6007, nnz_off=6, band=100, r=1, k=2, d_max=40), 4, True),
 }
 NSTEPS = 16
 
@@ -114,8 +119,10 @@ def test_sharded_equals_unsharded(name, monkeypatch):
         # every rank reaches the same (replicated) projected quantities
         np.testing.assert_array_equal(sh["rho"], shards[0]["rho"])
         np.testing.assert_array_equal(sh["T"], shards[0]["T"])
+        # rho_rel is normalised by ||C1 C2^T||: the reduction-order rounding of the sharded
+        # sums is ~1e-16 of that scale, so below rho_rel ~ 1e-6 an absolute floor applies
         for d, (a, b) in enumerate(zip(sh["rho"], rho1), 1):
-            assert abs(a - b) <= 1e-10 * b, (name, d, a, b)
+            assert abs(a - b) <= 1e-10 * b + 1e-15, (name, d, a, b)
         assert _rel(sh["sk"], sk1) <= 1e-12
     for w in (0, 1):
         for i in range(cfg.k):
@@ -123,18 +130,22 @@ def test_sharded_equals_unsharded(name, monkeypatch):
             assert _rel(full, blocks1[w][i]) <= 1e-10, (name, w, i)
 
 
-def test_sharded_matches_oracle_and_solution():
-    kw, P, tma = CASES["3d-r8k3-tma-P3"]
+@pytest.mark.parametrize("name", ["3d-r8k3-tma-P3", "csr-r2k2-P2"])
+def test_sharded_matches_oracle_and_solution(name):
+    kw, P, tma = CASES[name][:3]
     cfg = inputs.small_config(**kw)
     C1, C2 = inputs.make_rhs(cfg)
-    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2)
+    csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
+    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2, csr_pair=csr)
     ro = []
     for d in range(1, NSTEPS + 1):
         orc.step(1)
         ro.append(orc.residual(d).rho_rel)
     shards = _sharded(cfg, C1, C2, P, tma, NSTEPS, solution_rank=48)
+    # the parity rule of test_gpu_parity._rho_close: 1e-8 relative while rho_rel >= 1e-9
+    # (three decades below tol), rounding-noise floor 1e-12 below that
     for d, (a, b) in enumerate(zip(shards[0]["rho"], ro), 1):
-        assert abs(a - b) <= 1e-8 * b, (d, a, b)
+        assert abs(a - b) <= (1e-8 * b if b >= 1e-9 else 1e-12), (d, a, b)
     # the factored solution, assembled from the ranks' rows, equals the unsharded one
     g = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(),
                            stream=torch.cuda.current_stream().cuda_stream)

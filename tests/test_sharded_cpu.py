@@ -1,10 +1,12 @@
 """The row-sharded decomposition of SURVEY §8(e) on CPU: world size 2 and 3 with gloo.
 
-Each rank holds only its z-slab of every basis block (rows from the library's own host
-partition function, sylv_partition), and emulates in NumPy exactly the exchange steps the
-sharded CUDA path performs (engine.cu / comm.cuh):
-  * halo: the ghost planes of the newest block come from the neighbour ranks (send/recv),
-    and the stencil rows of the slab are applied to [ghost_lo; Z_loc; ghost_hi];
+Each rank holds only its z-slab (3-D stencil) or row range (CSR, c4's decomposition) of every
+basis block (rows from the library's own host partition function, sylv_partition), and
+emulates in NumPy exactly the exchange steps the sharded CUDA path performs (engine.cu /
+comm.cuh):
+  * halo: the ghost planes (stencil: N^2 rows; CSR: band = max |col - row| rows) of the
+    newest block come from the neighbour ranks (send/recv), and the operator rows of the
+    slab are applied to [ghost_lo; Z_loc; ghost_hi];
   * Gram-Schmidt inner products and the Gram of W' are allreduced (sum), the r x r
     normalisation (CholQR) is then identical on every rank;
   * the partial sketch S[:, rows_loc] W_loc uses GLOBAL row indices and is allreduced
@@ -26,8 +28,21 @@ import torch.multiprocessing as mp  # noqa: E402
 from oracle import alg1, operators, sparse_sign  # noqa: E402
 from synth import inputs  # noqa: E402
 
-CFG = dict(kind="stencil3d", N=12, r=2, k=2, d_max=12)
+CFGS = {
+    "stencil3d": dict(kind="stencil3d", N=12, r=2, k=2, d_max=12),
+    # row-sharded CSR (c4's decomposition): halo width = the band max |col - row|
+    "csr": dict(kind="csr", n=3001, nnz_off=6, band=200, r=2, k=2, d_max=12),
+}
 NSTEPS = 8
+
+
+def _halo_width(cfg, M):
+    if cfg.kind == "stencil3d":
+        return cfg.N * cfg.N
+    if cfg.kind == "stencil2d":
+        return cfg.N
+    coo = M.tocoo()
+    return int(np.abs(coo.col - coo.row).max())
 
 
 def _free_port():
@@ -129,18 +144,17 @@ class ShardedSequence:
         return Hb
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, kind):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2311_16019_b200 as pkg
-        cfg = inputs.small_config(**CFG)
+        cfg = inputs.small_config(**CFGS[kind])
         rows = pkg.partition(cfg, world, rank)               # the library's host partition
-        plane = cfg.N * cfg.N
         A, Bt, _ = operators.operator_pair(cfg)
         C1, C2 = inputs.make_rhs(cfg)
-        U = ShardedSequence(A, C1, rows, plane, cfg.seed_u, cfg, rank, world)
-        V = ShardedSequence(Bt, C2, rows, plane, cfg.seed_v, cfg, rank, world)
+        U = ShardedSequence(A, C1, rows, _halo_width(cfg, A), cfg.seed_u, cfg, rank, world)
+        V = ShardedSequence(Bt, C2, rows, _halo_width(cfg, Bt), cfg.seed_v, cfg, rank, world)
         for _ in range(NSTEPS):
             U.step()
             V.step()
@@ -149,19 +163,19 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_decomposition_matches_oracle(world):
+@pytest.mark.parametrize("kind,world", [("stencil3d", 2), ("stencil3d", 3), ("csr", 2), ("csr", 3)])
+def test_sharded_decomposition_matches_oracle(kind, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, kind)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    cfg = inputs.small_config(**CFG)
+    cfg = inputs.small_config(**CFGS[kind])
     orc = alg1.SylvesterSketchedKrylov.from_config(cfg)
     orc.step(NSTEPS)
     res.sort()
