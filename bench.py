@@ -212,7 +212,7 @@ def main():
     # SYLV_BENCH_REPLICAS=1 runs independent replicas instead (weak scaling).
     csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
     C1, C2 = inputs.make_rhs(cfg)
-    sharded = ws > 1 and not os.environ.get("SYLV_BENCH_REPLICAS") and cfg.kind.startswith("stencil")
+    sharded = ws > 1 and not os.environ.get("SYLV_BENCH_REPLICAS")
     shard_kw = {}
     if sharded:
         comm = pkg.nccl_comm()
@@ -344,7 +344,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": _workload_desc(cfg), "d_range": [args.warmup + 1, args.warmup + args.steps],
-                       "parallelism": (f"row-sharded z-slabs x{ws} (NCCL halo + allreduce)" if sharded
+                       "parallelism": ((f"row-sharded z-slabs x{ws} (NCCL halo + allreduce)" if cfg.kind.startswith("stencil")
+                                        else f"row-sharded 32-row-group ranges x{ws} (NCCL band halo + allreduce)") if sharded
                                        else "replicas" if ws > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (window of k+1 blocks per sequence >> 126 MB)"
                        if 8 * cfg.n * cfg.r * (cfg.k + 1) > 126e6 else "working set may be L2-resident"},
