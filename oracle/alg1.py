@@ -264,15 +264,39 @@ class SolveResult:
     solve_seconds: float
 
 
+def _predict_crossing(d1: int, r1: float, d2: int, r2: float, tol: float) -> float:
+    """Log-linear extrapolation of rho_rel through (d1, r1), (d2, r2) to rho_rel = tol."""
+    if not (r1 > r2 > 0) or not math.isfinite(r1) or d2 <= d1:
+        return math.nan
+    slope = (math.log(r2) - math.log(r1)) / (d2 - d1)
+    return d2 + (math.log(tol) - math.log(r2)) / slope
+
+
 def solve(obj: SylvesterSketchedKrylov, tol: float, d_max: int, keep_Y=True) -> SolveResult:
-    """Step + scheduled checks + bisection (R9).  d* = smallest d in the bisection
-    bracket with rho_rel < tol (strict).  Breakdown: solve at the current d (R11)."""
+    """Step + scheduled checks + search for the first crossing (R9).  d* = smallest d in the
+    final bracket with rho_rel < tol (strict).  Breakdown: solve at the current d (R11).
+
+    Schedule: check_schedule(); past its every-10 regime, when the log-linear extrapolation of
+    the last two valid checks puts the crossing d_hat before the next scheduled check, the
+    next check is at max(d_last + 1, ceil(d_hat) + 2) instead.  Search on the bracket
+    (d_fail, d_pass]: regula falsi on log rho_rel (x = lo + (log r_lo - log tol) /
+    (log r_lo - log r_hi) (hi - lo), checked at ceil(x) clamped into the bracket), a bisection
+    step after two steps that did not halve the bracket; a check that fails numerically
+    (singular) is replaced by the nearest d in the bracket (mid, mid+1, mid-1, mid+2, ...).
+    With rho_rel monotone on the bracket, every such search returns the bisection's d*."""
     sched = check_schedule(obj.r, d_max)
     hist: List[CheckResult] = []
+    seen: List[Tuple[int, float]] = []
     t_step = t_solve = 0.0
     d_fail, passing = 0, None
     skips = 0
-    for dc in sched:
+    for idx in range(len(sched)):
+        if len(seen) >= 2 and sched[idx] * obj.r > 800:
+            (d1, r1), (d2, r2) = seen[-2], seen[-1]
+            dh = _predict_crossing(d1, r1, d2, r2, tol)
+            if math.isfinite(dh) and dh + 2 < sched[idx]:
+                sched[idx] = max(d2 + 1, math.ceil(dh) + 2)
+        dc = sched[idx]
         t0 = time.perf_counter()
         while obj.d < dc and not obj.breakdown:
             obj.step()
@@ -287,6 +311,8 @@ def solve(obj: SylvesterSketchedKrylov, tol: float, d_max: int, keep_Y=True) -> 
                 break
             continue
         skips = 0
+        if math.isfinite(res.rho_rel):
+            seen.append((dc, res.rho_rel))
         if res.rho_rel < tol or obj.breakdown:
             passing = res
             break
@@ -295,18 +321,36 @@ def solve(obj: SylvesterSketchedKrylov, tol: float, d_max: int, keep_Y=True) -> 
         last = next((h for h in reversed(hist) if not h.singular), None)
         return SolveResult(obj.d, last.rho_rel if last else math.nan, False, hist,
                            last.Y if last else None, t_step, t_solve)
-    # bisection on (d_fail, d_c]
     lo, best = d_fail, passing
     hi = passing.d
+    r_lo = next((r for d, r in seen if d == lo), math.nan)
+    r_hi = passing.rho_rel
+    slow = 0
     while hi - lo > 1 and not obj.breakdown:
-        mid = (lo + hi) // 2
-        res = obj.residual(mid)
-        t_solve += res.seconds
-        hist.append(res)
-        if not res.singular and res.rho_rel < tol:
-            hi, best = mid, res
+        mid0 = (lo + hi) // 2
+        if slow < 2 and math.isfinite(r_lo) and math.isfinite(r_hi) and r_lo > r_hi > 0:
+            x = lo + (math.log(r_lo) - math.log(tol)) / (math.log(r_lo) - math.log(r_hi)) * (hi - lo)
+            mid0 = min(hi - 1, max(lo + 1, math.ceil(x)))
+        res = None
+        for t in range(8):
+            cand = mid0 + ((t + 1) // 2 if t % 2 else -(t // 2))
+            if cand <= lo or cand >= hi:
+                continue
+            r = obj.residual(cand)
+            t_solve += r.seconds
+            hist.append(r)
+            if not r.singular and math.isfinite(r.rho_rel):
+                res = r
+                break
+        width = hi - lo
+        if res is None:
+            lo, r_lo = mid0, math.nan
+            continue
+        if res.rho_rel < tol:
+            hi, r_hi, best = res.d, res.rho_rel, res
         else:
-            lo = mid
+            lo, r_lo = res.d, res.rho_rel
+        slow = slow + 1 if 2 * (hi - lo) > width else 0
     return SolveResult(best.d, best.rho_rel, True, hist, best.Y if keep_Y else None, t_step, t_solve)
 
 

@@ -1460,6 +1460,7 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
       c->stats.host_solves++;
       if (info < 0) return fail(c, SYLV_E_LAPACK, err);
       if (info > 0) {
+        c->hist.emplace_back(d, NAN);   // a failed check, kept in the history
         c->y_d = -1;
         if (rho) *rho = NAN;
         if (rho_rel) *rho_rel = NAN;
@@ -1617,7 +1618,23 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     return guard(c, [&]() -> sylv_status { return finish_steps(c, f, l); });
   };
   auto ok_step = [](sylv_status s) { return s == SYLV_OK || s == SYLV_E_BREAKDOWN || s == SYLV_E_NOT_CONVERGED; };
+  // valid checks so far (d, rho_rel): the crossing prediction below uses the last two
+  std::vector<std::pair<int, double>> seen;
+  auto predict = [&](int d1, double r1, int d2, double r2) -> double {   // log-linear crossing
+    if (!(r1 > r2) || !(r2 > 0) || !std::isfinite(r1) || d2 <= d1) return NAN;
+    const double slope = (std::log(r2) - std::log(r1)) / (d2 - d1);
+    return d2 + (std::log(c->tol) - std::log(r2)) / slope;
+  };
   for (size_t idx = 0; idx < sched.size(); ++idx) {
+    // past the every-10 regime: when the log-linear extrapolation of the last two checks puts
+    // the crossing well before the next scheduled check, check just past the prediction
+    // instead (same first crossing after the search below; fewer large projected solves)
+    if (seen.size() >= 2 && (int64_t)sched[idx] * c->R > 800) {
+      const auto& a = seen[seen.size() - 2];
+      const auto& b = seen.back();
+      const double dh = predict(a.first, a.second, b.first, b.second);
+      if (std::isfinite(dh) && dh + 2 < sched[idx]) sched[idx] = std::max(b.first + 1, (int)std::ceil(dh) + 2);
+    }
     const int dc = sched[idx];
     if (dc > c->dmax) break;
     if (c->d_done < dc && !c->broken) {
@@ -1657,6 +1674,7 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     }
     skips = 0;
     last_rr = rr;
+    if (std::isfinite(rr)) seen.emplace_back(dchk, rr);
     if (rr < c->tol || c->broken) {
       d_pass = dchk;
       rr_pass = rr;
@@ -1674,17 +1692,48 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     if (rho_rel) *rho_rel = last_rr;
     return fail(c, SYLV_E_NOT_CONVERGED, "tolerance not reached by d_max");
   }
+  // first crossing inside the bracket (d_fail, d_pass]: safeguarded regula falsi on
+  // log rho_rel (Illinois), a bisection step whenever the bracket does not halve; with
+  // rho_rel monotone on the bracket this returns the same d* as bisection
   int lo = d_fail, hi = d_pass;
+  double rlo = NAN, rhi = rr_pass;
+  for (const auto& e : seen)
+    if (e.first == lo) rlo = e.second;
+  int slow = 0;
   while (hi - lo > 1 && !pass_by_breakdown) {
-    const int mid = (lo + hi) / 2;
-    double rho, rr;
-    sylv_status s = sylv_sketch_residual(c, mid, &rho, &rr);
-    if (s == SYLV_OK && rr < c->tol) {
+    int mid0 = (lo + hi) / 2;
+    if (slow < 2 && std::isfinite(rlo) && std::isfinite(rhi) && rlo > rhi && rhi > 0) {
+      const double x = lo + (std::log(rlo) - std::log(c->tol)) / (std::log(rlo) - std::log(rhi)) * (hi - lo);
+      mid0 = std::min(hi - 1, std::max(lo + 1, (int)std::ceil(x)));
+    }
+    // a check that fails numerically (non-converged Schur iteration, non-finite projected
+    // matrix: ill-conditioned sketched basis) decides nothing: the nearest d inside the
+    // bracket with a valid check is used instead (mid, mid+1, mid-1, mid+2, ...)
+    int mid = -1;
+    double rho, rr = NAN;
+    for (int t = 0; t < 8; ++t) {
+      const int cand = mid0 + ((t & 1) ? (t + 1) / 2 : -(t / 2));
+      if (cand <= lo || cand >= hi) continue;
+      if (sylv_sketch_residual(c, cand, &rho, &rr) == SYLV_OK && std::isfinite(rr)) {
+        mid = cand;
+        break;
+      }
+    }
+    const int width = hi - lo;
+    if (mid < 0) {               // no valid check near the middle: keep the old rule
+      lo = mid0;
+      rlo = NAN;
+      continue;
+    }
+    if (rr < c->tol) {
       hi = mid;
+      rhi = rr;
       rr_pass = rr;
     } else {
       lo = mid;
+      rlo = rr;
     }
+    slow = (2 * (hi - lo) > width) ? slow + 1 : 0;
   }
   if (c->y_d != hi) {
     double rho, rr;

@@ -181,7 +181,9 @@ int sylvester_bs(int m, int r, std::vector<double>& MU, std::vector<double>& MV,
     return -2;
   }
   std::vector<double> ZU, ZV;
-  if (schur(m, MU, ZU, err) || schur(m, MV, ZV, err)) return -1;
+  // a Schur iteration that does not converge (badly scaled M of an ill-conditioned sketched
+  // basis) is a failed check at this d, not a missing library
+  if (schur(m, MU, ZU, err) || schur(m, MV, ZV, err)) return 1;
   // Ft = ZU^T F ZV = ZU[0:r,:]^T (B ZV[0:r,:])
   std::vector<double> Bc(r * r), tmp((size_t)r * m), F((size_t)m * m);
   for (int a = 0; a < r; ++a)

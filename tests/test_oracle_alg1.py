@@ -201,6 +201,59 @@ def test_check_schedule():
     assert alg1.check_schedule(8, 7) == [7]
 
 
+class _FakeRun:
+    """A stand-in for SylvesterSketchedKrylov with a prescribed rho_rel(d) (search logic only)."""
+
+    def __init__(self, rho, r=4, singular=()):
+        self.rho, self.r, self.d, self.breakdown = rho, r, 0, False
+        self.singular, self.calls = set(singular), []
+
+    def step(self):
+        self.d += 1
+
+    def residual(self, d):
+        self.calls.append(d)
+        if d in self.singular:
+            return alg1.CheckResult(d, math.nan, math.nan, None, True)
+        return alg1.CheckResult(d, self.rho(d), self.rho(d), None, False)
+
+
+@pytest.mark.parametrize("rate,r", [(0.985, 4), (0.97, 8), (0.991, 4), (0.9, 1)])
+def test_search_finds_the_first_crossing_of_a_monotone_rho(rate, r):
+    """R9 search (schedule + prediction + safeguarded regula falsi) on a strictly decreasing
+    rho_rel(d): d* is exactly the first d with rho_rel < tol (brute force), with no more
+    projected solves than the plain schedule + bisection would use."""
+    tol, d_max = 1e-6, 1500
+    rho = lambda d: 0.3 * rate ** d * (1 + 0.2 / (1 + d))   # strictly decreasing
+    first = next(d for d in range(1, d_max + 1) if rho(d) < tol)
+    fake = _FakeRun(rho, r=r)
+    res = alg1.solve(fake, tol, d_max, keep_Y=False)
+    assert res.converged and res.d_star == first
+    sched = alg1.check_schedule(r, d_max)
+    n_sched = next(i for i, d in enumerate(sched) if d >= first) + 1
+    lo = max([0] + [d for d in sched if d < first])
+    hi = min(d for d in sched if d >= first)
+    n_bisect = 0
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        lo, hi = (lo, mid) if rho(mid) < tol else (mid, hi)
+        n_bisect += 1
+    assert len(fake.calls) <= n_sched + n_bisect
+
+
+def test_search_is_a_valid_crossing_with_bumps_and_singular_checks():
+    """Non-monotone rho_rel (bumps near tol) and numerically failed checks: the returned d*
+    passes, the check just below it (if made) failed, and every failed check is skipped."""
+    tol = 1e-6
+    rho = lambda d: 2e-3 * 0.99 ** d * (1 + 0.05 * math.sin(d))
+    fake = _FakeRun(rho, r=4, singular={779, 780, 781, 800})
+    res = alg1.solve(fake, tol, 1500, keep_Y=False)
+    assert res.converged and rho(res.d_star) < tol and res.d_star not in fake.singular
+    below = [d for d in fake.calls if d < res.d_star and d not in fake.singular]
+    assert below and rho(max(below)) >= tol
+    assert max(below) == res.d_star - 1 or all(d not in fake.calls for d in range(max(below) + 1, res.d_star))
+
+
 def test_c0_regression_expectation():
     """Not a pin (parity unpinned for d* on the BJ configs): c0 converges near the
     survey-time expectation d* = 107 with a true residual of the same order."""
