@@ -236,6 +236,7 @@ struct sylv_ctx {
   bool y_dev = false;
   std::vector<double> Y;
   GpuSylv* gsolve = nullptr;    // device projected solver (created on first use)
+  int gpu_fail_d = 1 << 30;     // smallest d where the device solve fell back to the host
   std::vector<std::pair<int, double>> hist;
   sylv_stats stats{};
   std::vector<TimedPair> timed;
@@ -1029,7 +1030,9 @@ sylv_status guard(sylv_ctx* c, F&& f) {
 
 // Projected solve of check d on the device (sign iteration) or on the host (Bartels-Stewart)
 bool device_solve(const sylv_ctx* c, int d) {
-  return (c->cflags & 8) || (!(c->cflags & 16) && d * c->R >= 512);
+  // auto: device for d r >= 512, except at and beyond a d where it already fell back (the
+  // conditioning of the projected matrices only grows with d: c1 needs the host there)
+  return (c->cflags & 8) || (!(c->cflags & 16) && d * c->R >= 512 && d < c->gpu_fail_d);
 }
 
 // Enqueue block steps first..last (Alg. 1 lines 3-9 for both sequences) and the flag
@@ -1431,11 +1434,13 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
           c->stats.gpu_solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         } else {
           c->stats.gpu_solve_fallbacks++;
+          c->gpu_fail_d = std::min(c->gpu_fail_d, d);
           c->err = "device projected solve did not converge at d = " + std::to_string(d) + " (" +
                    std::to_string(c->gsolve->iterations) + " iterations); host fallback";
         }
       } catch (const ProjError& e) {
         c->stats.gpu_solve_fallbacks++;
+        c->gpu_fail_d = std::min(c->gpu_fail_d, d);
         c->err = "device projected solve failed at d = " + std::to_string(d) + ": " + e.what + "; host fallback";
         cudaGetLastError();
       }
