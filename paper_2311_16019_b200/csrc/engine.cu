@@ -647,11 +647,9 @@ void launch_sketch(sylv_ctx* c, Sequence& q, const double* X, int R, const doubl
     SYLV_DISPATCH_R(R, {
       k_sketch_pull<R_><<<(nw + kPullWarps - 1) / kPullWarps, kPullWarps * 32, 0, st>>>(
           c->n, X, q.ld, q.sp, q.pl_list, q.pl_off, q.pl_wpb, q.pl_bpw, q.pl_strips);
-      k_sketch_pull_fold<R_><<<(int)std::min<int64_t>(4 * c->sm, (q.s * R + 255) / 256), 256, 0, st>>>(
-          q.pl_strips, q.sp, q.pl_wpb, q.pl_bpw, q.skpart);
-      k_sketch_reduce<R_><<<red_grid, 256, 0, st>>>(q.skpart, 1, q.s, M, w);
+      k_sketch_pull_fold_apply<R_><<<red_grid, 256, 0, st>>>(q.pl_strips, q.sp, q.pl_wpb, q.pl_bpw, M, w);
     });
-    count(c, 3);
+    count(c, 2);
     return;
   }
   const dim3 g(c->nchunk, R);

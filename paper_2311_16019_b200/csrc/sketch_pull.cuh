@@ -11,8 +11,8 @@
 // x[32m + π⁻¹(j)] for all R columns — one coalesced 256-byte segment per column, permuted across
 // lanes — and accumulates in registers while the base is unchanged (≈ n/(32 b) groups share a
 // base).  Only on a base change is the register window added into the warp's private strip of
-// bpw + 31 slots (bpw <= kPullBpwMax bases per warp, chosen at init so the grid fills the GPU).  A fold kernel adds the ≤ 6 strips covering each slot in a fixed
-// order.  Every summation order is fixed by the stable sort: results are deterministic.
+// bpw + 31 slots (bpw <= kPullBpwMax bases per warp, chosen at init so the grid fills the GPU).  A fold kernel adds the strips covering each slot in a fixed order
+// and applies the r x r factor.  Every summation order is fixed by the stable sort: results are deterministic.
 //
 // Cost per (group, bucket, column): one 256-B L2 read (W is read from HBM once per chunk and
 // ζ times from L2) instead of a shared-memory read-modify-write chain.
@@ -187,28 +187,44 @@ __global__ void __launch_bounds__(kPullWarps * 32, pull_min_blocks<R>()) k_sketc
   for (int i = lane; i < R * kPullS; i += 32) out[i] = st[i];
 }
 
-// partial[c * s + t * b + p] = scale * Σ strips covering slot p of bucket t (fixed order).
-// Needs b >= bpw + 31 so a strip never covers a slot twice (b >= 64 is required at init).
+// Fold and right-multiply: w[q*R + c] = sum_a (scale * sum of the strips covering slot q of its
+// bucket, column a) M[a*R + c]  (M = nullptr: identity).  The strips covering slot p are those
+// of the warps whose bases q0 .. q0+bpw-1 reach it (slots q0 .. q0+bpw+30 mod b; zero past the
+// warp's own bases + 30), summed nearest first — a fixed order.  Needs b >= bpw + 31 so a
+// strip never covers a slot twice (b >= 64 is required at init).
 template <int R>
-__global__ void k_sketch_pull_fold(const double* __restrict__ strips, SketchParams sp, uint32_t wpb,
-                                   uint32_t bpw, double* __restrict__ partial) {
+__global__ void k_sketch_pull_fold_apply(const double* __restrict__ strips, SketchParams sp, uint32_t wpb,
+                                         uint32_t bpw, const double* __restrict__ M, double* __restrict__ w) {
   const uint32_t b = sp.b;
   const int64_t s = (int64_t)b * sp.zeta;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < s * R; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(idx / s);
-    const int64_t q = idx - (int64_t)c * s;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < s; q += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t t = (uint32_t)(q / b), p = (uint32_t)(q - (int64_t)t * b);
     const uint32_t wl = pull_owner(p, b, wpb);
-    double sum = 0.0;
-    // warps whose strip (slots q0 .. q0 + bpw + 30 mod b; zero past the warp's own bases + 30)
-    // covers p, nearest first; the distance (p - q0) mod b grows with k
+    double v[R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) v[a] = 0.0;
     for (uint32_t k = 0; k < wpb; ++k) {
-      const uint32_t w = (wl + wpb - k) % wpb;
-      const uint32_t dd = (p + b - pull_q0(w, b, wpb)) % b;
+      const uint32_t wq = (wl + wpb - k) % wpb;
+      const uint32_t dd = (p + b - pull_q0(wq, b, wpb)) % b;
       if (dd >= bpw + 31u) break;
-      sum += strips[((size_t)(t * wpb + w) * R + c) * kPullS + dd];
+      const double* st = strips + (size_t)(t * wpb + wq) * R * kPullS + dd;
+#pragma unroll
+      for (int a = 0; a < R; ++a) v[a] += st[a * kPullS];
     }
-    partial[idx] = sum * sp.scale;
+#pragma unroll
+    for (int a = 0; a < R; ++a) v[a] *= sp.scale;
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      double o;
+      if (M) {
+        o = 0.0;
+#pragma unroll
+        for (int a = 0; a < R; ++a) o = fma(v[a], __ldg(M + a * R + c), o);
+      } else {
+        o = v[c];
+      }
+      w[q * R + c] = o;
+    }
   }
 }
 

@@ -98,6 +98,61 @@ __global__ void __launch_bounds__(kSmallThreads) k_coef1(const double* __restric
   }
 }
 
+// Warp-cooperative Cholesky G = U^T U (upper, positive diagonal) and V = U^{-1}, R <= 8, run by
+// one full warp: lane j < R keeps column j of U in registers; row k of U needs the column-k
+// entries above it, broadcast by shuffles (R^2/2 shuffles, no serial thread-0 loops).  U, V:
+// R x R row-major in shared memory.  Returns false (on every lane) when G is not positive
+// definite; U = V = I then.
+template <int R>
+__device__ __forceinline__ bool warp_chol_inv(const double* G, double* U, double* V) {
+  const int lane = threadIdx.x & 31;
+  const int jj = lane < R ? lane : 0;
+  double u[R];
+#pragma unroll
+  for (int p = 0; p < R; ++p) u[p] = 0.0;
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    double t = G[k * R + jj];
+#pragma unroll
+    for (int p = 0; p < k; ++p) t -= __shfl_sync(SYLV_FULL_MASK, u[p], k) * u[p];   // U[p][k] U[p][j]
+    const double dk = __shfl_sync(SYLV_FULL_MASK, t, k);
+    if (!(dk > 0.0)) ok = false;                       // warp-uniform
+    const double d = ok ? sqrt(dk) : 1.0;
+    u[k] = (jj == k) ? d : (jj > k ? t / d : 0.0);
+  }
+  if (!ok) {
+#pragma unroll
+    for (int p = 0; p < R; ++p) u[p] = (p == jj) ? 1.0 : 0.0;
+  }
+  if (lane < R)
+#pragma unroll
+    for (int p = 0; p < R; ++p) U[p * R + lane] = u[p];
+  __syncwarp();
+  // column j of V by back substitution: V[j][j] = 1/U[j][j], V[i][j] = -sum_{p=i+1..j} U[i][p] V[p][j] / U[i][i]
+  if (lane < R) {
+    double v[R];
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      double val = 0.0;
+      if (i == lane) {
+        val = 1.0 / U[i * R + i];
+      } else if (i < lane) {
+        double s = 0.0;
+#pragma unroll
+        for (int p = i + 1; p < R; ++p)
+          if (p <= lane) s += U[i * R + p] * v[p];
+        val = -s / U[i * R + i];
+      }
+      v[i] = val;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) V[i * R + lane] = v[i];
+  }
+  __syncwarp();
+  return ok;
+}
+
 // G = W'^T W' -> h_{j+1,j} = chol(G) (upper, positive diagonal), R_{j+1} = h^{-1};
 // breakdown flag (bit 0) if min diag h <= 1e-14 ||W~||_F  (R11), with
 // ||W~||_F^2 = ||W'||_F^2 + sum_i ||h_{i,j}||_F^2 (window orthonormal); bit 1 if G not PD.
@@ -105,17 +160,21 @@ template <int R, int K>
 __global__ void __launch_bounds__(kSmallThreads) k_coef2(const double* __restrict__ partial, int nparts, int j,
                         double* __restrict__ Rall, double* __restrict__ Hc,
                         const double* __restrict__ hnorm2, int* __restrict__ flags) {
-  __shared__ double G[R * R];
+  __shared__ double G[R * R], h[R * R], hi[R * R];
   block_sum_parts(partial, nparts, R * R, R * R, G);
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  double h[R * R], hi[R * R];
-  int fl = 0;
-  if (!chol_upper<R>(G, h)) {
-    fl |= 2;
-    for (int e = 0; e < R * R; ++e) h[e] = (e % (R + 1) == 0) ? 1.0 : 0.0;
+  if (threadIdx.x >= 32) return;
+  const bool ok = warp_chol_inv<R>(G, h, hi);
+  if (threadIdx.x != 0) {
+    double* Hout = Hc + (int64_t)j * (K + 1) * R * R + K * R * R;
+    double* Rn = Rall + (int64_t)(j + 1) * R * R;
+    for (int e = threadIdx.x - 1; e < R * R; e += 31) {
+      Hout[e] = h[e];
+      Rn[e] = hi[e];
+    }
+    return;
   }
-  inv_upper<R>(h, hi);
+  int fl = ok ? 0 : 2;
   double tr = 0.0, mind = 1e300;
   for (int a = 0; a < R; ++a) {
     tr += G[a * R + a];
@@ -123,12 +182,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_coef2(const double* __restric
   }
   const double wn = sqrt(tr + hnorm2[j]);
   if (mind <= 1e-14 * wn) fl |= 1;
-  double* Hout = Hc + (int64_t)j * (K + 1) * R * R + K * R * R;
-  double* Rn = Rall + (int64_t)(j + 1) * R * R;
-  for (int e = 0; e < R * R; ++e) {
-    Hout[e] = h[e];
-    Rn[e] = hi[e];
-  }
   if (fl) atomicOr(flags + j, fl);
 }
 
@@ -138,23 +191,22 @@ template <int R>
 __global__ void __launch_bounds__(kSmallThreads) k_chol_small(const double* __restrict__ partial, int nparts,
                              double* __restrict__ tau_out, double* __restrict__ tinv_out,
                              const double* __restrict__ prev, int* __restrict__ flags, int slot) {
-  __shared__ double G[R * R];
+  __shared__ double G[R * R], t[R * R], ti[R * R];
   block_sum_parts(partial, nparts, R * R, R * R, G);
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  double t[R * R], ti[R * R];
-  if (!chol_upper<R>(G, t)) {
-    atomicOr(flags + slot, 4);
-    for (int e = 0; e < R * R; ++e) t[e] = (e % (R + 1) == 0) ? 1.0 : 0.0;
-  }
-  inv_upper<R>(t, ti);
-  for (int e = 0; e < R * R; ++e) tinv_out[e] = ti[e];
-  if (prev) {
-    double tp[R * R];
-    mm<R>(t, prev, tp);
-    for (int e = 0; e < R * R; ++e) tau_out[e] = tp[e];
-  } else {
-    for (int e = 0; e < R * R; ++e) tau_out[e] = t[e];
+  if (threadIdx.x >= 32) return;
+  const bool ok = warp_chol_inv<R>(G, t, ti);
+  if (!ok && threadIdx.x == 0) atomicOr(flags + slot, 4);
+  for (int e = threadIdx.x; e < R * R; e += 32) {
+    tinv_out[e] = ti[e];
+    if (prev) {
+      const int a = e / R, c = e % R;
+      double sacc = 0.0;
+      for (int p = 0; p < R; ++p) sacc += t[a * R + p] * prev[p * R + c];   // (t prev)[a][c]
+      tau_out[e] = sacc;
+    } else {
+      tau_out[e] = t[e];
+    }
   }
 }
 
