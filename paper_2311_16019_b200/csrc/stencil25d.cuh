@@ -141,7 +141,7 @@ __device__ __forceinline__ void issue_plane(const Tma25& tm, int nwin, double* s
 template <int TY, int R, int K, int PASS, bool GRAM>
 __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
     k_st3d(const __grid_constant__ Tma25 tm, St25 p, int nwin, const double* __restrict__ coef,
-           double* __restrict__ Wout, double* __restrict__ partial) {
+           double* __restrict__ Wout, double* __restrict__ partial, int slot0 = -1) {
   static_assert(R == 4 || R == 8, "R = 4 or 8");
   constexpr int kNS = stages25<R>();
   using Gm = Geo25<TY, R>;
@@ -342,12 +342,16 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       red[warp][i * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc[i][1] + acc2[i][1];
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < NA * R * R; e += blockDim.x) {
+    // slot0 >= 0 (pass 1 with nwin = 1 after the fused pass, stencil25d_fused.cuh): only
+    // P_{j} = Z_j^T A Z_j, written to slot slot0 of the K-slot record; the other slots hold the
+    // fused pass's P and are left alone
+    const int ne = slot0 >= 0 ? R * R : NA * R * R;
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
       const int i = e / (R * R), a = (e / R) % R, c = e % R;      // R x R blocks of the 8 x 8 D
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < TY; ++w) s += red[w][i * 64 + a * 8 + c];
-      partial[(int64_t)blockIdx.x * NA * R * R + e] = s;
+      partial[(int64_t)blockIdx.x * NA * R * R + (slot0 >= 0 ? slot0 * R * R + e : e)] = s;
     }
   }
 }
