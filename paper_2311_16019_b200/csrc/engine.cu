@@ -513,6 +513,7 @@ void setup_tma(sylv_ctx* c, Sequence& q) {
   if (const char* e = std::getenv("SYLV_G25MUL")) gmul = std::max(1, std::atoi(e));   // tuning
   const int grid = gmul * c->sm;
   int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, nz / 16), (8 * grid + tiles - 1) / tiles));
+  if (const char* e = std::getenv("SYLV_NSEG")) nseg = std::max(1, std::min(nz, std::atoi(e)));   // tuning
   p.zseg = (nz + nseg - 1) / nseg;
   p.nseg = (nz + p.zseg - 1) / p.zseg;
   p.items = tiles * p.nseg;
@@ -1779,6 +1780,17 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
   // first crossing inside the bracket (d_fail, d_pass]: safeguarded regula falsi on
   // log rho_rel (Illinois), a bisection step whenever the bracket does not halve; with
   // rho_rel monotone on the bracket this returns the same d* as bisection
+  // the projected solution of the best passing check so far (host-solved checks), so the
+  // final d* need not be solved again (c1: one m ~ 3100 solve ~ 12 s)
+  std::vector<double> best_Y;
+  int best_d = -1;
+  auto keep_if_pass = [&](int d) {
+    if (c->y_d == d && !c->y_dev) {
+      best_Y = c->Y;
+      best_d = d;
+    }
+  };
+  keep_if_pass(d_pass);
   int lo = d_fail, hi = d_pass;
   double rlo = NAN, rhi = rr_pass;
   for (const auto& e : seen)
@@ -1813,6 +1825,7 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
       hi = mid;
       rhi = rr;
       rr_pass = rr;
+      keep_if_pass(mid);
     } else {
       lo = mid;
       rlo = rr;
@@ -1820,8 +1833,14 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     slow = (2 * (hi - lo) > width) ? slow + 1 : 0;
   }
   if (c->y_d != hi) {
-    double rho, rr;
-    sylv_sketch_residual(c, hi, &rho, &rr);
+    if (best_d == hi) {                 // restore the kept solution of d*
+      c->Y.swap(best_Y);
+      c->y_d = hi;
+      c->y_dev = false;
+    } else {
+      double rho, rr;
+      sylv_sketch_residual(c, hi, &rho, &rr);
+    }
   }
   if (d_star) *d_star = hi;
   if (rho_rel) *rho_rel = rr_pass;
