@@ -34,6 +34,7 @@ CASES = {
     "3d-r8k4-tma": dict(kind="stencil3d", N=26, r=8, k=4, d_max=55),
     "3d-r4k2-tma": dict(kind="stencil3d", N=34, r=4, k=2, d_max=55),
     "3d-r4k3-tma": dict(kind="stencil3d", N=20, r=4, k=3, d_max=55),
+    "3d-r4k4-tma": dict(kind="stencil3d", N=18, r=4, k=4, d_max=55),
     "3d-r2k1": dict(kind="stencil3d", N=11, r=2, k=1, d_max=55),
     "csr-r2": dict(kind="csr", n=20011, nnz_off=20, band=300, r=2, k=2, d_max=55),
     "csr-r4k4": dict(kind="csr", n=5003, nnz_off=6, band=40, r=4, k=4, d_max=55),
@@ -203,11 +204,18 @@ def test_sketch_full_config_sizes(name):
     gpu.close()
 
 
-@pytest.mark.parametrize("name", ["3d-r8k3-tma", "3d-r8k4-tma", "3d-r4k2-tma", "3d-r4k3-tma"])
+# k = 1 (orthogonalise against the newest block only): the recurrence loses conditioning within
+# ~40 steps at r = 8, so it is checked against the generic passes over 20 steps, not in the
+# 50-step oracle parity window
+TMA_ONLY = {"3d-r8k1-tma": dict(kind="stencil3d", N=22, r=8, k=1, d_max=55)}
+
+
+@pytest.mark.parametrize("name", ["3d-r8k3-tma", "3d-r8k4-tma", "3d-r4k2-tma", "3d-r4k3-tma", "3d-r4k4-tma",
+                                  "3d-r8k1-tma"])
 def test_tma_passes_match_generic_passes(name):
     """The 2.5-D TMA passes and the generic DMMA passes compute the same recurrence: window
     blocks and per-step rho agree to rounding (1e-12 relative) over 20 steps."""
-    cfg = inputs.small_config(**CASES[name])
+    cfg = inputs.small_config(**{**CASES, **TMA_ONLY}[name])
     C1, C2 = inputs.make_rhs(cfg)
     st = torch.cuda.current_stream().cuda_stream
     a = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), stream=st)
