@@ -1132,7 +1132,8 @@ void enqueue_steps(sylv_ctx* c, int first, int last) {
   // pull sketch (sketch_pull.cuh) must not share L2 with a streaming pass — then each
   // sequence's sketch-space QR on its side stream, overlapping the next step's passes.
   // Push sketch (small n): sketch + QR on the side streams, overlapping the next passes.
-  const bool on_side = !c->seq[0].pl_list;
+  const char* sched_env = std::getenv("SYLV_SCHED");   // "overlap" | "phase" (tuning)
+  const bool on_side = sched_env ? std::strcmp(sched_env, "overlap") == 0 : !c->seq[0].pl_list;
   for (int j = first; j <= last; ++j) {
     if (serial) {
       step_passes(c, c->seq[0], j, c->st, false);
