@@ -280,7 +280,8 @@ def solve(obj: SylvesterSketchedKrylov, tol: float, d_max: int, keep_Y=True) -> 
     the last two valid checks puts the crossing d_hat before the next scheduled check, the
     next check is at max(d_last + 1, ceil(d_hat) + 2) instead.  Search on the bracket
     (d_fail, d_pass]: regula falsi on log rho_rel (x = lo + (log r_lo - log tol) /
-    (log r_lo - log r_hi) (hi - lo), checked at ceil(x) clamped into the bracket), a bisection
+    (log r_lo - log r_hi) (hi - lo), checked at ceil(x) clamped into the bracket, or at hi - 1 when
+that is within 2 of hi), a bisection
     step after two steps that did not halve the bracket; a check that fails numerically
     (singular) is replaced by the nearest d in the bracket (mid, mid+1, mid-1, mid+2, ...).
     With rho_rel monotone on the bracket, every such search returns the bisection's d*."""
@@ -331,6 +332,8 @@ def solve(obj: SylvesterSketchedKrylov, tol: float, d_max: int, keep_Y=True) -> 
         if slow < 2 and math.isfinite(r_lo) and math.isfinite(r_hi) and r_lo > r_hi > 0:
             x = lo + (math.log(r_lo) - math.log(tol)) / (math.log(r_lo) - math.log(r_hi)) * (hi - lo)
             mid0 = min(hi - 1, max(lo + 1, math.ceil(x)))
+            if hi - mid0 <= 2:               # crossing predicted just below hi: settle it at once
+                mid0 = hi - 1
         res = None
         for t in range(8):
             cand = mid0 + ((t + 1) // 2 if t % 2 else -(t // 2))

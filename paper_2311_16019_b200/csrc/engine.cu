@@ -1802,6 +1802,7 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     if (slow < 2 && std::isfinite(rlo) && std::isfinite(rhi) && rlo > rhi && rhi > 0) {
       const double x = lo + (std::log(rlo) - std::log(c->tol)) / (std::log(rlo) - std::log(rhi)) * (hi - lo);
       mid0 = std::min(hi - 1, std::max(lo + 1, (int)std::ceil(x)));
+      if (hi - mid0 <= 2) mid0 = hi - 1;   // crossing predicted just below hi: settle it at once
     }
     // a check that fails numerically (non-converged Schur iteration, non-finite projected
     // matrix: ill-conditioned sketched basis) decides nothing: the nearest d inside the
