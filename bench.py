@@ -17,7 +17,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -68,48 +67,75 @@ def algorithmic_bytes(cfg, n=None):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi clocks / throttle reasons every 200 ms around and during the timed region:
+    one looping nvidia-smi process (the profiling recipe's clocks line), started before the
+    region — spawning a process per sample stalls kernel launches of short runs — and
+    stopped after it."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index=0):
         self.index = index
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
+        self._p = None
+        self.t0 = self.t1 = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def region(self, start: bool):
+        """Mark the start / end of the timed region (wall clock)."""
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "200"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)                       # spawn + first sample before the timed region
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
+        if self._p is None:
+            return
+        time.sleep(0.25)                          # one more sample after the region
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=5)
+        except Exception:
+            self._p.kill()
+            out = ""
+        for line in (out or "").splitlines():
+            if line.strip():
+                self.rows.append([x.strip() for x in line.split(",")])
 
     def summary(self):
-        if not self.rows:
+        import datetime
+        rows = []
+        for r in self.rows:
+            try:
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except Exception:
+                continue
+            rows.append((ts, r[1:]))
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        # samples inside the timed region (+-0.2 s); a region shorter than the 200 ms sampling
+        # period gets the sample nearest to it
+        t0, t1 = self.t0 or rows[0][0], self.t1 or rows[-1][0]
+        inside = [v for ts, v in rows if t0 - 0.2 <= ts <= t1 + 0.2]
+        if not inside:
+            inside = [min(rows, key=lambda tv: min(abs(tv[0] - t0), abs(tv[0] - t1)))[1]]
+        sm = [float(r[0]) for r in inside if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in inside if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        reasons = sorted({names[i] for r in inside for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(inside), "samples_total": len(rows),
+                "how": "one looping nvidia-smi (-lms 200) started before and stopped after the timed region"}
 
 
 def dist_env():
@@ -245,10 +271,12 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
+        clk.region(True)
         e0.record(stream)
         d_done, st = solver.step(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.region(False)
         barrier()
     ms = e0.elapsed_time(e1)
     stats = attr_stats
