@@ -346,6 +346,21 @@ def main():
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         st3 = s3.stats()
+        # a7, timed separately: the second pass (replay of the basis with the stored
+        # coefficients, Y ~ Y1 Y2^T truncated to at most 32 columns) into device buffers
+        sec = None
+        if st_star == 0:
+            mr = 32
+            X1o = torch.empty((C1.shape[0], mr), dtype=torch.float64, device=dev)
+            X2o = torch.empty((C1.shape[0], mr), dtype=torch.float64, device=dev)
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            _, _, rk = s3.solution(d_star, mr, X1o, X2o)
+            torch.cuda.synchronize()
+            sec = {"seconds": time.perf_counter() - t2, "rank": rk, "max_rank": mr,
+                   "what": "sylv_sketch_solution(d*): SVD truncation of Y + replay of d* block steps per "
+                           "sequence (pass 2 with stored coefficients) + X accumulation, device outputs"}
+            del X1o, X2o
         s3.close()
         if ws > 1:
             t = torch.tensor([el], device=dev, dtype=torch.float64)
@@ -353,7 +368,7 @@ def main():
             el = float(t.item())
         ttt = {"seconds": el, "d_star": d_star, "rho_rel": rr_star, "converged": st_star == 0,
                "block_steps": st3["steps"], "host_solves": st3["host_solves"], "host_solve_s": st3["host_solve_s"],
-               "gpu_solves": st3["gpu_solves"], "gpu_solve_s": st3["gpu_solve_s"],
+               "gpu_solves": st3["gpu_solves"], "gpu_solve_s": st3["gpu_solve_s"], "second_pass": sec,
                "region": "wall clock: context init from device-resident C1, C2 + sylv_sketch_solve (steps, "
                          "canonical check schedule, projected solves: host Bartels-Stewart for d r < 512, device "
                          "sign-function iteration above, bisection); max over ranks"}

@@ -1600,9 +1600,11 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
       CK(cudaStreamSynchronize(c->st));
       c->y_dev = false;
     }
+    InitTrace tr;   // SYLV_TRACE_INIT=1: phase times on stderr
     std::vector<double> Y1, Y2;
     std::string err;
     const int l = svd_truncate(m, c->Y, c->rank_tol, max_rank, Y1, Y2, err);
+    tr.mark("solution: SVD of Y", c->st);
     if (l < 0) return fail(c, SYLV_E_LAPACK, err);
     if (rank) *rank = l;
     double* Xout[2] = {X1, X2};
@@ -1623,6 +1625,7 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
               s += q.Rh[(size_t)b * r * r + a * r + p] * (*Ys[qi])[(size_t)col * m + (b - 1) * r + p];
             M[(size_t)((b - 1) * r + a) * l + col] = s;
           }
+      tr.mark("solution: T^-1 Y, R_b blocks", c->st);
       const bool dev_out = is_device_ptr(Xout[qi]);
       double* Xd = dev_out ? Xout[qi] : dalloc<double>((size_t)c->n * ldx);
       CK(cudaMemsetAsync(Xd, 0, (size_t)c->n * ldx * sizeof(double), c->st));
@@ -1658,6 +1661,7 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
           CK(cudaGetLastError());
         }
         CK(cudaStreamSynchronize(c->st));
+        tr.mark("solution: replay + X accumulation", c->st);
         dfree(Md);
         dfree(rbuf);
       }

@@ -34,6 +34,9 @@ typedef void (*dgesvd_t)(const char*, const char*, const int*, const int*, doubl
                          double*, double*, const int*, double*, const int*, double*,
                          const int*, int*, fstrlen, fstrlen);
 
+typedef void (*dgesdd_t)(const char*, const int*, const int*, double*, const int*, double*, double*,
+                         const int*, double*, const int*, double*, const int*, int*, int*, fstrlen);
+
 struct Lapack {
   void* h = nullptr;
   dgees_t dgees = nullptr;
@@ -42,6 +45,7 @@ struct Lapack {
   dgemm_t dgemm = nullptr;
   dtrsm_t dtrsm = nullptr;
   dgesvd_t dgesvd = nullptr;
+  dgesdd_t dgesdd = nullptr;   // optional: divide and conquer (what numpy's svd calls)
 };
 Lapack g_lapack;
 std::mutex g_mu;
@@ -85,6 +89,7 @@ bool lapack_load(const char* path, std::string& err) {
   }
   std::string ignore;
   sym(h, "dtrsyl3", L.dtrsyl3, ignore);  // optional (LAPACK >= 3.11)
+  sym(h, "dgesdd", L.dgesdd, ignore);    // optional
   g_lapack = L;
   return true;
 }
@@ -242,18 +247,37 @@ int sylvester_bs(int m, int r, std::vector<double>& MU, std::vector<double>& MV,
 int svd_truncate(int m, const std::vector<double>& Yin, double rank_tol, int max_rank,
                  std::vector<double>& Y1, std::vector<double>& Y2, std::string& err) {
   std::vector<double> A(Yin), S(m), U((size_t)m * m), VT((size_t)m * m);
-  const char jobu = 'S', jobvt = 'S';
   int info = 0, lwork = -1;
   double wq = 0;
-  g_lapack.dgesvd(&jobu, &jobvt, &m, &m, A.data(), &m, S.data(), U.data(), &m, VT.data(), &m, &wq,
-                  &lwork, &info, 1, 1);
-  lwork = std::max(1, (int)wq);
-  std::vector<double> work(lwork);
-  g_lapack.dgesvd(&jobu, &jobvt, &m, &m, A.data(), &m, S.data(), U.data(), &m, VT.data(), &m,
-                  work.data(), &lwork, &info, 1, 1);
-  if (info != 0) {
-    err = "dgesvd info=" + std::to_string(info);
-    return -1;
+  bool done = false;
+  if (g_lapack.dgesdd) {
+    // divide and conquer (c3, m = 1872: ~9 s with dgesvd on the host); dgesvd if it fails
+    const char jobz = 'S';
+    std::vector<int> iwork((size_t)8 * m);
+    g_lapack.dgesdd(&jobz, &m, &m, A.data(), &m, S.data(), U.data(), &m, VT.data(), &m, &wq, &lwork,
+                    iwork.data(), &info, 1);
+    if (info == 0) {
+      lwork = std::max(1, (int)wq);
+      std::vector<double> work(lwork);
+      g_lapack.dgesdd(&jobz, &m, &m, A.data(), &m, S.data(), U.data(), &m, VT.data(), &m, work.data(), &lwork,
+                      iwork.data(), &info, 1);
+      done = info == 0;
+    }
+    if (!done) A = Yin;
+  }
+  if (!done) {
+    const char jobu = 'S', jobvt = 'S';
+    lwork = -1;
+    g_lapack.dgesvd(&jobu, &jobvt, &m, &m, A.data(), &m, S.data(), U.data(), &m, VT.data(), &m, &wq,
+                    &lwork, &info, 1, 1);
+    lwork = std::max(1, (int)wq);
+    std::vector<double> work(lwork);
+    g_lapack.dgesvd(&jobu, &jobvt, &m, &m, A.data(), &m, S.data(), U.data(), &m, VT.data(), &m,
+                    work.data(), &lwork, &info, 1, 1);
+    if (info != 0) {
+      err = "dgesvd info=" + std::to_string(info);
+      return -1;
+    }
   }
   int l = 0;
   if (m > 0 && S[0] > 0.0)
