@@ -239,6 +239,7 @@ struct sylv_ctx {
   bool y_dev = false;
   std::vector<double> Y;
   GpuSylv* gsolve = nullptr;    // device projected solver (created on first use)
+  cublasHandle_t blas = nullptr;  // second pass X accumulation (created on first use)
   int gpu_fail_d = 1 << 30;     // smallest d where the device solve fell back to the host
   std::vector<std::pair<int, double>> hist;
   sylv_stats stats{};
@@ -1321,6 +1322,7 @@ void sylv_sketch_destroy(sylv_ctx* ctx) {
   for (auto& q : ctx->seq) free_seq(q);
   dfree(ctx->red);
   delete ctx->gsolve;
+  if (ctx->blas) cublasDestroy(ctx->blas);
   for (cudaStream_t s : {ctx->st2, ctx->st3, ctx->st4, ctx->st_solve})
     if (s) cudaStreamDestroy(s);
   if (ctx->fork) cudaEventDestroy(ctx->fork);
@@ -1636,6 +1638,19 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
         CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
         auto rslot = [&](int j) { return rbuf + (int64_t)(j % (K + C)) * q.ld * r + q.gz; };
         CK(cudaMemcpyAsync(rslot(1) - q.gz, q.Cdev, (size_t)q.ld * r * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+        // the 2.5-D TMA pass 2 for the replay too: tensor maps of the replay slots
+        std::vector<CUtensorMap> rmapH, rmapW;
+        bool rtma = q.tma;
+        if (rtma) {
+          rmapH.resize(K + C);
+          rmapW.resize(K + C);
+          const int N = q.st25.N, nz = q.st25.nz;
+          for (int sl = 0; sl < K + C && rtma; ++sl) {
+            const double* base = rbuf + (int64_t)sl * q.ld * r;
+            rtma = encode_block_map(&rmapH[sl], base, N, nz + 2, q.ld, r, Geo25<kTY25>::HX, Geo25<kTY25>::HY) &&
+                   encode_block_map(&rmapW[sl], base, N, nz + 2, q.ld, r, Geo25<kTY25>::WX, kTY25);
+          }
+        }
         int j0 = 1;
         for (int j = 1; j <= d; ++j) {
           if (j >= 2) {  // Z_j from Z_{j-nwin..j-1} with the stored pass-2 coefficients of step j-1
@@ -1643,19 +1658,56 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
             const int nwin = std::min(K, jp);
             Win win{};
             for (int i = 0; i < nwin; ++i) win.p[i] = rslot(jp - nwin + 1 + i);
-            launch_pass2<false>(c, q, win, nwin, jp, nullptr, q.Kc + (int64_t)jp * (1 + K) * r * r, rslot(j), c->st,
-                                /*allow_tma=*/false);
+            const double* coef = q.Kc + (int64_t)jp * (1 + K) * r * r;
+            if (rtma) {
+              Tma25 tm;
+              tm.zd = rmapH[jp % (K + C)];
+              for (int i = 0; i < nwin - 1; ++i) tm.win[i] = rmapW[(jp - nwin + 1 + i) % (K + C)];
+#define SYLV_ST3D_R(RR, KK) k_st3d<kTY25, RR, KK, 2, false><<<c->G25, 32 * kTY25, c->smem25_2, c->st>>>(tm, q.st25, nwin, coef, rslot(j), q.part2)
+              if (r == 8) {
+                switch (K) {
+                  case 1: SYLV_ST3D_R(8, 1); break;
+                  case 2: SYLV_ST3D_R(8, 2); break;
+                  case 3: SYLV_ST3D_R(8, 3); break;
+                  case 4: SYLV_ST3D_R(8, 4); break;
+                }
+              } else {
+                switch (K) {
+                  case 1: SYLV_ST3D_R(4, 1); break;
+                  case 2: SYLV_ST3D_R(4, 2); break;
+                  case 3: SYLV_ST3D_R(4, 3); break;
+                  case 4: SYLV_ST3D_R(4, 4); break;
+                }
+              }
+#undef SYLV_ST3D_R
+              count(c);
+            } else {
+              launch_pass2<false>(c, q, win, nwin, jp, nullptr, coef, rslot(j), c->st, /*allow_tma=*/false);
+            }
             if (c->comm) c->comm->halo(rslot(j), r, q.ld, q.gz, c->st, kChanUMain);
           }
           if (j - j0 + 1 == C || j == d) {
-            ChunkPtrs cp{};
-            for (int b = j0; b <= j; ++b) cp.p[b - j0] = rslot(b);
-            const int64_t tot = c->n * (int64_t)l;
-            const int gx = (int)std::min<int64_t>((int64_t)c->sm * 8, (tot + 255) / 256);
-            SYLV_DISPATCH_R(r, {
-              k_xacc<R_><<<gx, kThreads, 0, c->st>>>(c->n, cp, j - j0 + 1, q.ld, Md + (int64_t)(j0 - 1) * r * l, l, Xd, ldx);
-            });
-            count(c);
+            // X += [U_j0 .. U_j] M[j0..j] as DGEMMs over runs of adjacent replay slots (a run's
+            // columns have the uniform stride ld): X^T (l x n, ld ldx) += M^T (l x kk) U^T
+            // the device projected solver's cuBLAS handle when it exists (already initialised)
+            cublasHandle_t hb = (c->gsolve && c->gsolve->hb) ? c->gsolve->hb : c->blas;
+            if (!hb) {
+              if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw Status{SYLV_E_CUDA, "cublasCreate"};
+              hb = c->blas;
+            }
+            if (cublasSetStream(hb, c->st) != CUBLAS_STATUS_SUCCESS) throw Status{SYLV_E_CUDA, "cublasSetStream"};
+            const double one = 1.0;
+            int b0 = j0;
+            while (b0 <= j) {
+              int b1 = b0;
+              while (b1 < j && (b1 + 1) % (K + C) != 0) ++b1;      // stop at the ring wrap
+              const int kk = (b1 - b0 + 1) * r;
+              if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, l, (int)c->n, kk, &one,
+                              Md + (int64_t)(b0 - 1) * r * l, l, rslot(b0), (int)q.ld, &one, Xd, (int)ldx) !=
+                  CUBLAS_STATUS_SUCCESS)
+                throw Status{SYLV_E_CUDA, "cublasDgemm (X accumulation)"};
+              b0 = b1 + 1;
+            }
             j0 = j + 1;
           }
           CK(cudaGetLastError());

@@ -741,32 +741,8 @@ __global__ void k_soa_mul_rowmajor(int64_t n, const double* __restrict__ Z, int6
   }
 }
 
-// =====================================================================================
-// Second pass accumulation X[row, l] += sum_b sum_a Z_b[row, a] M[(b*R + a)*ell + l]
-// (a7), one thread per (row, l); X row-major with leading dimension ldx.
-// =====================================================================================
+// Second pass (a7): blocks per X accumulation (the replay keeps k + chunk blocks; the
+// accumulation X += [U_j0 .. U_j] M is a cuBLAS DGEMM per run of adjacent replay slots, engine.cu)
 constexpr int kMaxChunk = 16;
-struct ChunkPtrs {
-  const double* p[kMaxChunk];
-};
-
-template <int R>
-__global__ void __launch_bounds__(kThreads) k_xacc(int64_t n, ChunkPtrs zb, int nb, int64_t ld,
-                                                   const double* __restrict__ M, int ell,
-                                                   double* __restrict__ X, int64_t ldx) {
-  const int64_t total = n * (int64_t)ell;
-  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * kThreads) {
-    const int64_t row = e / ell;
-    const int l = (int)(e - row * ell);
-    double acc = X[row * ldx + l];
-    for (int b = 0; b < nb; ++b) {
-#pragma unroll
-      for (int a = 0; a < R; ++a)
-        acc = fma(__ldg(zb.p[b] + a * ld + row), __ldg(M + (int64_t)(b * R + a) * ell + l), acc);
-    }
-    X[row * ldx + l] = acc;
-  }
-}
 
 }  // namespace sylv
