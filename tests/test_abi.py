@@ -54,3 +54,24 @@ def test_invalid_config_is_rejected_without_gpu_work():
     with pytest.raises(pkg.SylvError) as e:
         pkg.SylvSketch(A, A, C[:, :2], C[:, :2], r=2, k=2, d_max=5, s=60)   # s % zeta != 0
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("kind,N,n", [("stencil3d", 256, 256 ** 3), ("stencil2d", 512, 512 * 512),
+                                      ("csr", 1, 4194304), ("csr", 1, 20011)])
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_partition_tiles_rows_on_32_row_groups(kind, N, n, P):
+    """sylv_partition (host only): the ranks' ranges tile [0, n) in order, start at multiples
+    of 32 rows (the sketch hash's groups never straddle ranks), are whole planes / lines for
+    the stencils, and are balanced to within one plane group / one 32-row group."""
+    import paper_2311_16019_b200 as pkg
+    from synth import inputs
+    cfg = inputs.small_config(kind=kind, N=N, n=n) if kind == "csr" else inputs.small_config(kind=kind, N=N)
+    rows = [pkg.partition(cfg, P, r) for r in range(P)]
+    assert rows[0][0] == 0 and rows[-1][1] == cfg.n
+    assert all(rows[i][1] == rows[i + 1][0] for i in range(P - 1))
+    assert all(b % 32 == 0 and e > b for b, e in rows)
+    unit = N * N if kind == "stencil3d" else N if kind == "stencil2d" else 1
+    assert all(b % unit == 0 and (e % unit == 0 or e == cfg.n) for b, e in rows)
+    sizes = [e - b for b, e in rows]
+    g = 32 if kind == "csr" else max(unit, 32)
+    assert max(sizes) - min(sizes) <= 2 * g
