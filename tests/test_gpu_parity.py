@@ -55,7 +55,9 @@ def _rho_close(rr, ro):
     """1e-8 relative while rho_rel >= 1e-9 (three decades below tol = 1e-6); below that the
     iteration has converged past the tolerance and rho is rounding noise: both must be tiny."""
     if ro >= 1e-9:
-        return abs(rr - ro) <= 1e-8 * ro
+        # 1e-8 relative, with the rounding floor of a quantity normalised by ||C1 C2^T||
+        # (~1e-16 times the conditioning; 1e-15 absolute) below rho_rel ~ 1e-7
+        return abs(rr - ro) <= max(1e-8 * ro, 1e-15)
     return abs(rr - ro) <= 1e-12
 
 
