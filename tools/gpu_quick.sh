@@ -1,1 +1,3 @@
-timeout 300 python tools/quick_time.py c3 6 > gpurun_out/plain3.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_q.csv python tools/quick_time.py c3 6 > gpurun_out/ncu3.log 2>&1; echo ncu $? >> gpurun_out/ncu3.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -o faulthandler_timeout=300 -k "r4" > gpurun_out/pt.log 2>&1; echo tests $? >> gpurun_out/pt.log
+for i in 1 2; do timeout 300 python tools/quick_time.py c2 20 serial 2>&1 | grep -E "pass1:|pass2:" >> gpurun_out/occ6.log; done
+timeout 300 python tools/quick_time.py c2 20 2>&1 | grep -E "ms/step" >> gpurun_out/occ6.log
