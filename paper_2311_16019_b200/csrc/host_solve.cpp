@@ -8,7 +8,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <thread>
 
 namespace sylv {
 namespace {
@@ -37,8 +41,11 @@ typedef void (*dgesvd_t)(const char*, const char*, const int*, const int*, doubl
 typedef void (*dgesdd_t)(const char*, const int*, const int*, double*, const int*, double*, double*,
                          const int*, double*, const int*, double*, const int*, int*, int*, fstrlen);
 
+typedef int (*set_threads_local_t)(int);
+
 struct Lapack {
   void* h = nullptr;
+  set_threads_local_t set_threads_local = nullptr;   // OpenBLAS: BLAS threads of the calling thread
   dgees_t dgees = nullptr;
   dtrsyl_t dtrsyl = nullptr;
   dtrsyl3_t dtrsyl3 = nullptr;
@@ -90,6 +97,7 @@ bool lapack_load(const char* path, std::string& err) {
   std::string ignore;
   sym(h, "dtrsyl3", L.dtrsyl3, ignore);  // optional (LAPACK >= 3.11)
   sym(h, "dgesdd", L.dgesdd, ignore);    // optional
+  L.set_threads_local = reinterpret_cast<set_threads_local_t>(dlsym(h, "openblas_set_num_threads_local"));
   g_lapack = L;
   return true;
 }
@@ -185,10 +193,48 @@ int sylvester_bs(int m, int r, std::vector<double>& MU, std::vector<double>& MV,
     err = "LAPACK not loaded (sylv_set_lapack_path)";
     return -2;
   }
+  // SYLV_TRACE_INIT=1: phase times of the host solve on stderr (development aid)
+  const bool trace = std::getenv("SYLV_TRACE_INIT") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[host] %-24s m=%d %8.1f ms\n", what, m, std::chrono::duration<double, std::milli>(now - t0).count());
+    t0 = now;
+  };
   std::vector<double> ZU, ZV;
   // a Schur iteration that does not converge (badly scaled M of an ill-conditioned sketched
   // basis) is a failed check at this d, not a missing library
-  if (schur(m, MU, ZU, err) || schur(m, MV, ZV, err)) return 1;
+  // Opt-in (SYLV_HOST_PARALLEL=1): the two independent Schur decompositions on two host
+  // threads with half of the BLAS threads each (OpenBLAS per-thread thread counts).  c1 at
+  // m = 3128: 10.0 s -> 6.0 s, but the results are not reproducible run to run (rho_rel at c1's
+  // crossing moved by 1.4e-4 relative between two solves of the same matrices), so the default
+  // is one after the other.
+  const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+  if (m >= 512 && g_lapack.set_threads_local && std::getenv("SYLV_HOST_PARALLEL")) {
+    int su = 0, sv = 0;
+    std::string erru, errv;
+    const int half = (int)std::max(1u, hw / 2);
+    std::thread tu([&]() {
+      const int prev = g_lapack.set_threads_local(half);
+      su = schur(m, MU, ZU, erru);
+      g_lapack.set_threads_local(prev);
+    });
+    const int prev = g_lapack.set_threads_local(half);
+    sv = schur(m, MV, ZV, errv);
+    g_lapack.set_threads_local(prev);
+    tu.join();
+    lap("dgees M_U || M_V");
+    if (su || sv) {
+      err = su ? erru : errv;
+      return 1;
+    }
+  } else {
+    if (schur(m, MU, ZU, err)) return 1;
+    lap("dgees M_U");
+    if (schur(m, MV, ZV, err)) return 1;
+    lap("dgees M_V");
+  }
   // Ft = ZU^T F ZV = ZU[0:r,:]^T (B ZV[0:r,:])
   std::vector<double> Bc(r * r), tmp((size_t)r * m), F((size_t)m * m);
   for (int a = 0; a < r; ++a)
@@ -222,6 +268,7 @@ int sylvester_bs(int m, int r, std::vector<double>& MU, std::vector<double>& MV,
     g_lapack.dtrsyl(&ta, &tb, &isgn, &m, &m, MU.data(), &m, MV.data(), &m, F.data(), &m, &scale,
                     &info, 1, 1);
   }
+  lap("dtrsyl3");
   if (info < 0) {
     err = "dtrsyl info=" + std::to_string(info);
     return -1;
@@ -235,6 +282,7 @@ int sylvester_bs(int m, int r, std::vector<double>& MU, std::vector<double>& MV,
   gemm('N', 'N', m, m, m, 1.0 / scale, ZU.data(), m, F.data(), m, 0.0, W.data(), m);
   Y.assign((size_t)m * m, 0.0);
   gemm('N', 'T', m, m, m, 1.0, W.data(), m, ZV.data(), m, 0.0, Y.data(), m);
+  lap("back-transform GEMMs");
   for (double v : Y)
     if (!std::isfinite(v)) {
       err = "non-finite projected solution";
