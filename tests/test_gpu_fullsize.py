@@ -60,3 +60,56 @@ def test_fullsize_invariants(name, seqs):
         assert _rel(SU.T @ SU, Tn.T @ Tn) <= 1e-10, (name, which, _rel(SU.T @ SU, Tn.T @ Tn))
         del blocks, W, lhs, rhs
     g.close()
+
+
+@pytest.mark.parametrize("name,P", [("c3", 2), ("c4", 3)])
+def test_fullsize_sharded_matches_unsharded(name, P):
+    """The row-sharded path (virtual ranks of one process, the same code as NCCL ranks) at a
+    full BASELINE size: per-step rho and T equal the unsharded run up to reduction order."""
+    import threading
+    import paper_2311_16019_b200 as pkg
+    cfg = inputs.get_config(name)
+    csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
+    C1, C2 = inputs.make_rhs(cfg)
+    nsteps = 6
+    g = pkg.from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr,
+                        stream=torch.cuda.current_stream().cuda_stream)
+    rho1 = []
+    for d in range(1, nsteps + 1):
+        g.step(1)
+        rho1.append(g.residual(d)[1])
+    T1 = g.get_small(0, nsteps)[1]
+    g.close()
+    torch.cuda.empty_cache()
+    grp = pkg.LocalGroup(P)
+    out, errs = [None] * P, []
+
+    def worker(rank):
+        try:
+            torch.cuda.set_device(0)
+            b, e = pkg.partition(cfg, P, rank)
+            comm = grp.comm(rank)
+            st = torch.cuda.Stream()
+            h = pkg.from_config(cfg, C1=torch.from_numpy(C1[b:e]).cuda(), C2=torch.from_numpy(C2[b:e]).cuda(),
+                                csr_pair=csr, stream=st.cuda_stream, comm=comm, row_range=(b, e))
+            rho = []
+            for d in range(1, nsteps + 1):
+                h.step(1)
+                rho.append(h.residual(d)[1])
+            out[rank] = (rho, h.get_small(0, nsteps)[1])
+            h.close()
+            comm.close()
+        except Exception as ex:  # surfaced below
+            errs.append((rank, ex))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=900)
+    grp.close()
+    assert not errs, errs
+    for rho, T in out:
+        for d, (a, b) in enumerate(zip(rho, rho1), 1):
+            assert abs(a - b) <= 1e-10 * b + 1e-15, (name, d, a, b)
+        assert _rel(T, T1) <= 1e-10
