@@ -322,10 +322,16 @@ struct GpuSylv {
         const double dt = std::chrono::duration<double>(now() - ti).count();
         if (ns_steps && newton_steps + ns_steps > 0 && ns) t_ns += dt; else t_newton += dt;
       }
-      if (!std::isfinite(rel)) return false;
+      if (!std::isfinite(rel)) {
+        if (trace) std::fprintf(stderr, "[proj] m=%d non-finite step after %d iterations\n", m, iterations);
+        return false;
+      }
       if (rel < 1e-2) scale = false;                      // quadratic phase: unscaled
       if (last || rel < 1e-14) {                          // one step after rel < 1e-7: error ~ rel^2
-        if (!near_identity(A, m, st) || !near_identity(B, m, st)) return false;   // wrong fixed point
+        if (!near_identity(A, m, st) || !near_identity(B, m, st)) {          // wrong fixed point
+          if (trace) std::fprintf(stderr, "[proj] m=%d identity check failed after %d iterations\n", m, iterations);
+          if (!std::getenv("SYLV_PROJ_ACCEPT")) return false;   // development switch (accuracy study)
+        }
         ckb(cublasDscal(hb, (int)mm, &half, C, 1), "dscal (Y = C/2)");
         if (trace)
           std::fprintf(stderr, "[proj] m=%d build %.1f ms, %d Newton %.1f ms, %d NS %.1f ms\n", m, 1e3 * t_build,
@@ -337,6 +343,7 @@ struct GpuSylv {
       // not inferred from the step size: the projected matrices can be far from normal)
       if (allow_ns && !ns && rel < 5e-2 && sq_dev(A, m) < 0.3 && sq_dev(B, m) < 0.3) ns = true;
     }
+    if (trace) std::fprintf(stderr, "[proj] m=%d no convergence in 60 iterations (rel step history above)\n", m);
     return false;
   }
 };
