@@ -194,6 +194,8 @@ typedef struct {
   int64_t gpu_solves;        /* projected solves done on the device (sign iteration) */
   double gpu_solve_s;        /* wall seconds in them                               */
   int64_t gpu_solve_fallbacks; /* device solves that did not converge -> host BS   */
+  int64_t gpu_approx_checks;   /* solve driver: checks decided "rho_rel > 3 tol" by a
+                                  device solve that ended off the identity          */
 } sylv_stats;
 
 sylv_status sylv_sketch_stats(sylv_ctx* ctx, sylv_stats* out);

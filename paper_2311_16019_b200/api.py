@@ -48,7 +48,8 @@ class Stats(C.Structure):
                 ("ms_skqr", C.c_double), ("n_skqr", C.c_int64), ("ms_sketch", C.c_double),
                 ("n_sketch", C.c_int64), ("host_solve_s", C.c_double),
                 ("host_solves", C.c_int64), ("kappa_T_u", C.c_double), ("kappa_T_v", C.c_double),
-                ("gpu_solves", C.c_int64), ("gpu_solve_s", C.c_double), ("gpu_solve_fallbacks", C.c_int64)]
+                ("gpu_solves", C.c_int64), ("gpu_solve_s", C.c_double), ("gpu_solve_fallbacks", C.c_int64),
+                ("gpu_approx_checks", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -97,6 +97,8 @@ struct GpuSylv {
   double *Hb = nullptr, *work = nullptr, *dlog = nullptr;
   int *ipiv = nullptr, *info = nullptr;
   int iterations = 0;
+  bool allow_approx = false;   // accept a converged iteration that ends off the identity
+  bool off_identity = false;   // the last accepted solve ended off the identity (approximate)
   int newton_steps = 0, ns_steps = 0;
   double t_build = 0, t_newton = 0, t_ns = 0;   // seconds (SYLV_TRACE_PROJ)
 
@@ -328,9 +330,11 @@ struct GpuSylv {
       }
       if (rel < 1e-2) scale = false;                      // quadratic phase: unscaled
       if (last || rel < 1e-14) {                          // one step after rel < 1e-7: error ~ rel^2
+        off_identity = false;
         if (!near_identity(A, m, st) || !near_identity(B, m, st)) {          // wrong fixed point
           if (trace) std::fprintf(stderr, "[proj] m=%d identity check failed after %d iterations\n", m, iterations);
-          if (!std::getenv("SYLV_PROJ_ACCEPT")) return false;   // development switch (accuracy study)
+          if (!allow_approx && !std::getenv("SYLV_PROJ_ACCEPT")) return false;   // (development switch)
+          off_identity = true;          // approximate: the caller decides whether it may be used
         }
         ckb(cublasDscal(hb, (int)mm, &half, C, 1), "dscal (Y = C/2)");
         if (trace)
