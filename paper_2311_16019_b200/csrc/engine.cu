@@ -136,7 +136,6 @@ struct TimedPair {
 struct Sequence {
   // 2.5-D TMA passes (3-D stencil, r = 8, even N): tensor maps of the ring slots
   CUtensorMap mapH[kMaxK + 1];   // halo boxes
-  CUtensorMap mapH36[kMaxK + 1]; // 36-wide halo boxes (extra A^T blocks of the fused pass)
   bool fused = false;            // pass 2 fused with the old-block part of the next pass 1
   CUtensorMap mapW[kMaxK + 1];   // window boxes
   bool tma = false;
@@ -504,7 +503,6 @@ void setup_tma(sylv_ctx* c, Sequence& q) {
     const double* base = q.ring + (int64_t)j * q.ld * c->R;     // ghost plane 0 of slot j
     if (!encode_block_map(&q.mapH[j], base, N, nz + 2, q.ld, c->R, Geo25<kTY25>::HX, Geo25<kTY25>::HY)) return;
     if (!encode_block_map(&q.mapW[j], base, N, nz + 2, q.ld, c->R, Geo25<kTY25>::WX, kTY25)) return;
-    if (!encode_block_map(&q.mapH36[j], base, N, nz + 2, q.ld, c->R, Geo25x<kTY25>::HX2, Geo25<kTY25>::HY)) return;
   }
   St25& p = q.st25;
   p.N = N;
@@ -552,7 +550,7 @@ void setup_tma(sylv_ctx* c, Sequence& q) {
     int smem_sm = 0, dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-    if (2 * (c->smem25_f + 1024) > (size_t)smem_sm) q.fused = false;
+    if (2 * (c->smem25_f + 2048) > (size_t)smem_sm) q.fused = false;   // + static + reserved
   }
   if (c->R == 8) {
     switch (c->K) {
@@ -580,7 +578,7 @@ Tma25 tma_args(const Sequence& q, int j, int nwin) {
   return tm;
 }
 
-// Fused pass maps: Z_d halo, 36-wide halo boxes of the extra A^T blocks (window slots nw ..
+// Fused pass maps: Z_d halo, halo boxes (same geometry) of the extra A^T blocks (window slots nw ..
 // nwin-2), window boxes of the oldest nw blocks (stencil25d_fused.cuh)
 Tma25F tma_args_fused(const Sequence& q, int j, int nwin) {
   Tma25F tm;
@@ -590,7 +588,7 @@ Tma25F tma_args_fused(const Sequence& q, int j, int nwin) {
   for (int i = 0; i < nwin - 1; ++i) {
     const int slot = (j - nwin + 1 + i) % ns;
     if (i < nw) tm.win[i] = q.mapW[slot];
-    else tm.hx[i - nw] = q.mapH36[slot];
+    else tm.hx[i - nw] = q.mapH[slot];     // same geometry as Z_d's halo box
   }
   return tm;
 }

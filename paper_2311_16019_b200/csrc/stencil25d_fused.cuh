@@ -11,8 +11,8 @@
 //
 // Tiles, z-streaming, TMA stages and DMMA fragments as in stencil25d.cuh (pass 2).  A^T Z_d comes
 // from the same neighbour values as A Z_d (transposed coefficients: x -> -x etc. swap); the other
-// A^T blocks (the newest k-2 window blocks) arrive as halo boxes of width kTx+4 (36; Z_d's box is
-// 38 wide) with their z neighbours rolled in registers.  A^T Z_i is produced in the pass-2 element
+// A^T blocks (the newest k-2 window blocks) arrive as halo boxes of Z_d's geometry (38 wide; two
+// CTAs per SM still fit at r = 8, k = 3) with their z neighbours rolled in registers.  A^T Z_i is produced in the pass-2 element
 // pattern (B) and moved to the pass-1 pattern (A) by two shuffles per element, W' in pattern A is
 // the Gram's shuffle output, and P_i += (A^T Z_i)^T W' is one DMMA per 4 points.
 //
@@ -25,13 +25,14 @@ namespace sylv {
 
 template <int TY>
 struct Geo25x {
-  static constexpr int HX2 = kTx + 4;                  // extra halo box width (x0-2 .. x0+33)
+  static constexpr int HX2 = kTx + 6;                  // extra halo box width: Z_d's (38; a 36-wide box
+                                                       // gave 36 % bank conflicts)
   static constexpr int HCOL2 = HX2 * (TY + 2);
 };
 
 struct Tma25F {
   CUtensorMap zd;                // halo box (38 wide) of Z_d
-  CUtensorMap hx[kMaxK];         // extra halo boxes (36 wide) of the A^T window blocks, oldest first
+  CUtensorMap hx[kMaxK];         // extra halo boxes (Z_d's geometry) of the A^T window blocks, oldest first
   CUtensorMap win[kMaxK];        // window boxes of the other window blocks, oldest first
 };
 

@@ -1,1 +1,4 @@
-SYLV_FUSED=1 timeout 300 python tools/quick_time.py c3 4 serial > gpurun_out/plain5.log 2>&1 && SYLV_FUSED=1 timeout 600 ncu --set full --clock-control none -k regex:"k_st3d_fused" -s 2 -c 1 -o gpurun_out/prof_fused python tools/quick_time.py c3 4 serial > gpurun_out/ncu5.log 2>&1; echo ncu $? >> gpurun_out/ncu5.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -o faulthandler_timeout=300 -k "fused" > gpurun_out/pt.log 2>&1; echo tests $? >> gpurun_out/pt.log
+SYLV_FUSED=1 timeout 300 python tools/quick_time.py c3 20 serial 2>&1 | grep -E "pass1:|pass2:" > gpurun_out/fused2.log
+SYLV_FUSED=1 timeout 300 python tools/quick_time.py c3 20 2>&1 | grep -E "ms/step" >> gpurun_out/fused2.log
+timeout 300 python tools/quick_time.py c3 20 2>&1 | grep -E "ms/step" >> gpurun_out/fused2.log
