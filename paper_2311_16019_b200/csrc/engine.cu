@@ -157,7 +157,7 @@ struct Sequence {
   uint32_t* pl_list = nullptr;   // zeta x ngroups local group indices
   uint32_t* pl_off = nullptr;    // zeta x wpb + 1 per-warp segment offsets into pl_list
   double* pl_strips = nullptr;   // zeta x wpb x R x kPullS per-warp strips
-  uint32_t pl_nch = 0, pl_wpb = 0, pl_bpw = 1;
+  uint32_t pl_nch = 0, pl_wpb = 0, pl_bpw = 1, pl_kmax = 1;
   double* w = nullptr;        // s x R
   double* w2 = nullptr;       // s x R
   double* Q = nullptr;        // s x ldT (col-major)
@@ -710,7 +710,8 @@ void launch_sketch(sylv_ctx* c, Sequence& q, const double* X, int R, const doubl
     SYLV_DISPATCH_R(R, {
       k_sketch_pull<R_><<<(nw + kPullWarps - 1) / kPullWarps, kPullWarps * 32, 0, st>>>(
           c->n, X, q.ld, q.sp, q.pl_list, q.pl_off, q.pl_wpb, q.pl_bpw, q.pl_strips);
-      k_sketch_pull_fold_apply<R_><<<red_grid, 256, 0, st>>>(q.pl_strips, q.sp, q.pl_wpb, q.pl_bpw, M, w);
+      k_sketch_pull_fold_apply<R_><<<(int)std::min<int64_t>(8 * c->sm, (q.s + 256 / R_ - 1) / (256 / R_)), 256, 0, st>>>(
+          q.pl_strips, q.sp, q.pl_wpb, q.pl_bpw, q.pl_kmax, M, w);
     });
     count(c, 2);
     return;
@@ -750,6 +751,8 @@ void build_pull_lists(sylv_ctx* c, Sequence& q, cudaStream_t st) {
   q.pl_nch = (uint32_t)nch;
   q.pl_bpw = (uint32_t)bpw;
   q.pl_wpb = (uint32_t)wpb;
+  // fold: warps whose strips can cover a slot (shortest range floor(b / wpb) >= 1 bases)
+  q.pl_kmax = (uint32_t)std::min<int64_t>(wpb, (bpw + 31) / std::max<int64_t>(1, b / wpb) + 2);
   const int64_t nw = (int64_t)q.sp.zeta * wpb;
   uint32_t *keys = dalloc<uint32_t>(total), *keys2 = dalloc<uint32_t>(total), *vals = dalloc<uint32_t>(total);
   uint32_t* counts = dalloc<uint32_t>(nw + 1);

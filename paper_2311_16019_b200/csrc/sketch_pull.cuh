@@ -193,38 +193,44 @@ __global__ void __launch_bounds__(kPullWarps * 32, pull_min_blocks<R>()) k_sketc
 // warp's own bases + 30), summed nearest first — a fixed order.  Needs b >= bpw + 31 so a
 // strip never covers a slot twice (b >= 64 is required at init).
 template <int R>
-__global__ void k_sketch_pull_fold_apply(const double* __restrict__ strips, SketchParams sp, uint32_t wpb,
-                                         uint32_t bpw, const double* __restrict__ M, double* __restrict__ w) {
+__global__ void __launch_bounds__(256) k_sketch_pull_fold_apply(const double* __restrict__ strips, SketchParams sp,
+                                                                uint32_t wpb, uint32_t bpw, uint32_t kmax,
+                                                                const double* __restrict__ M, double* __restrict__ w) {
+  // one thread per (slot, column): the strip sums; then one per (slot, output column): x M.
+  // kmax bounds the candidate warps (their distance grows with k; the predicated loop keeps
+  // every candidate's load in flight, and adds them nearest first like the break-loop did)
+  constexpr int SPB = 256 / R;                         // slots per block
+  __shared__ double vs[SPB][R];
   const uint32_t b = sp.b;
   const int64_t s = (int64_t)b * sp.zeta;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < s; q += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t t = (uint32_t)(q / b), p = (uint32_t)(q - (int64_t)t * b);
-    const uint32_t wl = pull_owner(p, b, wpb);
-    double v[R];
-#pragma unroll
-    for (int a = 0; a < R; ++a) v[a] = 0.0;
-    for (uint32_t k = 0; k < wpb; ++k) {
-      const uint32_t wq = (wl + wpb - k) % wpb;
-      const uint32_t dd = (p + b - pull_q0(wq, b, wpb)) % b;
-      if (dd >= bpw + 31u) break;
-      const double* st = strips + (size_t)(t * wpb + wq) * R * kPullS + dd;
-#pragma unroll
-      for (int a = 0; a < R; ++a) v[a] += st[a * kPullS];
+  const int ls = threadIdx.x / R, a = threadIdx.x % R;
+  for (int64_t q0 = (int64_t)blockIdx.x * SPB; q0 < s; q0 += (int64_t)gridDim.x * SPB) {
+    const int64_t q = q0 + ls;
+    if (q < s) {
+      const uint32_t t = (uint32_t)(q / b), p = (uint32_t)(q - (int64_t)t * b);
+      const uint32_t wl = pull_owner(p, b, wpb);
+      double v = 0.0;
+      for (uint32_t k = 0; k < kmax; ++k) {
+        const uint32_t wq = (wl + wpb - k) % wpb;
+        const uint32_t dd = (p + b - pull_q0(wq, b, wpb)) % b;
+        if (dd < bpw + 31u) v += strips[((size_t)(t * wpb + wq) * R + a) * kPullS + dd];
+      }
+      vs[ls][a] = v * sp.scale;
     }
-#pragma unroll
-    for (int a = 0; a < R; ++a) v[a] *= sp.scale;
-#pragma unroll
-    for (int c = 0; c < R; ++c) {
+    __syncthreads();
+    if (q < s) {
+      const int c = a;
       double o;
       if (M) {
         o = 0.0;
 #pragma unroll
-        for (int a = 0; a < R; ++a) o = fma(v[a], __ldg(M + a * R + c), o);
+        for (int e = 0; e < R; ++e) o = fma(vs[ls][e], __ldg(M + e * R + c), o);
       } else {
-        o = v[c];
+        o = vs[ls][c];
       }
       w[q * R + c] = o;
     }
+    __syncthreads();
   }
 }
 

@@ -1,1 +1,2 @@
-timeout 300 python tools/quick_time.py c4 4 serial > gpurun_out/plain6.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_pass1_csr|k_sketch_pull|k_pass2_rows" -s 6 -c 3 -o gpurun_out/prof_c4 python tools/quick_time.py c4 4 serial > gpurun_out/ncu6.log 2>&1; echo ncu $? >> gpurun_out/ncu6.log
+timeout 900 python -m pytest tests/test_gpu_sketch_pull.py tests/test_gpu_sharded.py tests/test_gpu_parity.py -x -q -p no:cacheprovider -o faulthandler_timeout=300 -k "pull or full_config or sharded" > gpurun_out/pt.log 2>&1; echo tests $? >> gpurun_out/pt.log
+for c in c4 c3 c2 c1; do timeout 300 python tools/quick_time.py $c 20 2>&1 | grep -E "ms/step" >> gpurun_out/fold.log; done
