@@ -75,3 +75,22 @@ def test_partition_tiles_rows_on_32_row_groups(kind, N, n, P):
     sizes = [e - b for b, e in rows]
     g = 32 if kind == "csr" else max(unit, 32)
     assert max(sizes) - min(sizes) <= 2 * g
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the oracle arm, CPU only) prints one JSON line with the
+    contract's keys (c0, a few steps)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--config", "c0",
+                          "--steps", "3", "--warmup", "3"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
