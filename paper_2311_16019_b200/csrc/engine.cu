@@ -462,8 +462,14 @@ bool encode_block_map(CUtensorMap* m, const double* base, int N, int depth, int6
   cuuint64_t strides[3] = {(cuuint64_t)N * 8, (cuuint64_t)N * N * 8, (cuuint64_t)ld * 8};
   cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, 1, (cuuint32_t)R};
   cuuint32_t es[4] = {1, 1, 1, 1};
+  static const CUtensorMapL2promotion prom = [] {   // SYLV_TMA_L2PROM=0|64|128|256 (tuning)
+    const char* e = std::getenv("SYLV_TMA_L2PROM");
+    const int v = e ? std::atoi(e) : 256;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+           : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
