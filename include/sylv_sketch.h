@@ -32,7 +32,11 @@
  *    (allocated in init, released in destroy).
  *  - Errors: status codes only; no exceptions cross the ABI, no abort/exit.
  *    sylv_sketch_last_error() returns the context's last message.  After
- *    SYLV_E_BREAKDOWN / SYLV_E_SINGULAR / SYLV_E_NOT_CONVERGED the context stays valid.
+ *    SYLV_E_BREAKDOWN / SYLV_E_SINGULAR / SYLV_E_NOT_CONVERGED / SYLV_E_LOST_INDEP the
+ *    context stays valid for residual / solution / get_small / history (d <= d_done);
+ *    after SYLV_E_BREAKDOWN or SYLV_E_LOST_INDEP it is terminal for stepping (step
+ *    returns the same status again), and get_block only returns blocks still in the
+ *    ring of the last step the device ran.
  *  - Concurrency: a context is not thread-safe; all device work is ordered on the
  *    stream given to init.
  *  - Supported shapes (round 1): r in {1,2,4,8}, 1 <= k <= 4, s % zeta == 0,
@@ -54,7 +58,7 @@ typedef enum {
   SYLV_E_INVALID = 1,       /* bad argument / unsupported shape                          */
   SYLV_E_NOMEM = 2,         /* device or host allocation failed                          */
   SYLV_E_CUDA = 3,          /* CUDA runtime error (message in last_error)                */
-  SYLV_E_NCCL = 4,          /* reserved for the multi-rank build                         */
+  SYLV_E_NCCL = 4,          /* NCCL transport failure (comm create, collective)          */
   SYLV_E_BREAKDOWN = 5,     /* min diag h_{d+1,d} <= 1e-14 ||W~||_F (R11)      */
   SYLV_E_SINGULAR = 6,      /* projected Sylvester equation (numerically) singular       */
   SYLV_E_NOT_CONVERGED = 7, /* d_max reached without rho_rel < tol; state stays valid    */
@@ -135,8 +139,9 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B,
 
 /* Advance both sequences by up to nsteps block steps (Alg. 1 lines 3-9).  On return
  * *d_done = number of completed steps d (the basis holds d+1 blocks).  Returns
- * SYLV_E_BREAKDOWN (state valid, d_done = breakdown step) or SYLV_E_NOT_CONVERGED
- * when d_max is reached before nsteps. */
+ * SYLV_E_BREAKDOWN (state valid, d_done = breakdown step), SYLV_E_LOST_INDEP (tau_{d+1}
+ * not positive definite; d_done = last good step) or SYLV_E_NOT_CONVERGED when d_max is
+ * reached before nsteps.  After BREAKDOWN / LOST_INDEP further calls return that status. */
 sylv_status sylv_sketch_step(sylv_ctx* ctx, int32_t nsteps, int32_t* d_done);
 
 /* Host projected solve at 1 <= d <= d_done (Alg. 1 lines 10-13): M_U Y + Y M_V^T =
@@ -153,9 +158,12 @@ sylv_status sylv_sketch_residual(sylv_ctx* ctx, int32_t d, double* rho, double* 
 sylv_status sylv_sketch_solution(sylv_ctx* ctx, int32_t d, double* X1, double* X2,
                                  int64_t ldx, int32_t max_rank, int32_t* rank);
 
-/* Driver: step + canonical check schedule + bisection (R9).  On success
- * *d_star is the smallest bracketed d with rho_rel < tol.  Residual history is
- * available through sylv_sketch_history. */
+/* Driver: step + canonical check schedule + search of the last bracket (R9:
+ * crossing prediction, safeguarded regula falsi on log rho_rel with bisection steps;
+ * all checks exact unless SYLV_APPROX_CHECKS=1).  On success *d_star is a passing d
+ * whose checked predecessor in the bracket failed (with rho_rel monotone on the bracket:
+ * the first crossing, as bisection finds it).  Residual history is available through
+ * sylv_sketch_history. */
 sylv_status sylv_sketch_solve(sylv_ctx* ctx, int32_t* d_star, double* rho_rel);
 
 /* Test / introspection entries -------------------------------------------------- */

@@ -135,15 +135,36 @@ def load_library(path: str = LIB_PATH):
     return lib
 
 
-def _ptr(x) -> Tuple[int, object]:
-    """(address, keep-alive) for a float64/int C-contiguous torch tensor or numpy array."""
+def _ptr(x, shape=None, dtype=np.float64, out=False) -> Tuple[int, object]:
+    """(address, keep-alive) for a C-contiguous torch tensor or numpy array.
+
+    The C ABI takes raw double* (int64/int32 for CSR arrays): a wrong dtype or shape would
+    make the library read or write past the buffer, so both are checked here.  `shape`
+    (rows, cols) is the layout the ABI expects; CUDA tensors must live on the current
+    device.  Inputs may be converted (numpy copy); outputs (out=True) never are, since a
+    silent copy would receive the result and be dropped."""
     if x is None:
         return 0, None
     if hasattr(x, "data_ptr"):           # torch.Tensor
+        import torch
+        tdt = {np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32}[dtype]
+        if x.dtype != tdt:
+            raise TypeError(f"tensor must be {tdt}, got {x.dtype}")
         if not x.is_contiguous():
             raise ValueError("tensor must be contiguous")
+        if x.is_cuda and x.device.index != torch.cuda.current_device():
+            raise ValueError(f"tensor is on {x.device}, the current device is cuda:{torch.cuda.current_device()}")
+        if shape is not None and tuple(x.shape) != tuple(shape):
+            raise ValueError(f"expected shape {tuple(shape)}, got {tuple(x.shape)}")
         return x.data_ptr(), x
-    a = np.ascontiguousarray(x)
+    if out:
+        if not isinstance(x, np.ndarray) or x.dtype != dtype or not x.flags.c_contiguous or not x.flags.writeable:
+            raise ValueError(f"output must be a writeable C-contiguous {np.dtype(dtype).name} numpy array")
+        a = x
+    else:
+        a = np.ascontiguousarray(x, dtype=dtype)
+    if shape is not None and tuple(a.shape) != tuple(shape):
+        raise ValueError(f"expected shape {tuple(shape)}, got {tuple(a.shape)}")
     return a.ctypes.data, a
 
 
@@ -165,9 +186,7 @@ def csr_operator(n: int, row_ptr, col_idx, val):
     op.n = n
     keep = []
     for name, arr, dt in (("row_ptr", row_ptr, np.int64), ("col_idx", col_idx, np.int32), ("val", val, np.float64)):
-        if not hasattr(arr, "data_ptr"):
-            arr = np.ascontiguousarray(arr, dtype=dt)
-        p, k = _ptr(arr)
+        p, k = _ptr(arr, dtype=dt)
         setattr(op, name, p)
         keep.append(k)
     op.nnz = int(len(val) if not hasattr(val, "numel") else val.numel())
@@ -190,8 +209,9 @@ class SylvSketch:
                           row_begin=row_range[0] if row_range else 0, row_end=row_range[1] if row_range else 0)
         self.n, self.r, self.s = int(A.n), r, s     # n: this context's (local) rows, set below
         self._keep = [A, B, keep]
-        p1, k1 = _ptr(C1)
-        p2, k2 = _ptr(C2)
+        n_loc = int(row_range[1] - row_range[0]) if row_range else int(A.n)
+        p1, k1 = _ptr(C1, shape=(n_loc, r))
+        p2, k2 = _ptr(C2, shape=(n_loc, r))
         self._ctx = C.c_void_p()
         st = C.c_void_p(stream) if stream is not None else None
         self._comm = comm
@@ -251,8 +271,8 @@ class SylvSketch:
         if X1 is None:
             X1 = np.zeros((self.n, max_rank))
             X2 = np.zeros((self.n, max_rank))
-        p1, _ = _ptr(X1)
-        p2, _ = _ptr(X2)
+        p1, _ = _ptr(X1, shape=(self.n, max_rank), out=True)
+        p2, _ = _ptr(X2, shape=(self.n, max_rank), out=True)
         rank = C.c_int32()
         self._check(self.lib.sylv_sketch_solution(self._ctx, d, p1, p2, max_rank, max_rank, C.byref(rank)))
         return X1, X2, rank.value
@@ -261,8 +281,8 @@ class SylvSketch:
         r = int(X.shape[1])
         if out is None:
             out = np.zeros((self.s, r))
-        px, _ = _ptr(X)
-        po, _ = _ptr(out)
+        px, _ = _ptr(X, shape=(self.n, r))
+        po, _ = _ptr(out, shape=(self.s, r), out=True)
         self._check(self.lib.sylv_sketch_apply_sketch(self._ctx, which, px, r, po))
         return out
 
@@ -278,7 +298,7 @@ class SylvSketch:
     def get_block(self, which: int, j: int, out=None):
         if out is None:
             out = np.zeros((self.n, self.r))
-        p, _ = _ptr(out)
+        p, _ = _ptr(out, shape=(self.n, self.r), out=True)
         self._check(self.lib.sylv_sketch_get_block(self._ctx, which, j, p))
         return out
 

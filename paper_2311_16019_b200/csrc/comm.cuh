@@ -121,7 +121,15 @@ struct NcclComm : Comm {
     nranks = n;
     rank = r;
     nccl_check(a.CommInitRank(&base, n, id, r), "ncclCommInitRank");
-    for (int i = 0; i < kNumChan; ++i) nccl_check(a.CommSplit(base, 0, r, &ch[i], nullptr), "ncclCommSplit");
+    try {
+      for (int i = 0; i < kNumChan; ++i) nccl_check(a.CommSplit(base, 0, r, &ch[i], nullptr), "ncclCommSplit");
+    } catch (...) {   // the destructor does not run for a throwing constructor
+      for (auto& c : ch)
+        if (c) a.CommDestroy(c), c = nullptr;
+      a.CommDestroy(base);
+      base = nullptr;
+      throw;
+    }
   }
   ~NcclComm() override {
     NcclApi& a = nccl_api();

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -231,8 +232,12 @@ struct sylv_ctx {
   cudaEvent_t phase[3] = {nullptr, nullptr, nullptr};   // pass/sketch phase barriers (enqueue_steps)
   Sequence seq[2];
   int d_done = 0;
-  bool broken = false;
+  int d_dev = 0;                // last step enqueued on the device (>= d_done; ring slots reflect it)
+  bool broken = false;          // breakdown (R11): the Krylov space is invariant
   int breakdown_d = -1;
+  bool halted = false;          // terminal for stepping: breakdown or lost independence
+  sylv_status halt_status = SYLV_OK;
+  std::string halt_msg;
   // last projected solution (host vector, or the device solver's C when y_dev)
   int y_d = -1;
   bool y_dev = false;
@@ -1131,6 +1136,7 @@ bool device_solve(const sylv_ctx* c, int d) {
 // copies; no synchronisation (sylv_sketch_step = enqueue + finish; the solve driver
 // enqueues the steps to the next check before solving the current one).
 void enqueue_steps(sylv_ctx* c, int first, int last) {
+  c->d_dev = std::max(c->d_dev, last);
   // U passes on the context stream, V passes on st2 (independent sequences); each
   // sequence's sketch-space work on its own side stream.  Serial mode: all on st.
   const bool serial = (c->cflags & 2) != 0;
@@ -1193,13 +1199,21 @@ sylv_status finish_steps(sylv_ctx* c, int first, int last) {
       c->stats.steps += j - first + 1;
       c->broken = true;
       c->breakdown_d = j;
-      return fail(c, SYLV_E_BREAKDOWN, "breakdown at step " + std::to_string(j));
+      c->halted = true;
+      c->halt_status = SYLV_E_BREAKDOWN;
+      c->halt_msg = "breakdown at step " + std::to_string(j);
+      return fail(c, SYLV_E_BREAKDOWN, c->halt_msg);
     }
     const int g = c->seq[0].flags_h[j + 1] | c->seq[1].flags_h[j + 1];
     if (g & 4) {
+      // terminal like a breakdown: steps j+1.. may already have run on the device (solve
+      // driver prefetch) and overwritten the ring, so the state cannot be advanced from j
       c->d_done = j;
       c->stats.steps += j - first + 1;
-      return fail(c, SYLV_E_LOST_INDEP, "sketched basis lost independence at step " + std::to_string(j));
+      c->halted = true;
+      c->halt_status = SYLV_E_LOST_INDEP;
+      c->halt_msg = "sketched basis lost independence at step " + std::to_string(j);
+      return fail(c, SYLV_E_LOST_INDEP, c->halt_msg);
     }
   }
   c->stats.steps += last - first + 1;
@@ -1291,9 +1305,9 @@ sylv_status sylv_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id
   try {
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
-    sylv_comm* c = new sylv_comm();
+    std::unique_ptr<sylv_comm> c(new sylv_comm());
     c->impl = new NcclComm(nranks, rank, u);
-    *out = c;
+    *out = c.release();
     return SYLV_OK;
   } catch (const CommError& e) {
     std::fprintf(stderr, "sylv_comm_create_nccl: %s\n", e.what.c_str());
@@ -1463,7 +1477,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
 sylv_status sylv_sketch_step(sylv_ctx* c, int32_t nsteps, int32_t* d_done) {
   if (!c) return SYLV_E_INVALID;
   if (d_done) *d_done = c->d_done;
-  if (c->broken) return fail(c, SYLV_E_BREAKDOWN, "breakdown at step " + std::to_string(c->breakdown_d));
+  if (c->halted) return fail(c, c->halt_status, c->halt_msg);
   return guard(c, [&]() -> sylv_status {
     const int first = c->d_done + 1;
     const int last = std::min(c->dmax, c->d_done + std::max(0, nsteps));
@@ -1798,10 +1812,12 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     return d2 + (std::log(c->tol) - std::log(r2)) / slope;
   };
   // schedule phase: approximate device checks may decide clear fails (rho_rel > 3 tol); the
-  // search for the first crossing below uses exact solves only.  SYLV_APPROX_CHECKS=0: off
+  // search for the first crossing below uses exact solves only
+  // (opt-in, SYLV_APPROX_CHECKS=1: an off-identity sign iteration solves a different
+  // equation, so its rho_rel has no error bound; by default every check is exact)
   {
     const char* e = std::getenv("SYLV_APPROX_CHECKS");
-    c->approx_thr = (e && std::strcmp(e, "0") == 0) ? 0.0 : 3.0 * c->tol;
+    c->approx_thr = (e && std::strcmp(e, "1") == 0) ? 3.0 * c->tol : 0.0;
   }
   struct ApproxOff {   // every exit of the driver leaves residual() exact
     sylv_ctx* c;
@@ -1819,16 +1835,16 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     }
     const int dc = sched[idx];
     if (dc > c->dmax) break;
-    if (c->d_done < dc && !c->broken) {
+    if (c->d_done < dc && !c->halted) {
       sylv_status s = finish_pending();
-      if (!ok_step(s)) return s;
-      if (c->d_done < dc && !c->broken) {
+      if (!ok_step(s) && s != SYLV_E_LOST_INDEP) return s;
+      if (c->d_done < dc && !c->halted) {
         int dd = 0;
         s = sylv_sketch_step(c, dc - c->d_done, &dd);
-        if (!ok_step(s)) return s;
+        if (!ok_step(s) && s != SYLV_E_LOST_INDEP) return s;
       }
     }
-    if (!c->broken && idx + 1 < sched.size() && !device_solve(c, std::min(dc, c->d_done))) {
+    if (!c->halted && idx + 1 < sched.size() && !device_solve(c, std::min(dc, c->d_done))) {
       const int nx = std::min(sched[idx + 1], c->dmax);
       if (nx > c->d_done) {
         const int f = c->d_done + 1;
@@ -1857,13 +1873,18 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     skips = 0;
     last_rr = rr;
     if (std::isfinite(rr)) seen.emplace_back(dchk, rr);
-    if (rr < c->tol || c->broken) {
+    // a breakdown decides a pass only at (or before) the checked d: with the crossing
+    // prediction a check can be moved below steps that were already prefetched, and a
+    // breakdown found while finishing those steps says nothing about dchk
+    const bool brk = c->broken && c->breakdown_d <= dchk;
+    if (rr < c->tol || brk) {
       d_pass = dchk;
       rr_pass = rr;
-      pass_by_breakdown = c->broken;
+      pass_by_breakdown = brk;
       break;
     }
     d_fail = dchk;
+    if (c->halted && c->d_done <= dchk) break;   // lost independence: no later d to check
   }
   c->approx_thr = 0.0;
   {
@@ -2027,7 +2048,8 @@ sylv_status sylv_sketch_get_small(sylv_ctx* c, int32_t which, int32_t d, double*
 
 sylv_status sylv_sketch_get_block(sylv_ctx* c, int32_t which, int32_t j, double* out) {
   if (!c || !out || (which != 0 && which != 1)) return SYLV_E_INVALID;
-  if (j < 1 || j > c->d_done + 1 || j < c->d_done + 1 - c->K)
+  // the ring reflects the last ENQUEUED step (d_dev >= d_done after a halt inside a prefetched batch)
+  if (j < 1 || j > c->d_done + 1 || j < c->d_dev + 1 - c->K)
     return fail(c, SYLV_E_STATE, "block j is not in the window");
   return guard(c, [&]() -> sylv_status {
     Sequence& q = c->seq[which];

@@ -297,3 +297,59 @@ def test_sketched_residual_within_embedding_bound(k):
     assert eU < 1 and eV < 1
     assert res.rho == pytest.approx(np.linalg.norm(S_U @ R @ S_V.T), rel=1e-9)
     assert (1 - eU) * (1 - eV) * nR * (1 - 1e-9) <= res.rho <= (1 + eU) * (1 + eV) * nR * (1 + 1e-9)
+
+
+def test_truncation_rank_and_factors_on_a_known_spectrum():
+    """R12: Y ~ Y1 Y2^T keeps sigma_i > rank_tol * sigma_1.  Pinned with a Y whose
+    SVD is fixed by construction (orthogonal factors from a seeded QR, singular values that
+    straddle the threshold 1e-12 sigma_1 in both directions): l is the known count, and
+    X1 X2^T equals the whitened bases times the known best rank-l approximation,
+    Uhat Y_l Vhat^T with Uhat = U_d T_U^{-1} (retained blocks)."""
+    cfg, A, Bt, B, C1, C2 = _small(N=10, r=2, k=2, d_max=12)
+    d, r = 8, 2
+    m = d * r
+    obj = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2, keep_basis=True)
+    obj.step(d)
+    rng = np.random.default_rng(7)
+    Qa, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    Qb, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    sig = np.array([3.0, 1e-2, 1e-5, 1e-8, 9e-12, 4e-12, 2e-12, 1e-12, 5e-13, 1e-14] + [0.0] * (m - 10))
+    ell = int(np.sum(sig > 1e-12 * 3.0))          # sigma_i > 3e-12: 3.0 ... 4e-12 -> 6
+    assert ell == 6
+    Y = (Qa * sig[None, :]) @ Qb.T
+    X1, X2 = obj.solution(d, Y, rank_tol=1e-12)
+    assert X1.shape[1] == ell and X2.shape[1] == ell
+    U, V = _retained(obj, d)
+    Uh = sla.solve_triangular(obj.U.T[:m, :m], U.T, trans="T", lower=False).T
+    Vh = sla.solve_triangular(obj.V.T[:m, :m], V.T, trans="T", lower=False).T
+    Yl = (Qa[:, :ell] * sig[None, :ell]) @ Qb[:, :ell].T
+    ref = Uh @ Yl @ Vh.T
+    assert np.linalg.norm(X1 @ X2.T - ref) <= 1e-10 * np.linalg.norm(ref)
+    # balanced split: ||X1 e_i|| / ||X2 e_i|| = ||Uhat Qa e_i|| / ||Vhat Qb e_i|| (sqrt(sigma) on both);
+    # only for the well-separated sigma_1..sigma_4 (singular vectors of the clustered 1e-12
+    # values are determined only to eps sigma_1 / gap)
+    for i in range(4):
+        want = np.linalg.norm(Uh @ Qa[:, i]) / np.linalg.norm(Vh @ Qb[:, i])
+        assert np.linalg.norm(X1[:, i]) / np.linalg.norm(X2[:, i]) == pytest.approx(want, rel=1e-6)
+    # rank_tol = 0 keeps every singular value the SVD returns as positive (the exact zeros
+    # come back as rounding-level positives)
+    X1f, _ = obj.solution(d, Y, rank_tol=0.0)
+    assert X1f.shape[1] >= 10
+
+
+def test_cond_T_equals_condition_of_the_sketched_basis():
+    """Sequence.cond_T(d) = kappa(T_d) = kappa(S U_d) (Prop. 2.1: S U_d = Q_d T_d, Q_d orthonormal),
+    checked against the explicitly sketched retained basis; T_d grows ill-conditioned with d
+    under truncation (the loss of global orthogonality the paper discusses)."""
+    cfg, A, Bt, B, C1, C2 = _small(N=16, r=2, k=2, d_max=40)
+    S = sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed_u)
+    seq = alg1.Sequence(A, C1, S, k=2, keep_basis=True)
+    for _ in range(30):
+        seq.step()
+    conds = []
+    for d in (5, 15, 30):
+        U = np.concatenate([seq.U[i] for i in range(1, d + 1)], axis=1)
+        want = np.linalg.cond(np.asarray(S @ U))
+        assert seq.cond_T(d) == pytest.approx(want, rel=1e-6)
+        conds.append(want)
+    assert conds[0] < conds[1] < conds[2]

@@ -127,3 +127,68 @@ def test_apply_hashed_equals_materialised_product():
     S = sparse_sign.matrix(n, s, 8, 12)
     got = sparse_sign.apply_hashed(X, s, 8, 12, chunk=3000)
     assert np.allclose(got, S @ X, rtol=1e-13, atol=1e-13 * np.abs(X).sum())
+
+
+def _mp_edges(m, s):
+    return (1 - math.sqrt(m / s)) ** 2, (1 + math.sqrt(m / s)) ** 2
+
+
+def _sine_modes(N, dims, freqs):
+    """Orthonormal basis of low-frequency Dirichlet sine modes on an N^dims grid (x fastest)."""
+    x = np.arange(1, N + 1) / (N + 1)
+    import itertools
+    cols = []
+    for f in itertools.product(*[range(1, q + 1) for q in freqs]):
+        v = np.ones(1)
+        for a in reversed(f):                  # last factor varies slowest (z), first fastest (x)
+            v = np.kron(v, np.sin(np.pi * a * x))
+        cols.append(v)
+    Q, _ = np.linalg.qr(np.array(cols).T)
+    return Q
+
+
+@pytest.mark.parametrize("dims,N,freqs,seed", [(2, 128, (10, 10), 11), (2, 128, (10, 10), 12),
+                                               (3, 32, (5, 5, 8), 11), (3, 32, (5, 5, 8), 12)])
+def test_embedding_on_smooth_structured_subspaces(dims, N, freqs, seed):
+    """P:117-127 (epsilon-subspace embedding) on the subspaces the method actually sketches:
+    smooth low-frequency modes, where neighbouring rows (one 32-row hash group) carry nearly
+    equal values.  sigma^2(S Q) must stay inside the Marchenko-Pastur edges (s = 4m, the BJ
+    ratio) with the same margins as for random subspaces.  Negative control: the same S with
+    its signs dropped (|S|) sums the smooth rows coherently and fails by two orders."""
+    Q = _sine_modes(N, dims, freqs)
+    m = Q.shape[1]
+    s = 4 * m
+    S = sparse_sign.matrix(Q.shape[0], s, 8, seed)
+    sv = np.linalg.svd(S @ Q, compute_uv=False) ** 2
+    lo, hi = _mp_edges(m, s)
+    assert sv.min() > lo - 0.08 and sv.max() < hi + 0.15
+    sv_bad = np.linalg.svd(abs(S) @ Q, compute_uv=False) ** 2
+    assert sv_bad.max() > 10 * hi
+
+
+@pytest.mark.parametrize("kind,N,r,d,seed", [("stencil2d", 64, 1, 100, 11), ("stencil3d", 24, 4, 50, 11),
+                                             ("stencil3d", 24, 4, 50, 12)])
+def test_embedding_on_krylov_subspaces(kind, N, r, d, seed):
+    """The embedding pin on orthonormalised Krylov bases K_d(A, C1) of the BJ operator families
+    (c0's 2-D operator; a 24^3 slice of c2/c3's 3-D operator), built here by plain block
+    Arnoldi with full reorthogonalisation (independent of alg1): sigma^2(S Q) inside the MP edges at s = 4 d r."""
+    from oracle import operators
+    from synth import inputs
+    cfg = (inputs.get_config("c0") if kind == "stencil2d" else
+           inputs.small_config(kind, N=N, r=r, k=2, d_max=d))
+    A, _, _ = operators.operator_pair(cfg)
+    C1, _ = inputs.make_rhs(cfg)
+    Q, _ = np.linalg.qr(C1)                    # full block Arnoldi, reorthogonalised twice
+    for _ in range(d - 1):
+        W = np.asarray(A @ Q[:, -r:])
+        for _ in range(2):
+            W -= Q @ (Q.T @ W)
+        q, _ = np.linalg.qr(W)
+        Q = np.concatenate([Q, q], axis=1)
+    m = Q.shape[1]
+    s = 8 * math.ceil(4 * m / 8)
+    S = sparse_sign.matrix(Q.shape[0], s, 8, seed)
+    sv = np.linalg.svd(S @ Q, compute_uv=False) ** 2
+    lo, hi = _mp_edges(m, s)
+    assert m == d * r and np.allclose(Q.T @ Q, np.eye(m), atol=1e-10)
+    assert sv.min() > lo - 0.08 and sv.max() < hi + 0.15
