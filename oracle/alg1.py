@@ -145,7 +145,9 @@ class Sequence:
             for i in range(max(1, j - k + 1), j + 1):
                 W = W - U[i] @ self.H[(i, j)]
             U[j + 1] = sla.solve_triangular(self.H[(j + 1, j)], W.T, trans="T", lower=False).T
-            X = X + U[j + 1] @ Z[j * r:(j + 1) * r]
+            Zj = Z[j * r:(j + 1) * r]
+            for i0 in range(0, X.shape[0], 1 << 20):          # X += U_{j+1} Z_{j+1} (row blocks:
+                X[i0:i0 + (1 << 20)] += U[j + 1][i0:i0 + (1 << 20)] @ Zj   # memory only, same sums)
             for i in list(U):
                 if i < j + 2 - k:
                     del U[i]
@@ -357,16 +359,43 @@ that is within 2 of hi), a bisection
     return SolveResult(best.d, best.rho_rel, True, hist, best.Y if keep_Y else None, t_step, t_solve)
 
 
-def true_residual(A, B, C1, C2, X1, X2) -> Tuple[float, float]:
-    """||A X + X B - C1 C2^T||_F and its ratio to ||C1 C2^T||_F for X = X1 X2^T (P:224, P:290),
-    without Gram matrices: L = [A X1, X1, C1], R = [X2, B^T X2, C2], N = diag(I, I, -I),
-    ||L N R^T||_F = ||R_L N R_R^T||_F with Householder R-factors."""
-    L = np.concatenate([np.asarray(A @ X1), X1, C1], axis=1)
-    Rm = np.concatenate([X2, np.asarray(B.T @ X2), C2], axis=1)
-    l = X1.shape[1]
+def rfactor_rows(n: int, rows_of, chunk: Optional[int] = None) -> np.ndarray:
+    """Householder R-factor of an n-row matrix given by rows_of(slice) (numpy.linalg.qr).
+    chunk: R of [M_1; M_2; ...] = R of the stacked per-block R-factors (up to row signs,
+    which the residual norm below does not see) — the same factor without holding M whole."""
+    if chunk is None or chunk >= n:
+        return np.linalg.qr(rows_of(slice(0, n)), mode="r")
+    parts = [np.linalg.qr(rows_of(slice(i, min(n, i + chunk))), mode="r") for i in range(0, n, chunk)]
+    return np.linalg.qr(np.concatenate(parts, axis=0), mode="r")
+
+
+def residual_rfactor_L(A, X1, C1, chunk: Optional[int] = None) -> np.ndarray:
+    """R-factor of L = [A X1, X1, C1] (O8 below)."""
+    Acsr = A.tocsr()
+    return rfactor_rows(X1.shape[0], lambda sl: np.concatenate([np.asarray(Acsr[sl] @ X1), X1[sl], C1[sl]], axis=1),
+                        chunk)
+
+
+def residual_rfactor_R(B, X2, C2, chunk: Optional[int] = None) -> np.ndarray:
+    """R-factor of R = [X2, B^T X2, C2] (O8 below)."""
+    Bt = B.T.tocsr()
+    return rfactor_rows(X2.shape[0], lambda sl: np.concatenate([X2[sl], np.asarray(Bt[sl] @ X2), C2[sl]], axis=1),
+                        chunk)
+
+
+def residual_from_rfactors(RL, RR, l: int, C1, C2) -> Tuple[float, float]:
+    """||R_L N R_R^T||_F with N = diag(I_l, I_l, -I_r), and its ratio to ||C1 C2^T||_F."""
     N = np.diag(np.concatenate([np.ones(2 * l), -np.ones(C1.shape[1])]))
-    RL = np.linalg.qr(L, mode="r")
-    RR = np.linalg.qr(Rm, mode="r")
     res = float(np.linalg.norm(RL @ N @ RR.T))
     rc = float(np.linalg.norm(np.linalg.qr(C1, mode="r") @ np.linalg.qr(C2, mode="r").T))
     return res, res / rc
+
+
+def true_residual(A, B, C1, C2, X1, X2, chunk: Optional[int] = None) -> Tuple[float, float]:
+    """||A X + X B - C1 C2^T||_F and its ratio to ||C1 C2^T||_F for X = X1 X2^T (P:224, P:290),
+    without Gram matrices: L = [A X1, X1, C1], R = [X2, B^T X2, C2], N = diag(I, I, -I),
+    A X + X B - C1 C2^T = L N R^T, so the norm is ||R_L N R_R^T||_F with Householder R-factors.
+    chunk: row-blocked R-factors (see rfactor_rows)."""
+    RL = residual_rfactor_L(A, X1, C1, chunk)
+    RR = residual_rfactor_R(B, X2, C2, chunk)
+    return residual_from_rfactors(RL, RR, X1.shape[1], C1, C2)

@@ -187,6 +187,10 @@ def test_true_residual_matches_dense():
     res, rel = alg1.true_residual(A, B, C1, C2, X1, X2)
     assert res == pytest.approx(np.linalg.norm(R), rel=1e-10)
     assert rel == pytest.approx(np.linalg.norm(R) / np.linalg.norm(C1 @ C2.T), rel=1e-10)
+    for chunk in (7, 32, 80):                  # row-blocked R-factors (TSQR), ragged last block
+        res_c, rel_c = alg1.true_residual(A, B, C1, C2, X1, X2, chunk=chunk)
+        assert res_c == pytest.approx(np.linalg.norm(R), rel=1e-10)
+        assert rel_c == pytest.approx(rel, rel=1e-10)
 
 
 def test_check_schedule():

@@ -94,18 +94,33 @@ def main():
     ell = int(np.count_nonzero(sig > alg1.RANK_TOL * sig[0]))
     rec["rank"] = ell
     rec["sigma_head"] = [float(x) for x in sig[:8]]
-    est_gb = cfg.n * (2 * ell + cfg.r) * 8 * 4 / 1e9
+    # memory-lean second pass: one sequence's factor at a time (X1 -> R_L, then X2 -> R_R; the
+    # same quantities as alg1.solution + alg1.true_residual, O8), row-blocked R-factors
+    est_gb = cfg.n * ell * 8 / 1e9
     rec["true_residual_mem_est_gb"] = est_gb
     if est_gb > a.mem_gb:
         rec["true_residual"] = None
         rec["true_residual_skipped"] = f"memory estimate {est_gb:.0f} GB > {a.mem_gb} GB"
         dump()
         return
-    t1 = time.perf_counter()
-    X1, X2 = obj.solution(sol.d_star, sol.Y)
-    rec["second_pass_s"] = time.perf_counter() - t1
+    obj.U.U.clear()                     # the window blocks are not needed by the replay
+    obj.V.U.clear()
+    import scipy.linalg as sla
+    W, sg, Zt = np.linalg.svd(sol.Y)
+    m = sol.d_star * cfg.r
+    Y1 = W[:, :ell] * np.sqrt(sg[:ell])[None, :]
+    Y2 = Zt[:ell].T * np.sqrt(sg[:ell])[None, :]
     A, _, B = operators.operator_pair(cfg, csr)
-    res, rel = alg1.true_residual(A, B, obj.C1, obj.C2, X1, X2)
+    chunk = 1 << 20 if cfg.n > (1 << 21) else None
+    t1 = time.perf_counter()
+    X1 = obj.U.replay(sla.solve_triangular(obj.U.T[:m, :m], Y1, lower=False), sol.d_star)
+    RL = alg1.residual_rfactor_L(A, X1, obj.C1, chunk)
+    del X1
+    X2 = obj.V.replay(sla.solve_triangular(obj.V.T[:m, :m], Y2, lower=False), sol.d_star)
+    RR = alg1.residual_rfactor_R(B, X2, obj.C2, chunk)
+    del X2
+    rec["second_pass_s"] = time.perf_counter() - t1
+    res, rel = alg1.residual_from_rfactors(RL, RR, ell, obj.C1, obj.C2)
     rec["true_residual"] = res
     rec["true_rel"] = rel
     print(f"[{cfg.name}] rank {ell} true_rel {rel:.6e} (second pass {rec['second_pass_s']:.1f}s)", flush=True)
