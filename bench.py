@@ -145,6 +145,23 @@ def dist_env():
     return ws, rank, local
 
 
+def _golden(name):
+    """The oracle's golden record of a config (tests/golden/<cfg>.json, written by
+    tools/make_golden.py from oracle/ alone): d*, rank, oracle timings on the build host."""
+    p = os.path.join(ROOT, "tests", "golden", f"{name}.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
+
+
+def _rank_cap(cfg, d, gold):
+    """Column capacity of the solution buffers: above the rank at rank_tol (the oracle's rank
+    from the golden, x1.5), so the truncation is decided by rank_tol, not by the buffer."""
+    want = int(1.5 * gold["rank"]) + 8 if gold and gold.get("rank") else 256
+    return max(1, min(d * cfg.r, want))
+
+
 def traffic_for(cfg_name, kernel):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
@@ -208,6 +225,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance solve")
+    ap.add_argument("--no-near", action="store_true", help="skip the timed window near d*")
     args = ap.parse_args()
 
     from synth import inputs
@@ -308,35 +326,11 @@ def main():
     # aggregate over the job's GPUs, against the aggregate peak
     step_gbs = (ab_job["step"] if sharded else ab["step"] * ws) / (ms / args.steps * 1e-3) / 1e9
 
-    # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the region
-    e2e = None
-    if not args.no_e2e:
-        C1h = torch.from_numpy(C1).pin_memory()
-        C2h = torch.from_numpy(C2).pin_memory()
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        s2 = pkg.from_config(cfg, C1=C1h, C2=C2h, csr_pair=csr, stream=stream.cuda_stream, **shard_kw)
-        s2.step(args.warmup + args.steps)
-        rho, rr = s2.residual(args.warmup + args.steps)          # D2H of the step's result (host solve)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        s2.close()
-        if ws > 1:
-            t = torch.tensor([el], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            el = float(t.item())
-        nst = args.warmup + args.steps
-        mirror = 2 * 8 * ((cfg.k + 1) * cfg.r ** 2 + cfg.r * ((nst // 2 + 1) * cfg.r + cfg.r))
-        e2e = {"value": (1 if sharded else ws) * nst / el, "unit": UNIT,
-               "h2d_bytes_per_step": int(2 * 8 * C1.shape[0] * cfg.r * (1 if sharded else ws) / nst),
-               "d2h_bytes_per_step": int(mirror),
-               "region": f"init(host C1,C2 pinned; H2D) + {nst} steps + residual(d) host solve; wall clock, "
-                         f"max over ranks", "rho_rel": rr}
-
     # ---- time to tolerance (BASELINE metric's first part): full solve with the canonical
-    # check schedule (R9): init from device C + steps + projected solves + bisection
+    # check schedule (R9): init from device C + steps + projected solves + search,
+    # then the second pass (a7) at the context's rank_tol (no rank cap below the rank)
     ttt = None
+    gold = _golden(cfg.name)
     if not args.no_ttt:
         barrier()
         torch.cuda.synchronize()
@@ -346,32 +340,115 @@ def main():
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         st3 = s3.stats()
-        # a7, timed separately: the second pass (replay of the basis with the stored
-        # coefficients, Y ~ Y1 Y2^T truncated to at most 32 columns) into device buffers
         sec = None
         if st_star == 0:
-            mr = 32
+            mr = _rank_cap(cfg, d_star, gold)
             X1o = torch.empty((C1.shape[0], mr), dtype=torch.float64, device=dev)
             X2o = torch.empty((C1.shape[0], mr), dtype=torch.float64, device=dev)
             torch.cuda.synchronize()
             t2 = time.perf_counter()
             _, _, rk = s3.solution(d_star, mr, X1o, X2o)
             torch.cuda.synchronize()
-            sec = {"seconds": time.perf_counter() - t2, "rank": rk, "max_rank": mr,
-                   "what": "sylv_sketch_solution(d*): SVD truncation of Y + replay of d* block steps per "
-                           "sequence (pass 2 with stored coefficients) + X accumulation, device outputs"}
+            sec = {"seconds": time.perf_counter() - t2, "rank": rk, "max_rank": mr, "rank_tol": 1e-12,
+                   "capped": rk >= mr,
+                   "what": "sylv_sketch_solution(d*): SVD truncation of Y at rank_tol + replay of d* block steps "
+                           "per sequence (pass 2 with stored coefficients) + X accumulation, device outputs"}
             del X1o, X2o
         s3.close()
+        torch.cuda.empty_cache()
         if ws > 1:
             t = torch.tensor([el], device=dev, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             el = float(t.item())
         ttt = {"seconds": el, "d_star": d_star, "rho_rel": rr_star, "converged": st_star == 0,
+               "oracle_d_star": gold.get("d_star") if gold else None,
                "block_steps": st3["steps"], "host_solves": st3["host_solves"], "host_solve_s": st3["host_solve_s"],
                "gpu_solves": st3["gpu_solves"], "gpu_solve_s": st3["gpu_solve_s"], "second_pass": sec,
                "region": "wall clock: context init from device-resident C1, C2 + sylv_sketch_solve (steps, "
                          "canonical check schedule, projected solves: host Bartels-Stewart for d r < 512, device "
-                         "sign-function iteration above, bisection); max over ranks"}
+                         "sign-function iteration above, search of the last bracket); max over ranks"}
+
+    # ---- steps near d* (the regime that decides time to tolerance: m = d r sketch-space
+    # columns, the CGS2 sweeps of Q grow with d): a second timed window d* - 30 .. d* - 10
+    near = None
+    dref = (ttt or {}).get("d_star") or (gold or {}).get("d_star")
+    if not args.no_near and dref and dref - 30 > args.warmup:
+        d0, nn = dref - 30, 20
+        s4 = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, timing=True, stream=stream.cuda_stream, **shard_kw)
+        s4.step(d0)
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(stream)
+        s4.step(nn)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_n = e0.elapsed_time(e1)
+        s4.close()
+        if ws > 1:
+            t = torch.tensor([ms_n], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms_n = float(t.item())
+        # per-kernel split near d* (serial attribution context, CUDA events per launch)
+        s5 = pkg.from_config(cfg, C1=C1d, C2=C2d, csr_pair=csr, timing=True, stream=stream.cuda_stream, serial=True,
+                             **shard_kw)
+        s5.step(d0)
+        s5.reset_stats()
+        s5.step(10)
+        torch.cuda.synchronize()
+        a5 = s5.stats()
+        s5.close()
+        torch.cuda.empty_cache()
+        m_mid = (d0 + 5) * cfg.r
+        q_bytes = 8 * cfg.s * m_mid                     # one sweep of Q (s x m), per sequence
+        skqr_ms = a5["ms_skqr"] / max(1, a5["n_skqr"])
+        step_b = (ab_job["step"] if sharded else ab["step"] * ws)
+        near = {"d_range": [d0 + 1, d0 + nn], "value": (1 if sharded else ws) * nn / (ms_n * 1e-3),
+                "unit": UNIT, "ms_per_step": ms_n / nn,
+                "step_roofline_frac": step_b / (ms_n / nn * 1e-3) / 1e9 / (peak * ws),
+                "kernels_ms": {"pass1": a5["ms_pass1"] / max(1, a5["n_pass1"]),
+                               "pass2": a5["ms_pass2"] / max(1, a5["n_pass2"]),
+                               "sketch": a5["ms_sketch"] / max(1, a5["n_sketch"]), "skqr": skqr_ms},
+                "skqr": {"m": m_mid, "Q_sweeps": 4, "bytes_per_launch": 4 * q_bytes,
+                         "GBps": 4 * q_bytes / (skqr_ms * 1e-3) / 1e9,
+                         "frac": 4 * q_bytes / (skqr_ms * 1e-3) / 1e9 / peak,
+                         "what": "sketch-space QR update (a5): block CGS2 = 4 sweeps of Q (Q^T w, Q c twice) "
+                                 "+ CholQR2, per sequence; timed including its sketch launch"}}
+
+    # ---- end to end through the C ABI with HOST buffers: init from pinned host C1, C2
+    # (H2D inside), sylv_sketch_solve to tolerance, and the solution X1, X2 (rank_tol) into
+    # pinned host buffers (D2H inside) — the calls a user makes, wall clock, max over ranks
+    e2e = None
+    if not args.no_e2e:
+        C1h = torch.from_numpy(C1).pin_memory()
+        C2h = torch.from_numpy(C2).pin_memory()
+        mr = _rank_cap(cfg, (ttt or {}).get("d_star") or cfg.d_max, gold)
+        X1h = torch.empty((C1.shape[0], mr), dtype=torch.float64).pin_memory()
+        X2h = torch.empty((C1.shape[0], mr), dtype=torch.float64).pin_memory()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s2 = pkg.from_config(cfg, C1=C1h, C2=C2h, csr_pair=csr, stream=stream.cuda_stream, **shard_kw)
+        d_e, rr_e, st_e = s2.solve()
+        rk = 0
+        if st_e == 0:
+            _, _, rk = s2.solution(d_e, mr, X1h.numpy(), X2h.numpy())
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        nst = s2.stats()["steps"]
+        s2.close()
+        if ws > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        mirror = 2 * 8 * ((cfg.k + 1) * cfg.r ** 2 + cfg.r * ((nst // 2 + 1) * cfg.r + cfg.r))
+        e2e = {"value": (1 if sharded else ws) * nst / el, "unit": UNIT, "seconds": el, "d_star": d_e,
+               "rho_rel": rr_e, "rank": rk, "max_rank": mr,
+               "h2d_bytes_per_step": int(2 * 8 * C1.shape[0] * cfg.r * (1 if sharded else ws) / max(1, nst)),
+               "d2h_bytes_per_step": int(mirror + 2 * 8 * C1.shape[0] * mr * (1 if sharded else ws) / max(1, nst)),
+               "region": "init(pinned host C1, C2: H2D) + sylv_sketch_solve to rho_rel < tol (all block steps, "
+                         "projected solves, search) + sylv_sketch_solution(d*) at rank_tol into pinned host X1, X2 "
+                         "(D2H); value = block steps run / wall clock, max over ranks"}
+        del X1h, X2h
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -380,6 +457,19 @@ def main():
         cpu = {"value": steps_o / secs_o, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                "sample": f"{steps_o} oracle block steps (both sequences) of {cfg.name} from d=1, "
                          f"after {setup_o:.0f} s oracle setup (excluded); ~{budget:.0f} s budget"}
+        if gold and gold.get("oracle_time_to_tol_s"):
+            # the oracle's whole run to tolerance (setup + steps + its schedule of Bartels-Stewart
+            # solves + search), measured once by tools/make_golden.py on the build container
+            cpu["time_to_tolerance"] = {
+                "seconds": gold["oracle_time_to_tol_s"], "d_star": gold.get("d_star"),
+                "cores": gold.get("host", {}).get("cores"), "solve_s": gold.get("solve_wall_s"),
+                "second_pass_s": gold.get("second_pass_s"),
+                "where": "build container (tests/golden, tools/make_golden.py), not this box",
+                "extrapolated_on_this_box_s": (gold.get("steps_done", gold["d_star"]) / (steps_o / secs_o)
+                                               + sum(h.get("solve_s", 0.0) for h in gold.get("history", []))
+                                               if gold.get("d_star") else None),
+                "extrapolation": "this box's oracle step rate x the golden's steps + the golden's "
+                                 "projected-solve seconds (solves not re-timed here)"}
 
     if rank == 0:
         line = {
@@ -408,7 +498,7 @@ def main():
             "step_roofline": {"bytes_per_step": ab_job["step"] if sharded else ab["step"] * ws, "GBps": step_gbs,
                               "frac": step_gbs / (peak * ws), "frac_of_8TBps": step_gbs / (NOMINAL_HBM_GBS * ws),
                               "what": "SURVEY §8(d) B_n per block step (both sequences) / device step time"},
-            "time_to_tolerance": ttt,
+            "time_to_tolerance": ttt, "near_dstar": near,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }

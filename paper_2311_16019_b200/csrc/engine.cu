@@ -1055,7 +1055,7 @@ void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t 
   }
   // ---- a5: block CGS2 against Q (m = j R columns); CholQR2; T column
   const int m = j * R;
-  const dim3 gq((m + kWarps - 1) / kWarps, c->RT);
+  const dim3 gq((m + kQtwCols - 1) / kQtwCols, c->RT);
   const int cols_per_chunk = (m + c->CC - 1) / c->CC;
   const int ncc = (m + cols_per_chunk - 1) / cols_per_chunk;
   const dim3 gc((unsigned)((q.s + kThreads - 1) / kThreads), ncc);
@@ -1436,10 +1436,12 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     CK(cudaDeviceGetAttribute(&c->sm, cudaDevAttrMultiProcessorCount, dev));
     const int64_t rows_per_cta = (int64_t)kWarps * (32 / r);
     c->G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sm * 4, (c->n + rows_per_cta - 1) / rows_per_cta));
-    // Q^T w: (ceil(m/8) x RT) CTAs; at least 2 per SM at the smallest m
-    c->RT = (int)std::max<int64_t>(1, std::min<int64_t>(64, c->s / 512));
-    c->tileQ = (c->s + c->RT - 1) / c->RT;
-    c->CC = (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * c->sm + (c->s / 256)) / std::max<int64_t>(1, c->s / 256)));
+    // Q^T w: (ceil(m / kQtwCols) x RT) CTAs, row tiles of qtw_tile<R>() rows
+    SYLV_DISPATCH_R(r, { c->tileQ = qtw_tile<R_>(); });
+    c->RT = (int)((c->s + c->tileQ - 1) / c->tileQ);
+    // Q c: (ceil(s/256) x CC) CTAs, ~4 per SM at the full width (each thread streams a row
+    // of its column chunk with 8 loads in flight)
+    c->CC = (int)std::max<int64_t>(1, std::min<int64_t>(16, (4 * c->sm + (c->s / 256)) / std::max<int64_t>(1, c->s / 256)));
     // sketch kernel: whole sketch column (s doubles) in shared memory per CTA
     c->sk_smem = (size_t)sketch_smem_doubles(c->s, c->zeta) * sizeof(double);
     int max_optin = 0;

@@ -233,37 +233,84 @@ __global__ void __launch_bounds__(kThreads) k_rmul(int64_t rows, const double* _
   }
 }
 
-// partial[(rt*m + j)*R + c] = sum_{rows in tile rt} Q[j*s + row] w[row*R + c]
+// partial[(rt*m + j)*R + c] = sum_{rows in tile rt} Q[j*s + row] w[row*R + c]   (a5: Q^T w)
+//
+// One CTA per (row tile of qtw_tile<R>() rows, group of kQtwCols columns).  The tile of w is staged
+// once in shared memory, column-major (lane-consecutive rows: conflict-free reads), so every
+// element of w is read from L2 once per column group instead of once per column; each warp
+// register-blocks kQtwU columns (kQtwU coalesced 256-byte Q loads per 32 rows, R FMAs per
+// loaded w value and column) and reduces its kQtwU x R sums by a fixed shuffle tree at the end
+// of the tile (deterministic).  Q (s x m, column-major) is read exactly once from HBM.
+template <int R> constexpr int qtw_tile() { return 4096 / R; }   // rows per tile (w tile: 32 KB)
+constexpr int kQtwU = 4;                       // columns per warp and pass
+constexpr int kQtwCols = kWarps * kQtwU * 2;   // columns per CTA (two passes of the warps)
 template <int R>
-__global__ void __launch_bounds__(kThreads) k_qtw(const double* __restrict__ Q, int64_t s, int m,
+__global__ void __launch_bounds__(kThreads, 2) k_qtw(const double* __restrict__ Q, int64_t s, int m,
                                                   const double* __restrict__ w, int64_t tile,
                                                   double* __restrict__ partial) {
+  __shared__ double ws[R][qtw_tile<R>() + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int j = blockIdx.x * kWarps + warp;
   const int rt = blockIdx.y;
   const int64_t r0 = (int64_t)rt * tile;
-  const int64_t r1 = min(s, r0 + tile);
-  double acc[R];
+  const int nr = (int)(tile < s - r0 ? tile : s - r0);
+  for (int e = threadIdx.x; e < nr * R; e += kThreads) ws[e % R][e / R] = __ldg(w + r0 * R + e);
+  __syncthreads();
+  const double* __restrict__ q0 = Q + r0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int j0 = blockIdx.x * kQtwCols + pass * kWarps * kQtwU + warp * kQtwU;
+    if (j0 >= m) break;
+    double acc[kQtwU][R];
 #pragma unroll
-  for (int c = 0; c < R; ++c) acc[c] = 0.0;
-  if (j < m) {
-    const double* __restrict__ q = Q + (int64_t)j * s;
-    for (int64_t row = r0 + lane; row < r1; row += 32) {
-      const double qv = __ldg(q + row);
+    for (int u = 0; u < kQtwU; ++u)
 #pragma unroll
-      for (int c = 0; c < R; ++c) acc[c] = fma(qv, __ldg(w + row * R + c), acc[c]);
+      for (int c = 0; c < R; ++c) acc[u][c] = 0.0;
+    const double* __restrict__ qc[kQtwU];
+#pragma unroll
+    for (int u = 0; u < kQtwU; ++u) qc[u] = q0 + (int64_t)min(j0 + u, m - 1) * s;   // clamped: zero-weighted below
+    // 4 row strides of kQtwU loads in flight per warp (HBM latency x bandwidth)
+    int row = lane;
+    for (; row + 96 < nr; row += 128) {
+      double qv[4][kQtwU];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int u = 0; u < kQtwU; ++u) qv[i][u] = __ldg(qc[u] + row + 32 * i);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+          const double wv = ws[c][row + 32 * i];
+#pragma unroll
+          for (int u = 0; u < kQtwU; ++u) acc[u][c] = fma(qv[i][u], wv, acc[u][c]);
+        }
     }
-  }
+    for (; row < nr; row += 32) {
+      double qv[kQtwU];
 #pragma unroll
-  for (int c = 0; c < R; ++c) {
-    double v = acc[c];
+      for (int u = 0; u < kQtwU; ++u) qv[u] = __ldg(qc[u] + row);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(SYLV_FULL_MASK, v, off);
-    acc[c] = v;
-  }
-  if (j < m && lane == 0) {
+      for (int c = 0; c < R; ++c) {
+        const double wv = ws[c][row];
 #pragma unroll
-    for (int c = 0; c < R; ++c) partial[((int64_t)rt * m + j) * R + c] = acc[c];
+        for (int u = 0; u < kQtwU; ++u) acc[u][c] = fma(qv[u], wv, acc[u][c]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kQtwU; ++u)
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        double v = acc[u][c];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(SYLV_FULL_MASK, v, off);
+        acc[u][c] = v;
+      }
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < kQtwU; ++u)
+        if (j0 + u < m)
+#pragma unroll
+          for (int c = 0; c < R; ++c) partial[((int64_t)rt * m + j0 + u) * R + c] = acc[u][c];
+    }
   }
 }
 
@@ -299,7 +346,17 @@ __global__ void __launch_bounds__(kThreads) k_qc_part(const double* __restrict__
     __syncthreads();
     if (row < s) {
       const double* __restrict__ q = Q + (int64_t)jj * s + row;
-      for (int t = 0; t < nj; ++t) {
+      int t = 0;
+      for (; t + 8 <= nj; t += 8) {          // 8 column loads in flight per thread
+        double qv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) qv[u] = __ldg(q + (int64_t)(t + u) * s);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int c = 0; c < R; ++c) acc[c] = fma(qv[u], cs[(t + u) * R + c], acc[c]);
+      }
+      for (; t < nj; ++t) {
         const double qv = __ldg(q + (int64_t)t * s);
 #pragma unroll
         for (int c = 0; c < R; ++c) acc[c] = fma(qv, cs[t * R + c], acc[c]);
