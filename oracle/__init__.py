@@ -20,9 +20,12 @@ Modules
                  incremental sketched QR (CGS2), projected Sylvester solve,
                  sketched residual, check schedule, two-pass reconstruction,
                  true residual.
+  alg2         — the paper's comparison methods: Alg. 2 (truncated Arnoldi without a
+                 sketch, Prop. 3.2 residual bound) and the full Arnoldi /
+                 Galerkin method.
 
 Pins (tests/test_oracle_*.py, `-m "not gpu"`) tie each part to mathematics the
 paper fixes; see DESIGN.md §"Oracle pins".  Parts with no pin say
 "parity unpinned" in their docstring.
 """
-from . import sparse_sign, operators, alg1  # noqa: F401
+from . import sparse_sign, operators, alg1, alg2  # noqa: F401
