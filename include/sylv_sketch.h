@@ -114,7 +114,18 @@ typedef struct {
   int64_t row_begin;     /* sharded contexts: this rank's global rows [row_begin, */
   int64_t row_end;       /* row_end); 0, 0 = sylv_partition's balanced split.     */
                          /* Single-rank contexts: 0, 0 (or 0, n).                  */
+  int32_t method;        /* SYLV_METHOD_*: 0 = sketched-and-truncated (Alg. 1, the
+                            hot path); 1 = truncated Arnoldi without a sketch (Alg. 2,
+                            PAPER.md:1178-1206: H_d Y + Y G_d^T = E1 b1 b2^T E1^T with
+                            b = R(C), rho = the Prop. 3.2 bound sqrt(dr)(||Y E_d g^T|| +
+                            ||h E_d^T Y||); s, zeta, seeds unused);
+                            2 = full Arnoldi / Galerkin (every block
+                            retained and orthonormalised against all previous ones by
+                            block CGS2; k is ignored (= d_max); exact residual norm;
+                            single-rank only; needs (d_max+1) n r doubles per sequence) */
 } sylv_config;
+
+enum { SYLV_METHOD_SKETCHED = 0, SYLV_METHOD_TRUNCATED = 1, SYLV_METHOD_FULL = 2 };
 
 /* Create a context and run Alg. 1 line 1: U1 ell = C1, V1 ell' = C2
  * (CholQR on the device), beta_1 = R(S_U C1), beta_2 = R(S_V C2), T_1 = tau_1 =

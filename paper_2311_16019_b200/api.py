@@ -39,7 +39,10 @@ class Config(C.Structure):
     _fields_ = [("r", C.c_int32), ("k", C.c_int32), ("d_max", C.c_int32), ("zeta", C.c_int32),
                 ("s", C.c_int64), ("seed_u", C.c_uint64), ("seed_v", C.c_uint64), ("tol", C.c_double),
                 ("rank_tol", C.c_double), ("chunk", C.c_int32), ("flags", C.c_int32),
-                ("row_begin", C.c_int64), ("row_end", C.c_int64)]
+                ("row_begin", C.c_int64), ("row_end", C.c_int64), ("method", C.c_int32)]
+
+
+METHODS = {"sketched": 0, "truncated": 1, "full": 2}   # SYLV_METHOD_* (include/sylv_sketch.h)
 
 
 class Stats(C.Structure):
@@ -200,13 +203,15 @@ class SylvSketch:
                  zeta: int = 8, seed_u: int = 11, seed_v: int = 12, tol: float = 1e-6,
                  rank_tol: float = 1e-12, chunk: int = 0, timing: bool = False, stream=None,
                  keep=None, serial: bool = False, tma: bool = True, comm: "Comm" = None,
-                 proj: str = "auto",
+                 proj: str = "auto", method: str = "sketched",
                  row_range: Optional[Tuple[int, int]] = None):
         self.lib = load_library()
         self.cfg = Config(r=r, k=k, d_max=d_max, zeta=zeta, s=s, seed_u=seed_u, seed_v=seed_v, tol=tol,
                           rank_tol=rank_tol, chunk=chunk, flags=(1 if timing else 0) | (2 if serial else 0) | (0 if tma else 4)
                           | {"auto": 0, "gpu": 8, "host": 16}[proj],
-                          row_begin=row_range[0] if row_range else 0, row_end=row_range[1] if row_range else 0)
+                          row_begin=row_range[0] if row_range else 0, row_end=row_range[1] if row_range else 0,
+                          method=METHODS[method])
+        self.method = method
         self.n, self.r, self.s = int(A.n), r, s     # n: this context's (local) rows, set below
         self._keep = [A, B, keep]
         n_loc = int(row_range[1] - row_range[0]) if row_range else int(A.n)

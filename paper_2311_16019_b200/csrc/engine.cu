@@ -31,6 +31,7 @@
 #include "sketch_pull.cuh"
 #include "comm.cuh"
 #include "proj_gpu.cuh"
+#include "full_arnoldi.cuh"
 
 using namespace sylv;
 
@@ -212,6 +213,8 @@ struct sylv_ctx {
   int64_t n_global = 0, row_begin = 0, row_end = 0;
   double* red = nullptr;        // multi-rank: reduced partials (k r^2 + r^2 per sequence)
   int R = 1, K = 1, dmax = 0, zeta = 8, chunk = 0, cflags = 0;
+  int method = SYLV_METHOD_SKETCHED;   // sylv_config.method
+  int RTn = 1, tpcN = 1, CCn = 1;      // full method: n-space Q^T w row chunks / tiles per CTA, Q c chunks
   int64_t n = 0, s = 0;
   double tol = 1e-6, rank_tol = 1e-12;
   int sm = 148;
@@ -421,23 +424,30 @@ void free_seq(Sequence& q) {
 
 // CholQR2 of the s x R block `in` (destroyed): q written to Q[:, col0:col0+R]
 // (column-major), R-factor tau (positive diagonal) to `tau_out` (device, R x R).
-void cholqr2(sylv_ctx* c, Sequence& q, double* in, int64_t col0, double* tau_out, int flag_slot,
-             cudaStream_t st) {
+// General form: `rows` x R row-major `in` (destroyed; q.w2 holds rows x R scratch) -> `out`
+// column-major with column stride out_ld.
+void cholqr2_into(sylv_ctx* c, Sequence& q, double* in, int64_t rows, double* out, int64_t out_ld,
+                  double* tau_out, int flag_slot, cudaStream_t st) {
   const int R = c->R;
-  const int gs = (int)std::min<int64_t>(c->G, (q.s + 255) / 256);
+  const int gs = (int)std::min<int64_t>(c->G, (rows + 255) / 256);
   double* ta = q.small;            // R^2
   double* tai = q.small + 64;      // R^2
   double* tbi = q.small + 128;     // R^2
   SYLV_DISPATCH_R(R, {
-    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, in, q.part_s);
+    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(rows, in, q.part_s);
     k_chol_small<R_><<<1, kSmallThreads, 0, st>>>(q.part_s, gs, ta, tai, nullptr, q.flags, flag_slot);
-    k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, in, tai, q.w2, 0);
-    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(q.s, q.w2, q.part_s);
+    k_rmul<R_><<<gs, kThreads, 0, st>>>(rows, in, tai, q.w2, 0);
+    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(rows, q.w2, q.part_s);
     k_chol_small<R_><<<1, kSmallThreads, 0, st>>>(q.part_s, gs, tau_out, tbi, ta, q.flags, flag_slot);
-    k_rmul<R_><<<gs, kThreads, 0, st>>>(q.s, q.w2, tbi, q.Q + col0 * q.s, q.s);
+    k_rmul<R_><<<gs, kThreads, 0, st>>>(rows, q.w2, tbi, out, out_ld);
   });
   count(c, 6);
   CK(cudaGetLastError());
+}
+
+void cholqr2(sylv_ctx* c, Sequence& q, double* in, int64_t col0, double* tau_out, int flag_slot,
+             cudaStream_t st) {
+  cholqr2_into(c, q, in, q.s, q.Q + col0 * q.s, q.s, tau_out, flag_slot, st);
 }
 
 // ---- 2.5-D TMA passes ------------------------------------------------------------------
@@ -868,16 +878,24 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   const int R = c->R, K = c->K;
   const int64_t blk = q.ld * R, sR = c->s * R, ldT = q.ldT;
   tr.mark("setup", c->st);
-  q.ring = dalloc<double>((size_t)(K + 1) * blk);
+  const bool sketched = c->method == SYLV_METHOD_SKETCHED;
+  const bool full = c->method == SYLV_METHOD_FULL;
+  q.ring = dalloc<double>((size_t)(K + 1) * blk);     // full method: the retained basis (d_max + 1 slots)
   q.Cdev = dalloc<double>(blk);
   if (A->kind == SYLV_OP_CSR) q.Yt = dalloc<double>(blk);
   if (A->kind == SYLV_OP_CSR && R % 2 == 0) q.Zaos = dalloc<double>((size_t)(c->n + 2 * q.gz) * R);
-  q.sk = dalloc<double>(sR);
-  q.skpart = dalloc<double>((size_t)c->nchunk * sR);
-  if (c->sk_pull && q.sp.b >= 64) build_pull_lists(c, q, c->st);
-  q.w = dalloc<double>(sR);
-  q.w2 = dalloc<double>(sR);
-  q.Q = dalloc<double>((size_t)c->s * ldT);
+  if (sketched) {
+    q.sk = dalloc<double>(sR);
+    q.skpart = dalloc<double>((size_t)c->nchunk * sR);
+    if (c->sk_pull && q.sp.b >= 64) build_pull_lists(c, q, c->st);
+    q.Q = dalloc<double>((size_t)c->s * ldT);
+  }
+  // w, w2: the s x R sketched block (sketched) / the n x R applied block (full method)
+  const int64_t wrows = full ? c->n : (sketched ? c->s : 0);
+  if (wrows) {
+    q.w = dalloc<double>((size_t)wrows * R);
+    q.w2 = dalloc<double>((size_t)wrows * R);
+  }
   q.Tdev = dalloc<double>((size_t)ldT * ldT);
   q.Rall = dalloc<double>((size_t)(c->dmax + 2) * R * R);
   q.Kc = dalloc<double>((size_t)(c->dmax + 1) * (1 + K) * R * R);
@@ -894,14 +912,16 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     CK(cudaEventCreateWithFlags(&q.ev_c2[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&q.ev_sk[i], cudaEventDisableTiming));
   }
-  q.cpart = dalloc<double>((size_t)c->RT * ldT * R);
-  q.csum = dalloc<double>(ldT * R);
-  q.c2 = dalloc<double>(ldT * R);
-  q.qcpart = dalloc<double>((size_t)c->CC * sR);
+  if (sketched || full) {
+    q.cpart = dalloc<double>((size_t)(full ? c->RTn : c->RT) * ldT * R);
+    q.csum = dalloc<double>(ldT * R);
+    q.c2 = dalloc<double>(ldT * R);
+    q.qcpart = dalloc<double>(full ? (size_t)c->CCn * c->n * R : (size_t)c->CC * sR);
+  }
   q.small = dalloc<double>(512);
   CK(cudaMemsetAsync(q.ring, 0, (size_t)(K + 1) * blk * sizeof(double), c->st));
   tr.mark("device allocations + memsets", c->st);
-  setup_tma(c, q);
+  if (!full) setup_tma(c, q);
   tr.mark("tensor maps", c->st);
   CK(cudaMemsetAsync(q.Tdev, 0, (size_t)ldT * ldT * sizeof(double), c->st));
   CK(cudaMemsetAsync(q.flags, 0, (c->dmax + 2) * sizeof(int), c->st));
@@ -942,6 +962,27 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   count(c, 2);
   CK(cudaGetLastError());
   tr.mark("C upload, SoA, halo, Gram", c->st);
+  if (!sketched) {
+    // Alg. 2 / full method, line 1: U_1 beta = C with beta = ell = R(C); no sketch, T = I
+    // (the unwhitened projection: M_U = H_d), R_1 = ell^{-1}; the full method stores U_1
+    // normalised in slot 1 (R_1 = I)
+    k_set_identity<<<(int)std::min<int64_t>(1024, (ldT * ldT + 255) / 256), 256, 0, c->st>>>(q.Tdev, ldT);
+    if (full) {
+      SYLV_DISPATCH_R(R, { k_soa_rmul_inplace<R_><<<c->sm * 4, kThreads, 0, c->st>>>(c->n, q.slot(1), q.ld, elli_d); });
+      k_set_identity<<<1, 64, 0, c->st>>>(q.Rall + R * R, R);
+      k_set_identity<<<1, 64, 0, c->st>>>(q.Rall, R);
+    } else {
+      CK(cudaMemcpyAsync(q.Rall + R * R, elli_d, R * R * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    }
+    count(c, full ? 4 : 1);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(q.ell, ell_d, R * R * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(q.flags_h, q.flags, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    std::memcpy(q.beta, q.ell, sizeof(q.beta));   // the projected right-hand side uses R(C)
+    if (q.flags_h[0]) throw Status{SYLV_E_INVALID, "C1 or C2 is rank deficient"};
+    return;
+  }
   launch_sketch(c, q, q.cdata(), R, nullptr, q.sk, c->st);
   if (c->comm) c->comm->allreduce(q.sk, (size_t)q.s * R, c->st, kChanSetup);
   CK(cudaGetLastError());
@@ -1064,15 +1105,15 @@ void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t 
   const int gw = (int)std::min<int64_t>(1024, (q.s * R + 255) / 256);
   SYLV_DISPATCH_R(R, {
     // pass A: c1 = Q^T w
-    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, q.s, m, q.w, c->tileQ, q.cpart);
+    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, q.s, q.s, m, q.w, c->tileQ, 1, q.cpart);
     k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.csum, nullptr);
     // w -= Q c1
-    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, q.s, m, q.csum, cols_per_chunk, q.qcpart);
+    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, q.s, q.s, m, q.csum, cols_per_chunk, q.qcpart);
     k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, q.s * R);
     // pass B: c2 = Q^T w, csum += c2
-    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, q.s, m, q.w, c->tileQ, q.cpart);
+    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, q.s, q.s, m, q.w, c->tileQ, 1, q.cpart);
     k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.c2, q.csum);
-    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, q.s, m, q.c2, cols_per_chunk, q.qcpart);
+    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, q.s, q.s, m, q.c2, cols_per_chunk, q.qcpart);
     k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, q.s * R);
   });
   count(c, 8);
@@ -1087,6 +1128,45 @@ void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t 
   CK(cudaGetLastError());
   if (timing) { CK(cudaEventRecord(t3.b, st)); c->timed.push_back(t3); }
   if (!sketch_on_side && st != c->st && st != c->st2) CK(cudaEventRecord(q.ev_sk[j % ne], st));   // w free
+}
+
+// Full Arnoldi (method 2), step j of one sequence on `st`: W~ = A U_j
+// (row-major n x R in q.w), block CGS2 against ALL retained blocks U_1..U_j (two sweeps of the
+// basis: c1 = U^T W~, W~ -= U c1, c2 = U^T W~, W~ -= U c2; h_{.,j} = c1 + c2), CholQR2 ->
+// U_{j+1} normalised into ring slot j+1 (SoA) and h_{j+1,j}; H column j mirrored to the host.
+void step_full(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
+  const int R = c->R, K = c->K;
+  const int64_t n = c->n;
+  const int m = j * R;
+  const double* Ub = q.slot(1);   // basis column (b-1) R + c at Ub + ((b-1) R + c) ld (no ring wrap)
+  const int ga = (int)std::min<int64_t>((int64_t)c->sm * 8, (n + kThreads - 1) / kThreads);
+  SYLV_DISPATCH_R(R, { k_apply_rowmajor<R_><<<ga, kThreads, 0, st>>>(q.op, q.slot(j), q.ld, q.w); });
+  const dim3 gq((m + kQtwCols - 1) / kQtwCols, c->RTn);
+  const int cpc = (m + c->CCn - 1) / c->CCn;
+  const int ncc = (m + cpc - 1) / cpc;
+  const dim3 gc((unsigned)((n + kThreads - 1) / kThreads), ncc);
+  const int64_t mR = (int64_t)m * R;
+  const int gr = (int)std::min<int64_t>(1024, (mR + 255) / 256);
+  const int gw = (int)std::min<int64_t>(4 * c->sm, (n * R + 255) / 256);
+  SYLV_DISPATCH_R(R, {
+    k_qtw<R_><<<gq, kThreads, 0, st>>>(Ub, n, q.ld, m, q.w, c->tileQ, c->tpcN, q.cpart);
+    k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RTn, mR, q.csum, nullptr);
+    k_qc_part<R_><<<gc, kThreads, 0, st>>>(Ub, n, q.ld, m, q.csum, cpc, q.qcpart);
+    k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, n * R);
+    k_qtw<R_><<<gq, kThreads, 0, st>>>(Ub, n, q.ld, m, q.w, c->tileQ, c->tpcN, q.cpart);
+    k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RTn, mR, q.c2, q.csum);
+    k_qc_part<R_><<<gc, kThreads, 0, st>>>(Ub, n, q.ld, m, q.c2, cpc, q.qcpart);
+    k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, n * R);
+  });
+  count(c, 9);
+  CK(cudaGetLastError());
+  double* tau = q.small + 384;
+  cholqr2_into(c, q, q.w, n, q.slot(j + 1), q.ld, tau, j + 1, st);
+  SYLV_DISPATCH_R(R, { k_full_hcol<R_><<<1, kSmallThreads, 0, st>>>(q.csum, tau, m, j, K, q.Hc, q.Rall, q.flags); });
+  count(c);
+  CK(cudaGetLastError());
+  const size_t hb = (size_t)(K + 1) * R * R;
+  CK(cudaMemcpyAsync(q.Hh + (size_t)j * hb, q.Hc + (size_t)j * hb, hb * sizeof(double), cudaMemcpyDeviceToHost, st));
 }
 
 // Host copy of the leading rows x rows block of T (upper triangular, column-major, ldT).
@@ -1153,7 +1233,13 @@ void enqueue_steps(sylv_ctx* c, int first, int last) {
   const char* sched_env = std::getenv("SYLV_SCHED");   // "overlap" | "phase" (tuning)
   const bool on_side = sched_env ? std::strcmp(sched_env, "overlap") == 0 : !c->seq[0].pl_list;
   for (int j = first; j <= last; ++j) {
-    if (serial) {
+    if (c->method == SYLV_METHOD_FULL) {          // comparison method: full Arnoldi
+      step_full(c, c->seq[0], j, c->st);
+      step_full(c, c->seq[1], j, serial ? c->st : c->st2);
+    } else if (c->method == SYLV_METHOD_TRUNCATED) {   // Alg. 2: the n-space passes only
+      step_passes(c, c->seq[0], j, c->st, false);
+      step_passes(c, c->seq[1], j, serial ? c->st : c->st2, false);
+    } else if (serial) {
       step_passes(c, c->seq[0], j, c->st, false);
       step_sketch(c, c->seq[0], j, c->st, c->st, false);
       step_passes(c, c->seq[1], j, c->st, false);
@@ -1370,15 +1456,19 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
   *out = c;
   const int r = cfg->r;
   if (!(r == 1 || r == 2 || r == 4 || r == 8)) return fail(c, SYLV_E_INVALID, "r must be 1, 2, 4 or 8");
-  if (cfg->k < 1 || cfg->k > kMaxK) return fail(c, SYLV_E_INVALID, "k must be in [1, 4]");
+  const int method = cfg->method;
+  if (method < SYLV_METHOD_SKETCHED || method > SYLV_METHOD_FULL) return fail(c, SYLV_E_INVALID, "unknown method");
+  const bool sketched = method == SYLV_METHOD_SKETCHED;
+  if (method != SYLV_METHOD_FULL && (cfg->k < 1 || cfg->k > kMaxK)) return fail(c, SYLV_E_INVALID, "k must be in [1, 4]");
   if (cfg->d_max < 1) return fail(c, SYLV_E_INVALID, "d_max must be >= 1");
-  if (cfg->zeta < 1 || cfg->s <= 0 || cfg->s % cfg->zeta) return fail(c, SYLV_E_INVALID, "s must be a positive multiple of zeta");
-  if (cfg->s < (int64_t)(cfg->d_max + 1) * r) return fail(c, SYLV_E_INVALID, "s must be >= (d_max+1) r");
+  if (sketched && (cfg->zeta < 1 || cfg->s <= 0 || cfg->s % cfg->zeta)) return fail(c, SYLV_E_INVALID, "s must be a positive multiple of zeta");
+  if (sketched && cfg->s < (int64_t)(cfg->d_max + 1) * r) return fail(c, SYLV_E_INVALID, "s must be >= (d_max+1) r");
+  if (method == SYLV_METHOD_FULL && nccl_comm) return fail(c, SYLV_E_INVALID, "the full method is single-rank only");
   if (A->n != B->n || A->n <= 0) return fail(c, SYLV_E_INVALID, "A and B must be n x n with equal n");
   Comm* comm = nccl_comm ? static_cast<sylv_comm*>(nccl_comm)->impl : nullptr;
   if (comm && (A->kind != B->kind || (A->kind != SYLV_OP_CSR && A->grid[0] != B->grid[0])))
     return fail(c, SYLV_E_INVALID, "sharded contexts need A and B of the same kind (and grid for stencils)");
-  if ((uint64_t)A->n * cfg->zeta >= (1ull << 32)) return fail(c, SYLV_E_INVALID, "n*zeta must be < 2^32");
+  if (sketched && (uint64_t)A->n * cfg->zeta >= (1ull << 32)) return fail(c, SYLV_E_INVALID, "n*zeta must be < 2^32");
   for (const sylv_operator* o : {A, B}) {
     if (o->kind == SYLV_OP_STENCIL2D || o->kind == SYLV_OP_STENCIL3D) {
       const int64_t N = o->grid[0];
@@ -1394,9 +1484,10 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     c->st = (cudaStream_t)stream;
     c->rst = c->st;
     c->R = r;
-    c->K = cfg->k;
+    c->method = method;
+    c->K = method == SYLV_METHOD_FULL ? cfg->d_max : cfg->k;   // full: every block is in the window
     c->dmax = cfg->d_max;
-    c->zeta = cfg->zeta;
+    c->zeta = sketched ? cfg->zeta : 8;
     c->n_global = A->n;
     c->row_begin = 0;
     c->row_end = A->n;
@@ -1426,7 +1517,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
       throw Status{SYLV_E_INVALID, "a row range needs a communicator"};
     }
     c->n = c->row_end - c->row_begin;
-    c->s = cfg->s;
+    c->s = sketched ? cfg->s : (int64_t)(cfg->d_max + 1) * r;   // unsketched: s only sizes unused scratch
     c->tol = cfg->tol;
     c->rank_tol = cfg->rank_tol > 0 ? cfg->rank_tol : 1e-12;
     c->chunk = cfg->chunk > 0 ? std::min(cfg->chunk, kMaxChunk) : std::min(cfg->k + 1, kMaxChunk);
@@ -1442,12 +1533,20 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     // Q c: (ceil(s/256) x CC) CTAs, ~4 per SM at the full width (each thread streams a row
     // of its column chunk with 8 loads in flight)
     c->CC = (int)std::max<int64_t>(1, std::min<int64_t>(16, (4 * c->sm + (c->s / 256)) / std::max<int64_t>(1, c->s / 256)));
+    if (method == SYLV_METHOD_FULL) {
+      // n-space Q^T w over the retained basis: ~2 CTAs per SM of row chunks, each `tpcN` tiles
+      const int64_t tiles = (c->n + c->tileQ - 1) / c->tileQ;
+      c->tpcN = (int)std::max<int64_t>(1, (tiles + 2 * c->sm - 1) / (2 * c->sm));
+      c->RTn = (int)((tiles + c->tpcN - 1) / c->tpcN);
+      c->CCn = 1;
+    }
     // sketch kernel: whole sketch column (s doubles) in shared memory per CTA
     c->sk_smem = (size_t)sketch_smem_doubles(c->s, c->zeta) * sizeof(double);
     int max_optin = 0;
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    if (c->sk_smem > (size_t)max_optin)
+    if (sketched && c->sk_smem > (size_t)max_optin)
       throw Status{SYLV_E_INVALID, "s too large: the sketch column (8 s bytes) must fit in shared memory"};
+    if (!sketched) c->sk_smem = 0;
     SYLV_DISPATCH_R(r, {
       CK(cudaFuncSetAttribute(k_sketch_cols<R_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sk_smem));
     });
@@ -1622,7 +1721,13 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
         }
     }
     c->y_d = approx_used ? -1 : d;   // an approximate Y is never kept as the solution of d
-    const double rh = rho_of(lrow, lcol);
+    double rh = rho_of(lrow, lcol);
+    if (c->method == SYLV_METHOD_TRUNCATED) {
+      // Alg. 2 line 12 / Prop. 3.2: rho = sqrt(dr) (||Y E_d g^T|| + ||h E_d^T Y||)
+      std::vector<double> zc((size_t)m * r, 0.0);
+      const double a = rho_of(lrow, zc), b = rho_of(zc, lcol);
+      rh = std::sqrt((double)m) * (a + b);
+    }
     if (rho) *rho = rh;
     if (rho_rel) *rho_rel = rh / bn;
     c->hist.emplace_back(d, rh / bn);
@@ -1677,7 +1782,24 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
       const bool dev_out = is_device_ptr(Xout[qi]);
       double* Xd = dev_out ? Xout[qi] : dalloc<double>((size_t)c->n * ldx);
       CK(cudaMemsetAsync(Xd, 0, (size_t)c->n * ldx * sizeof(double), c->st));
-      if (l > 0) {
+      if (l > 0 && c->method == SYLV_METHOD_FULL) {
+        // full method: the basis is retained and normalised (R_b = I, T = I): X = U_d Y_q,
+        // one DGEMM over the d contiguous ring slots (X^T += M^T U^T)
+        double* Md = dalloc<double>(M.size());
+        CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+        cublasHandle_t hb = (c->gsolve && c->gsolve->hb) ? c->gsolve->hb : c->blas;
+        if (!hb) {
+          if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw Status{SYLV_E_CUDA, "cublasCreate"};
+          hb = c->blas;
+        }
+        if (cublasSetStream(hb, c->st) != CUBLAS_STATUS_SUCCESS) throw Status{SYLV_E_CUDA, "cublasSetStream"};
+        const double one = 1.0;
+        if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, l, (int)c->n, m, &one, Md, l, q.slot(1), (int)q.ld, &one, Xd,
+                        (int)ldx) != CUBLAS_STATUS_SUCCESS)
+          throw Status{SYLV_E_CUDA, "cublasDgemm (X = U Y)"};
+        CK(cudaStreamSynchronize(c->st));
+        dfree(Md);
+      } else if (l > 0) {
         double* Md = dalloc<double>(M.size());
         double* rbuf = dalloc<double>((size_t)(K + C) * q.ld * r);
         CK(cudaMemsetAsync(rbuf, 0, (size_t)(K + C) * q.ld * r * sizeof(double), c->st));   // ghosts = 0
@@ -1971,6 +2093,7 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
 
 sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X, int32_t r, double* Yout) {
   if (!c || !X || !Yout || (which != 0 && which != 1)) return SYLV_E_INVALID;
+  if (c->method != SYLV_METHOD_SKETCHED) return fail(c, SYLV_E_STATE, "this context has no sketch (method 1 / 2)");
   if (!(r == 1 || r == 2 || r == 4 || r == 8)) return fail(c, SYLV_E_INVALID, "r must be 1, 2, 4 or 8");
   return guard(c, [&]() -> sylv_status {
     Sequence& q = c->seq[which];

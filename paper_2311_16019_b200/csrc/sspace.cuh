@@ -244,29 +244,36 @@ __global__ void __launch_bounds__(kThreads) k_rmul(int64_t rows, const double* _
 template <int R> constexpr int qtw_tile() { return 4096 / R; }   // rows per tile (w tile: 32 KB)
 constexpr int kQtwU = 4;                       // columns per warp and pass
 constexpr int kQtwCols = kWarps * kQtwU * 2;   // columns per CTA (two passes of the warps)
+// Q may be any column-major matrix of `s` rows with column stride ldq (the sketched basis:
+// ldq = s; the retained n-space basis of the full method: ldq = the SoA block stride).  A CTA
+// processes `tpc` consecutive row tiles of its row chunk (blockIdx.y), keeping its column sums
+// in registers across them, so the partials stay small when s is large.
 template <int R>
-__global__ void __launch_bounds__(kThreads, 2) k_qtw(const double* __restrict__ Q, int64_t s, int m,
-                                                  const double* __restrict__ w, int64_t tile,
+__global__ void __launch_bounds__(kThreads, 2) k_qtw(const double* __restrict__ Q, int64_t s, int64_t ldq, int m,
+                                                  const double* __restrict__ w, int64_t tile, int tpc,
                                                   double* __restrict__ partial) {
   __shared__ double ws[R][qtw_tile<R>() + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rt = blockIdx.y;
-  const int64_t r0 = (int64_t)rt * tile;
-  const int nr = (int)(tile < s - r0 ? tile : s - r0);
-  for (int e = threadIdx.x; e < nr * R; e += kThreads) ws[e % R][e / R] = __ldg(w + r0 * R + e);
-  __syncthreads();
-  const double* __restrict__ q0 = Q + r0;
   for (int pass = 0; pass < 2; ++pass) {
     const int j0 = blockIdx.x * kQtwCols + pass * kWarps * kQtwU + warp * kQtwU;
-    if (j0 >= m) break;
     double acc[kQtwU][R];
 #pragma unroll
     for (int u = 0; u < kQtwU; ++u)
 #pragma unroll
       for (int c = 0; c < R; ++c) acc[u][c] = 0.0;
+   for (int tt = 0; tt < tpc; ++tt) {
+    const int64_t r0 = ((int64_t)rt * tpc + tt) * tile;
+    if (r0 >= s) break;                                   // block-uniform
+    const int nr = (int)(tile < s - r0 ? tile : s - r0);
+    __syncthreads();                                      // previous tile's readers done
+    for (int e = threadIdx.x; e < nr * R; e += kThreads) ws[e % R][e / R] = __ldg(w + r0 * R + e);
+    __syncthreads();
+    if (j0 >= m) continue;                                // (no early exit: barriers above)
+    const double* __restrict__ q0 = Q + r0;
     const double* __restrict__ qc[kQtwU];
 #pragma unroll
-    for (int u = 0; u < kQtwU; ++u) qc[u] = q0 + (int64_t)min(j0 + u, m - 1) * s;   // clamped: zero-weighted below
+    for (int u = 0; u < kQtwU; ++u) qc[u] = q0 + (int64_t)min(j0 + u, m - 1) * ldq;   // clamped: zero-weighted below
     // 4 row strides of kQtwU loads in flight per warp (HBM latency x bandwidth)
     int row = lane;
     for (; row + 96 < nr; row += 128) {
@@ -295,6 +302,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_qtw(const double* __restrict__ 
         for (int u = 0; u < kQtwU; ++u) acc[u][c] = fma(qv[u], wv, acc[u][c]);
       }
     }
+   }
+    if (j0 >= m) continue;
 #pragma unroll
     for (int u = 0; u < kQtwU; ++u)
 #pragma unroll
@@ -327,7 +336,7 @@ __global__ void k_red_parts(const double* __restrict__ partial, int nparts, int6
 
 // partial2[(cc*s + row)*R + c] = sum_{j in chunk cc} Q[j*s + row] cvec[j*R + c]
 template <int R>
-__global__ void __launch_bounds__(kThreads) k_qc_part(const double* __restrict__ Q, int64_t s, int m,
+__global__ void __launch_bounds__(kThreads) k_qc_part(const double* __restrict__ Q, int64_t s, int64_t ldq, int m,
                                                       const double* __restrict__ cvec, int cols_per_chunk,
                                                       double* __restrict__ partial2) {
   constexpr int kStage = 256;
@@ -345,19 +354,19 @@ __global__ void __launch_bounds__(kThreads) k_qc_part(const double* __restrict__
     for (int e = threadIdx.x; e < nj * R; e += kThreads) cs[e] = cvec[(int64_t)jj * R + e];
     __syncthreads();
     if (row < s) {
-      const double* __restrict__ q = Q + (int64_t)jj * s + row;
+      const double* __restrict__ q = Q + (int64_t)jj * ldq + row;
       int t = 0;
       for (; t + 8 <= nj; t += 8) {          // 8 column loads in flight per thread
         double qv[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) qv[u] = __ldg(q + (int64_t)(t + u) * s);
+        for (int u = 0; u < 8; ++u) qv[u] = __ldg(q + (int64_t)(t + u) * ldq);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
 #pragma unroll
           for (int c = 0; c < R; ++c) acc[c] = fma(qv[u], cs[(t + u) * R + c], acc[c]);
       }
       for (; t < nj; ++t) {
-        const double qv = __ldg(q + (int64_t)t * s);
+        const double qv = __ldg(q + (int64_t)t * ldq);
 #pragma unroll
         for (int c = 0; c < R; ++c) acc[c] = fma(qv, cs[t * R + c], acc[c]);
       }
