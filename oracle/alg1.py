@@ -48,13 +48,20 @@ class Sequence:
     (s x (d+1)r, orthonormal) and T_{d+1} ((d+1)r square, upper triangular).
     """
 
-    def __init__(self, M, C: np.ndarray, S, k: int, keep_basis: bool = False):
+    def __init__(self, M, C: np.ndarray, S, k: int, keep_basis: bool = False, sketched_gs: bool = False):
         self.M, self.S, self.k = M, S, k
+        # f3 (P:1207): "use the sketched inner product also in the computation of the truncated
+        # bases": h_{i,d} = (S U_i)^T (S W~) and the new block S-orthonormal, (S U)^T (S U) = I
+        self.sketched_gs = sketched_gs
         self.n, self.r = C.shape
         self.C = np.array(C, dtype=np.float64)
         self.keep_basis = keep_basis
         # Alg. 1 line 1 (P:887): U_1 ell = C (skinny QR), Q_1 beta = S C.
-        U1, self.ell = qr_pos(self.C)
+        if sketched_gs:                                         # U_1 ell = C, S-orthonormal U_1
+            _, self.ell = qr_pos(np.asarray(S @ self.C))
+            U1 = sla.solve_triangular(self.ell, self.C.T, trans="T", lower=False).T
+        else:
+            U1, self.ell = qr_pos(self.C)
         _, self.beta = qr_pos(S @ self.C)
         # R3: T_1 = tau_1 = R(S U_1) (= beta ell^{-1}); the paper prints T_1 = beta.
         Q1, tau1 = qr_pos(np.asarray(S @ U1))
@@ -71,6 +78,8 @@ class Sequence:
         d = self.d + 1
         k, r = self.k, self.r
         W = np.asarray(self.M @ self.U[d])                      # line 3: W~ = A U_d
+        if self.sketched_gs:
+            return self._step_sketched_gs(d, W)
         self.Wnorm[d] = float(np.linalg.norm(W))
         for i in range(max(1, d - k + 1), d + 1):               # lines 4-7, R5 window
             h = self.U[i].T @ W                                 # h_{i,d} = U_i^T W~
@@ -80,6 +89,33 @@ class Sequence:
         self.H[(d + 1, d)] = hsub
         if np.min(np.abs(np.diag(hsub))) <= BREAKDOWN_RTOL * self.Wnorm[d]:
             self.breakdown = True
+        self._update_sketched_qr(d, Unew)
+
+    def _step_sketched_gs(self, d: int, W: np.ndarray) -> None:
+        """f3: lines 4-8 with the sketched inner product <x, y>_S = (S x)^T (S y): the
+        window blocks are S-orthonormal, h_{i,d} = (S U_i)^T (S W~) (MGS order), and
+        U_{d+1} h_{d+1,d} = W~ with (S U_{d+1})^T (S U_{d+1}) = I, i.e. h_{d+1,d} = R of the
+        positive-diagonal QR of S W~ (R10).  No inner product in R^n.  The breakdown test
+        (R11) measures W~ in the sketched norm."""
+        k = self.k
+        S = self.S
+        SW = np.asarray(S @ W)
+        self.Wnorm[d] = float(np.linalg.norm(SW))
+        for i in range(max(1, d - k + 1), d + 1):
+            SUi = np.asarray(S @ self.U[i])
+            h = SUi.T @ SW                                      # h_{i,d} = <U_i, W~>_S
+            W = W - self.U[i] @ h
+            SW = SW - SUi @ h
+            self.H[(i, d)] = h
+        _, hsub = qr_pos(np.asarray(S @ W))                     # S-normalisation of the new block
+        Unew = sla.solve_triangular(hsub, W.T, trans="T", lower=False).T
+        self.H[(d + 1, d)] = hsub
+        if np.min(np.abs(np.diag(hsub))) <= BREAKDOWN_RTOL * self.Wnorm[d]:
+            self.breakdown = True
+        self._update_sketched_qr(d, Unew)
+
+    def _update_sketched_qr(self, d: int, Unew: np.ndarray) -> None:
+        k, r = self.k, self.r
         # line 9 (P:897-898): Q_{d+1} T_{d+1} = S [U_d, U_{d+1}], update only (P:850-852).
         w = np.asarray(self.S @ Unew)
         c1 = self.Q.T @ w
@@ -136,7 +172,8 @@ class Sequence:
     # ---- second pass -----------------------------------------------------
     def replay(self, Z: np.ndarray, d: int) -> np.ndarray:
         """X = U_d Z regenerating U_1..U_d from C and the stored h_{i,j}: no inner
-        products.  U_1 = C ell^{-1}; U_{j+1} = (M U_j - sum U_i h_{i,j}) h_{j+1,j}^{-1}."""
+        products (P:926-928).  U_1 = C ell^{-1}; U_{j+1} = (M U_j - sum U_i h_{i,j}) h_{j+1,j}^{-1}
+        (the same for the sketched-GS basis: only the coefficients differ)."""
         r, k = self.r, self.k
         U = {1: sla.solve_triangular(self.ell, self.C.T, trans="T", lower=False).T}
         X = U[1] @ Z[0:r]
@@ -167,9 +204,9 @@ class CheckResult:
 class SylvesterSketchedKrylov:
     """Both sequences of Alg. 1 plus the projected solve, the check and the solution."""
 
-    def __init__(self, A, Bt, C1, C2, S_U, S_V, k: int):
-        self.U = Sequence(A, C1, S_U, k)
-        self.V = Sequence(Bt, C2, S_V, k)
+    def __init__(self, A, Bt, C1, C2, S_U, S_V, k: int, sketched_gs: bool = False):
+        self.U = Sequence(A, C1, S_U, k, sketched_gs=sketched_gs)
+        self.V = Sequence(Bt, C2, S_V, k, sketched_gs=sketched_gs)
         self.A, self.Bt = A, Bt
         self.C1, self.C2 = np.asarray(C1), np.asarray(C2)
         self.r = self.U.r
@@ -177,14 +214,14 @@ class SylvesterSketchedKrylov:
         self.d = 0
 
     @classmethod
-    def from_config(cls, cfg, C1=None, C2=None, csr_pair=None, keep_basis=False):
+    def from_config(cls, cfg, C1=None, C2=None, csr_pair=None, keep_basis=False, sketched_gs=False):
         from synth.inputs import make_rhs
         A, Bt, _ = operators.operator_pair(cfg, csr_pair)
         if C1 is None:
             C1, C2 = make_rhs(cfg)
         S_U = sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed_u)
         S_V = sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed_v)
-        obj = cls(A, Bt, C1, C2, S_U, S_V, cfg.k)
+        obj = cls(A, Bt, C1, C2, S_U, S_V, cfg.k, sketched_gs=sketched_gs)
         obj.U.keep_basis = obj.V.keep_basis = keep_basis
         obj.cfg = cfg
         return obj

@@ -357,3 +357,59 @@ def test_cond_T_equals_condition_of_the_sketched_basis():
         assert seq.cond_T(d) == pytest.approx(want, rel=1e-6)
         conds.append(want)
     assert conds[0] < conds[1] < conds[2]
+
+
+# ---- f3: sketched inner products inside the truncated Gram-Schmidt -------------------
+
+@pytest.mark.parametrize("k,r", [(2, 2), (3, 1)])
+def test_sketched_gs_basis_relations(k, r):
+    """Sketched-GS oracle: window blocks S-orthonormal ((S U_i)^T (S U_j) = delta_ij
+    inside the window), the truncated Arnoldi relation A U_d = U_{d+1} H_und_d (an
+    algebraic identity of the recurrence), Prop. 2.1 (S U = Q T), and rho equal to the
+    explicitly sketched residual ||S_U R S_V^T||_F (the whitened relations hold for any basis)."""
+    cfg, A, Bt, B, C1, C2 = _small(N=12, r=r, k=k, d_max=14)
+    d = 10
+    s = 8 * math.ceil(4 * (d + 1) * r / 8)
+    S_U = sparse_sign.matrix(cfg.n, s, 8, 11)
+    S_V = sparse_sign.matrix(cfg.n, s, 8, 12)
+    o = alg1.SylvesterSketchedKrylov(A, Bt, C1, C2, S_U, S_V, k=k, sketched_gs=True)
+    o.U.keep_basis = o.V.keep_basis = True
+    o.step(d)
+    U = np.concatenate([o.U.U[i] for i in range(1, d + 2)], axis=1)
+    SU = np.asarray(S_U @ U)
+    for j in range(1, d + 2):
+        for i in range(max(1, j - k + 1), j + 1):
+            G = SU[:, (i - 1) * r:i * r].T @ SU[:, (j - 1) * r:j * r]
+            assert np.allclose(G, np.eye(r) if i == j else 0.0, atol=1e-11)
+    # Euclidean orthonormality is NOT what this basis has
+    assert np.abs(o.U.U[d + 1].T @ o.U.U[d + 1] - np.eye(r)).max() > 1e-3
+    lhs = A @ U[:, :d * r]
+    assert np.linalg.norm(lhs - U @ o.U.Hbar(d)) <= 1e-11 * np.linalg.norm(lhs)
+    assert np.linalg.norm(o.U.Q @ o.U.T - SU) <= 1e-11 * np.linalg.norm(SU)
+    res = o.residual(d)
+    m = d * r
+    V = np.concatenate([o.V.U[i] for i in range(1, d + 1)], axis=1)
+    Uh = sla.solve_triangular(o.U.T[:m, :m], U[:, :m].T, trans="T", lower=False).T
+    Vh = sla.solve_triangular(o.V.T[:m, :m], V.T, trans="T", lower=False).T
+    X = Uh @ res.Y @ Vh.T
+    R = A @ X + (B.T @ X.T).T - C1 @ C2.T
+    assert res.rho == pytest.approx(np.linalg.norm(np.asarray(S_U @ (S_V @ R.T).T)), rel=1e-9)
+    X1, X2 = o.solution(d, res.Y, rank_tol=0.0)
+    assert np.linalg.norm(X1 @ X2.T - X) <= 1e-9 * np.linalg.norm(X)
+
+
+def test_sketched_gs_with_identity_sketch_is_galerkin():
+    """S = I, k >= d: the sketched inner product is the Euclidean one, the basis orthonormal, and
+    the method reduces to the full Arnoldi / Galerkin method: Y and rho equal the
+    oracle/alg2 full method's."""
+    from oracle import alg2
+    cfg, A, Bt, B, C1, C2 = _small(N=8, r=2, k=50, d_max=8)
+    d = 6
+    I = sp.identity(cfg.n, format="csr")
+    o = alg1.SylvesterSketchedKrylov(A, Bt, C1, C2, I, I, k=50, sketched_gs=True)
+    o.step(d)
+    f = alg2.TruncatedArnoldiSylvester(A, Bt, C1, C2, k=50, full=True)
+    f.step(d)
+    ro, rf = o.residual(d), f.residual(d)
+    assert ro.rho == pytest.approx(rf.rho, rel=1e-8)
+    assert np.linalg.norm(ro.Y - rf.Y) <= 1e-8 * np.linalg.norm(rf.Y)
