@@ -122,10 +122,14 @@ typedef struct {
                             2 = full Arnoldi / Galerkin (every block
                             retained and orthonormalised against all previous ones by
                             block CGS2; k is ignored (= d_max); exact residual norm;
-                            single-rank only; needs (d_max+1) n r doubles per sequence) */
+                            single-rank only; needs (d_max+1) n r doubles per sequence);
+                            3 = sketched-and-truncated with the sketched inner product also
+                            in the truncated Gram-Schmidt (h_{i,d} = (S U_i)^T
+                            (S W~), S-orthonormal blocks; no inner product over n, hence no
+                            n-space allreduce on several ranks) */
 } sylv_config;
 
-enum { SYLV_METHOD_SKETCHED = 0, SYLV_METHOD_TRUNCATED = 1, SYLV_METHOD_FULL = 2 };
+enum { SYLV_METHOD_SKETCHED = 0, SYLV_METHOD_TRUNCATED = 1, SYLV_METHOD_FULL = 2, SYLV_METHOD_SKETCHED_GS = 3 };
 
 /* Create a context and run Alg. 1 line 1: U1 ell = C1, V1 ell' = C2
  * (CholQR on the device), beta_1 = R(S_U C1), beta_2 = R(S_V C2), T_1 = tau_1 =

@@ -42,7 +42,7 @@ class Config(C.Structure):
                 ("row_begin", C.c_int64), ("row_end", C.c_int64), ("method", C.c_int32)]
 
 
-METHODS = {"sketched": 0, "truncated": 1, "full": 2}   # SYLV_METHOD_* (include/sylv_sketch.h)
+METHODS = {"sketched": 0, "truncated": 1, "full": 2, "sketched_gs": 3}   # SYLV_METHOD_* (include/sylv_sketch.h)
 
 
 class Stats(C.Structure):

@@ -32,6 +32,7 @@
 #include "comm.cuh"
 #include "proj_gpu.cuh"
 #include "full_arnoldi.cuh"
+#include "sketched_gs.cuh"
 
 using namespace sylv;
 
@@ -151,7 +152,8 @@ struct Sequence {
   // device
   double* ring = nullptr;     // (K+1) blocks, SoA R x ld
   double* Cdev = nullptr;     // SoA R x ld block (allocation; data at Cdev + gz)
-  double* Yt = nullptr;       // CSR: A Z_d (SoA)
+  double* Yt = nullptr;       // CSR / sketched GS: A Z_d (SoA)
+  double* skz = nullptr;      // sketched GS (f3): (K+1) ring of S Z_j, s x R row-major each
   double* Zaos = nullptr;     // CSR, r even: row-interleaved copy of Z_d for the pass-1 gathers
   double* sk = nullptr;       // s x R (row-major)
   double* skpart = nullptr;   // nchunk x R x s sketch partials
@@ -407,7 +409,7 @@ void free_seq(Sequence& q) {
   for (cudaEvent_t e : q.ev_c2) cudaEventDestroy(e);
   for (cudaEvent_t e : q.ev_sk) cudaEventDestroy(e);
   double* dp[] = {q.ring, q.Cdev, q.Yt, q.Zaos, q.sk, q.skpart, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
-                  q.part1, q.part2, q.part_s, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv};
+                  q.part1, q.part2, q.part_s, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv, q.skz};
   for (double* p : dp) dfree(p);
   dfree(q.flags);
   dfree(q.pl_list);
@@ -878,11 +880,13 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   const int R = c->R, K = c->K;
   const int64_t blk = q.ld * R, sR = c->s * R, ldT = q.ldT;
   tr.mark("setup", c->st);
-  const bool sketched = c->method == SYLV_METHOD_SKETCHED;
+  const bool sgs = c->method == SYLV_METHOD_SKETCHED_GS;
+  const bool sketched = c->method == SYLV_METHOD_SKETCHED || sgs;
   const bool full = c->method == SYLV_METHOD_FULL;
   q.ring = dalloc<double>((size_t)(K + 1) * blk);     // full method: the retained basis (d_max + 1 slots)
   q.Cdev = dalloc<double>(blk);
-  if (A->kind == SYLV_OP_CSR) q.Yt = dalloc<double>(blk);
+  if (A->kind == SYLV_OP_CSR || sgs) q.Yt = dalloc<double>(blk);
+  if (sgs) q.skz = dalloc<double>((size_t)(K + 1) * sR);
   if (A->kind == SYLV_OP_CSR && R % 2 == 0) q.Zaos = dalloc<double>((size_t)(c->n + 2 * q.gz) * R);
   if (sketched) {
     q.sk = dalloc<double>(sR);
@@ -987,7 +991,11 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   if (c->comm) c->comm->allreduce(q.sk, (size_t)q.s * R, c->st, kChanSetup);
   CK(cudaGetLastError());
   tr.mark("sketch of C", c->st);
+  // sketched GS (f3): S Z_1 = S C kept (the s-space ring), ell = R(S C) = beta, so U_1 = C beta^{-1}
+  // is S-orthonormal and T_1 = beta ell^{-1} = I
+  if (sgs) CK(cudaMemcpyAsync(q.skz + sR, q.sk, sR * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
   cholqr2(c, q, q.sk, 0, beta_d, 0, c->st);
+  if (sgs) CK(cudaMemcpyAsync(ell_d, beta_d, R * R * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
   SYLV_DISPATCH_R(R, { k_init_tau<R_><<<1, 1, 0, c->st>>>(beta_d, ell_d, q.Tdev, ldT, q.Rall + R * R); });
   count(c);
   CK(cudaGetLastError());
@@ -1004,6 +1012,8 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
 // step_sketch (line 9): the sketch of the new block on `st` (it reads the block just written
 // and the ring slot is rewritten only by a later pass on the same stream), then the sketch-space
 // QR update on `side`, which overlaps the next step's passes.
+void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st);
+
 void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, bool sketch_on_side) {
   const int R = c->R, K = c->K;
   const int nwin = std::min(K, j);
@@ -1094,7 +1104,15 @@ void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t 
   } else if (sketch_on_side && st != c->st && st != c->st2) {
     CK(cudaEventRecord(q.ev_sk[j % ne], st));                 // ring slot j+1 read
   }
-  // ---- a5: block CGS2 against Q (m = j R columns); CholQR2; T column
+  qr_update(c, q, j, st);
+  if (timing) { CK(cudaEventRecord(t3.b, st)); c->timed.push_back(t3); }
+  if (!sketch_on_side && st != c->st && st != c->st2) CK(cudaEventRecord(q.ev_sk[j % ne], st));   // w free
+}
+
+// a5 (Alg. 1 line 9): block CGS2 of w = S U_{j+1} (s x R, q.w) against Q (m = j R
+// columns), CholQR2 (positive diagonal) -> Q[:, m:m+R], T column [c1 + c2; tau] on `st`.
+void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
+  const int R = c->R;
   const int m = j * R;
   const dim3 gq((m + kQtwCols - 1) / kQtwCols, c->RT);
   const int cols_per_chunk = (m + c->CC - 1) / c->CC;
@@ -1126,8 +1144,57 @@ void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t 
   });
   count(c);
   CK(cudaGetLastError());
-  if (timing) { CK(cudaEventRecord(t3.b, st)); c->timed.push_back(t3); }
-  if (!sketch_on_side && st != c->st && st != c->st2) CK(cudaEventRecord(q.ev_sk[j % ne], st));   // w free
+}
+
+// Sketched inner products in the truncated GS (method 3, f3), step j of one
+// sequence: n-space apply + sketch of the matvec, s-space coefficients (no reduction over n),
+// the pass-2 update without Gram, s-space normalisation; the sketched QR update (a5) on `side`
+// (sketched_gs.cuh).
+void step_sgs(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t side) {
+  const int R = c->R, K = c->K;
+  const int nwin = std::min(K, j);
+  const int ne = K + 2;
+  const int64_t sR = q.s * R;
+  auto skz = [&](int i) { return q.skz + (int64_t)(i % (K + 1)) * sR; };
+  Win win{}, zs{};
+  for (int i = 0; i < nwin; ++i) {
+    win.p[i] = q.slot(j - nwin + 1 + i);
+    zs.p[i] = skz(j - nwin + 1 + i);
+  }
+  const int ga = (int)std::min<int64_t>((int64_t)c->sm * 8, (c->n + kThreads - 1) / kThreads);
+  SYLV_DISPATCH_R(R, { k_apply_soa<R_><<<ga, kThreads, 0, st>>>(q.op, q.slot(j), q.ld, q.Yt); });
+  count(c);
+  // the sketch buffer q.sk is reused every step: the previous step's s-space kernels ran on st
+  launch_sketch(c, q, q.Yt, R, nullptr, q.sk, st);
+  if (c->comm) c->comm->allreduce(q.sk, (size_t)sR, st, q.which == 0 ? kChanUMain : kChanVMain);
+  const int gs = (int)std::max<int64_t>(1, std::min<int64_t>(c->G, (q.s + kThreads - 1) / kThreads));
+  SYLV_DISPATCH_RK(R, K, {
+    k_skpass1<R_, K_><<<dim3(gs, K_ * R_), kThreads, 0, st>>>(zs, nwin, q.s, q.sk, q.part1);
+    k_coef1<R_, K_><<<1, kSmallThreads, 0, st>>>(q.part1, gs, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
+  });
+  count(c, 2);
+  const double* coef = q.Kc + (int64_t)j * (1 + K) * R * R;
+  launch_pass2<false>(c, q, win, nwin, j, q.Yt, coef, q.slot(j + 1), st);
+  if (c->comm) c->comm->halo(q.slot(j + 1), R, q.ld, q.gz, st, q.which == 0 ? kChanUMain : kChanVMain);
+  SYLV_DISPATCH_RK(R, K, {
+    k_skpass2<R_, K_><<<gs, kThreads, 0, st>>>(zs, nwin, q.s, q.sk, coef, skz(j + 1), q.part2);
+    k_coef2<R_, K_><<<1, kSmallThreads, 0, st>>>(q.part2, gs, j, q.Rall, q.Hc, q.hn2, q.flags);
+  });
+  count(c, 2);
+  CK(cudaGetLastError());
+  const size_t hb = (size_t)(K + 1) * R * R;
+  CK(cudaMemcpyAsync(q.Hh + (size_t)j * hb, q.Hc + (size_t)j * hb, hb * sizeof(double), cudaMemcpyDeviceToHost, st));
+  // w = S U_{j+1} = (S Z_{j+1}) R_{j+1}, once the previous QR update is done with w
+  if (j >= 2 && side != st) CK(cudaStreamWaitEvent(st, q.ev_sk[(j - 1) % ne], 0));
+  const int gw = (int)std::min<int64_t>(c->G, (q.s + 255) / 256);
+  SYLV_DISPATCH_R(R, { k_rmul<R_><<<gw, kThreads, 0, st>>>(q.s, skz(j + 1), q.Rall + (int64_t)(j + 1) * R * R, q.w, 0); });
+  count(c);
+  if (side != st) {
+    CK(cudaEventRecord(q.ev_c2[j % ne], st));
+    CK(cudaStreamWaitEvent(side, q.ev_c2[j % ne], 0));
+  }
+  qr_update(c, q, j, side);
+  if (side != st) CK(cudaEventRecord(q.ev_sk[j % ne], side));
 }
 
 // Full Arnoldi (method 2), step j of one sequence on `st`: W~ = A U_j
@@ -1233,7 +1300,10 @@ void enqueue_steps(sylv_ctx* c, int first, int last) {
   const char* sched_env = std::getenv("SYLV_SCHED");   // "overlap" | "phase" (tuning)
   const bool on_side = sched_env ? std::strcmp(sched_env, "overlap") == 0 : !c->seq[0].pl_list;
   for (int j = first; j <= last; ++j) {
-    if (c->method == SYLV_METHOD_FULL) {          // comparison method: full Arnoldi
+    if (c->method == SYLV_METHOD_SKETCHED_GS) {   // f3: sketched inner products in the GS
+      step_sgs(c, c->seq[0], j, c->st, serial ? c->st : c->st3);
+      step_sgs(c, c->seq[1], j, serial ? c->st : c->st2, serial ? c->st : c->st4);
+    } else if (c->method == SYLV_METHOD_FULL) {          // comparison method: full Arnoldi
       step_full(c, c->seq[0], j, c->st);
       step_full(c, c->seq[1], j, serial ? c->st : c->st2);
     } else if (c->method == SYLV_METHOD_TRUNCATED) {   // Alg. 2: the n-space passes only
@@ -1457,8 +1527,8 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
   const int r = cfg->r;
   if (!(r == 1 || r == 2 || r == 4 || r == 8)) return fail(c, SYLV_E_INVALID, "r must be 1, 2, 4 or 8");
   const int method = cfg->method;
-  if (method < SYLV_METHOD_SKETCHED || method > SYLV_METHOD_FULL) return fail(c, SYLV_E_INVALID, "unknown method");
-  const bool sketched = method == SYLV_METHOD_SKETCHED;
+  if (method < SYLV_METHOD_SKETCHED || method > SYLV_METHOD_SKETCHED_GS) return fail(c, SYLV_E_INVALID, "unknown method");
+  const bool sketched = method == SYLV_METHOD_SKETCHED || method == SYLV_METHOD_SKETCHED_GS;
   if (method != SYLV_METHOD_FULL && (cfg->k < 1 || cfg->k > kMaxK)) return fail(c, SYLV_E_INVALID, "k must be in [1, 4]");
   if (cfg->d_max < 1) return fail(c, SYLV_E_INVALID, "d_max must be >= 1");
   if (sketched && (cfg->zeta < 1 || cfg->s <= 0 || cfg->s % cfg->zeta)) return fail(c, SYLV_E_INVALID, "s must be a positive multiple of zeta");
