@@ -201,6 +201,18 @@ class CheckResult:
     seconds: float = 0.0
 
 
+def sketch_pair(cfg):
+    """(S_U, S_V) of a config: the hashed sparse-sign embeddings (R1, seeds seed_u / seed_v), or
+    the paper's SRDCT (R2) with the signs and rows synth/ draws from the same seeds."""
+    if getattr(cfg, "sketch", "sparse_sign") == "srdct":
+        from synth.inputs import srdct_rows, srdct_signs
+        from .srdct import SRDCT
+        return tuple(SRDCT(cfg.n, cfg.s, srdct_signs(cfg.n, sd), srdct_rows(cfg.n, cfg.s, sd))
+                     for sd in (cfg.seed_u, cfg.seed_v))
+    return (sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed_u),
+            sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed_v))
+
+
 class SylvesterSketchedKrylov:
     """Both sequences of Alg. 1 plus the projected solve, the check and the solution."""
 
@@ -219,8 +231,7 @@ class SylvesterSketchedKrylov:
         A, Bt, _ = operators.operator_pair(cfg, csr_pair)
         if C1 is None:
             C1, C2 = make_rhs(cfg)
-        S_U = sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed_u)
-        S_V = sparse_sign.matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed_v)
+        S_U, S_V = sketch_pair(cfg)
         obj = cls(A, Bt, C1, C2, S_U, S_V, cfg.k, sketched_gs=sketched_gs)
         obj.U.keep_basis = obj.V.keep_basis = keep_basis
         obj.cfg = cfg

@@ -43,6 +43,33 @@ def stencil_matrix(N: int, w, nu: float = 1.0) -> sp.csr_matrix:
     return sp.csr_matrix(A)
 
 
+def variable_fd_matrix(dim: int, N: int, nu: float, wfun) -> sp.csr_matrix:
+    """-nu Laplace + w . grad with a variable field w (the paper's Ex. 6.1 / 6.3
+    operators), centred differences, Dirichlet, h = 1/(N+1), x fastest: assembled as
+        A = nu L + sum_e diag(w_e(nodes)) D_e
+    with L the Kronecker-sum Laplacian (stencil_matrix with w = 0) and D_e the Kronecker
+    embedding of the 1-D central difference tridiag(-1, 0, 1) / (2h) along direction e.
+    (The GPU receives the same operator as a CSR matrix assembled point by point in synth/;
+    the pin test checks the two agree.)"""
+    h = 1.0 / (N + 1)
+    I = sp.identity(N, format="csr")
+    D1 = sp.diags([-np.ones(N - 1), np.ones(N - 1)], [-1, 1], shape=(N, N), format="csr") / (2 * h)
+    L = stencil_matrix(N, (0.0,) * dim, nu=nu)
+    g = np.arange(1, N + 1) * h
+    if dim == 2:
+        Y, X = np.meshgrid(g, g, indexing="ij")
+        w = wfun(X.ravel(), Y.ravel())
+        Ds = [sp.kron(I, D1), sp.kron(D1, I)]
+    else:
+        Z, Y, X = np.meshgrid(g, g, g, indexing="ij")
+        w = wfun(X.ravel(), Y.ravel(), Z.ravel())
+        Ds = [sp.kron(sp.kron(I, I), D1), sp.kron(sp.kron(I, D1), I), sp.kron(sp.kron(D1, I), I)]
+    A = L
+    for e in range(dim):
+        A = A + sp.diags(w[e]) @ Ds[e]
+    return sp.csr_matrix(A)
+
+
 def csr_from_triplet(trip, n: int) -> sp.csr_matrix:
     row_ptr, col, val = trip
     return sp.csr_matrix((val, col.astype(np.int64), row_ptr), shape=(n, n))
@@ -54,6 +81,10 @@ def operator_pair(cfg, csr_pair=None):
     if cfg.kind.startswith("stencil"):
         A = stencil_matrix(cfg.N, cfg.wA)
         B = stencil_matrix(cfg.N, cfg.wB)
+    elif getattr(cfg, "fd_dim", 0):
+        from synth.inputs import VELOCITY              # the problem's velocity fields (input data)
+        A = variable_fd_matrix(cfg.fd_dim, cfg.fd_N, cfg.nu, VELOCITY[cfg.wA_field])
+        B = variable_fd_matrix(cfg.fd_dim, cfg.fd_N, cfg.nu, VELOCITY[cfg.wB_field])
     else:
         if csr_pair is None:
             from synth.inputs import config_csr

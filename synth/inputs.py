@@ -44,6 +44,16 @@ class Config:
     seed_u: int = SKETCH_SEEDS[0]
     seed_v: int = SKETCH_SEEDS[1]
     tol: float = TOL
+    # paper workloads: variable-coefficient convection-diffusion assembled as
+    # CSR (kind 'csr'): fd_dim 2/3, N interior nodes per direction, viscosity nu, named
+    # velocity fields (VELOCITY below) for A and B
+    fd_dim: int = 0
+    fd_N: int = 0
+    nu: float = 1.0
+    wA_field: str = ""
+    wB_field: str = ""
+    sketch: str = "sparse_sign"     # or "srdct" (the paper's subsampled randomized DCT)
+    normalize_rhs: str = ""         # "" | "columns" (c1) | "unit" (each of C1, C2 to unit Frobenius norm)
 
     @property
     def dim(self) -> int:
@@ -71,8 +81,36 @@ CONFIGS = {
 }
 
 
+# Velocity fields of the paper's experiments (problem data, not the method): w(x, y[, z]) at the
+# grid points, arrays in, tuple of arrays out.
+VELOCITY = {
+    "ex61_A": lambda x, y: (np.ones_like(x), np.ones_like(x)),                       # w_A = (1, 1)
+    "ex61_B": lambda x, y: (3 * y * (1 - x ** 2), -2 * x * (1 - y ** 2)),            # w_B
+    "ex63_A": lambda x, y, z: (x * np.sin(x), y * np.cos(y), np.exp(z ** 2 - 1)),   # w_A
+    "ex63_B": lambda x, y, z: ((1 - x ** 2) * y * z, np.ones_like(x), np.exp(z)),   # w_B
+}
+
+
+def _paper_61(nu, N=300):
+    n = N * N
+    return Config(name=f"ex61_nu{nu:g}", kind="csr", n=n, r=1, k=10, d_max=600, s=1200, fd_dim=2, fd_N=N, nu=nu,
+                  wA_field="ex61_A", wB_field="ex61_B", sketch="srdct", normalize_rhs="unit")
+
+
+def _paper_63(N):
+    n = N ** 3
+    return Config(name=f"ex63_n{n}", kind="csr", n=n, r=1, k=3, d_max=250, s=500, fd_dim=3, fd_N=N, nu=0.005,
+                  wA_field="ex63_A", wB_field="ex63_B", sketch="srdct", normalize_rhs="unit")
+
+
+# The paper's own workloads (P:969-979 Ex. 6.1, table tab1:ex2; P:1120-1128 Ex. 6.3, table tab1:ex3):
+# seeded N(0,1) right-hand sides stand in for MATLAB rng('default') (d comparable qualitatively only).
+PAPER_CONFIGS = {c.name: c for c in [_paper_61(0.1), _paper_61(0.01), _paper_61(0.001)]
+                 + [_paper_63(N) for N in (50, 60, 70, 80, 90, 100)]}
+
+
 def get_config(name: str) -> Config:
-    return CONFIGS[name]
+    return CONFIGS[name] if name in CONFIGS else PAPER_CONFIGS[name]
 
 
 def make_rhs(cfg: Config) -> Tuple[np.ndarray, np.ndarray]:
@@ -84,6 +122,9 @@ def make_rhs(cfg: Config) -> Tuple[np.ndarray, np.ndarray]:
     if cfg.normalize_c:
         C1 /= np.linalg.norm(C1, axis=0, keepdims=True)
         C2 /= np.linalg.norm(C2, axis=0, keepdims=True)
+    if cfg.normalize_rhs == "unit":                   # P:977 (c1, c2 unit norm) / P:1122 (||c1 c2^T|| = 1)
+        C1 /= np.linalg.norm(C1)
+        C2 /= np.linalg.norm(C2)
     return np.ascontiguousarray(C1), np.ascontiguousarray(C2)
 
 
@@ -133,11 +174,65 @@ def banded_csr(n: int, nnz_off: int, band: int, seed: int):
     return row_ptr, allc.reshape(-1).astype(np.int32), np.ascontiguousarray(allv.reshape(-1))
 
 
+def fd_csr(dim: int, N: int, nu: float, field: str):
+    """Centred finite differences of L(u) = -nu Lap u + w . grad u (eq. condiff_op) on the
+    unit square / cube, N interior nodes per direction, h = 1/(N+1), homogeneous Dirichlet, x
+    fastest (R14), w = VELOCITY[field] evaluated at the node: row (i, j[, l]) has the diagonal
+    2 dim nu / h^2 and, per direction e, the neighbours -nu/h^2 -+ w_e / (2h) (minus side / plus
+    side).  Assembled stencil-point by stencil-point; returns the CSR triplet with sorted columns."""
+    h = 1.0 / (N + 1)
+    g = np.arange(1, N + 1) * h
+    if dim == 2:
+        Y, X = np.meshgrid(g, g, indexing="ij")      # row index = x + N y (x fastest)
+        coords = (X.ravel(), Y.ravel())
+        idx = [np.tile(np.arange(N), N), np.repeat(np.arange(N), N)]
+    else:
+        Z, Y, X = np.meshgrid(g, g, g, indexing="ij")
+        coords = (X.ravel(), Y.ravel(), Z.ravel())
+        idx = [np.tile(np.arange(N), N * N), np.tile(np.repeat(np.arange(N), N), N), np.repeat(np.arange(N), N * N)]
+    w = VELOCITY[field](*coords)
+    n = N ** dim
+    rows = np.arange(n, dtype=np.int64)
+    R, Cc, V = [rows], [rows], [np.full(n, 2.0 * dim * nu / h ** 2)]
+    stride = 1
+    for e in range(dim):
+        for sgn in (-1, 1):
+            ok = (idx[e] > 0) if sgn < 0 else (idx[e] < N - 1)
+            R.append(rows[ok])
+            Cc.append(rows[ok] + sgn * stride)
+            V.append(-nu / h ** 2 + sgn * w[e][ok] / (2 * h))
+        stride *= N
+    R, Cc, V = np.concatenate(R), np.concatenate(Cc), np.concatenate(V)
+    order = np.lexsort((Cc, R))
+    R, Cc, V = R[order], Cc[order], V[order]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(row_ptr, R + 1, 1)
+    return np.cumsum(row_ptr), Cc.astype(np.int32), np.ascontiguousarray(V)
+
+
 def config_csr(cfg: Config):
-    """(A, B) CSR triplets for a 'csr' config (seeds seed_a, seed_b)."""
+    """(A, B) CSR triplets for a 'csr' config: the banded random matrices (seeds seed_a, seed_b),
+    or the paper's variable-coefficient operators (fd_dim > 0)."""
+    if cfg.fd_dim:
+        return (fd_csr(cfg.fd_dim, cfg.fd_N, cfg.nu, cfg.wA_field),
+                fd_csr(cfg.fd_dim, cfg.fd_N, cfg.nu, cfg.wB_field))
     A = banded_csr(cfg.n, cfg.csr_nnz_off, cfg.csr_band, cfg.seed_a)
     B = banded_csr(cfg.n, cfg.csr_nnz_off, cfg.csr_band, cfg.seed_b)
     return A, B
+
+
+def srdct_signs(n: int, seed: int) -> np.ndarray:
+    """The Rademacher diagonal E of the SRDCT sketch: n signs +-1 (int8) from numpy
+    PCG64(seed + 7919).  A random number of the method, passed to both sides as an input."""
+    rng = np.random.Generator(np.random.PCG64(seed + 7919))
+    return np.where(rng.integers(0, 2, size=n) == 1, 1, -1).astype(np.int8)
+
+
+def srdct_rows(n: int, s: int, seed: int) -> np.ndarray:
+    """The row selection D of the SRDCT sketch: s distinct rows of [0, n), drawn with numpy
+    PCG64(seed) and sorted.  A random number of the method, passed to both sides as an input."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return np.sort(rng.choice(n, size=s, replace=False)).astype(np.int64)
 
 
 def small_config(kind="stencil2d", N=12, r=2, k=2, d_max=20, s: Optional[int] = None,
