@@ -127,7 +127,18 @@ typedef struct {
                             in the truncated Gram-Schmidt (h_{i,d} = (S U_i)^T
                             (S W~), S-orthonormal blocks; no inner product over n, hence no
                             n-space allreduce on several ranks) */
+  int32_t sketch_kind;   /* SYLV_SKETCH_*: 0 = hashed sparse sign (zeta nonzeros per
+                            column, seeds seed_u / seed_v; BASELINE); 1 = the paper's
+                            SRDCT S = sqrt(n/s) D N E (scale read as
+                            sqrt(n/s), R2): E = the n signs below (+-1),
+                            N = orthonormal DCT-II, D = the s rows below; single-rank */
+  const int8_t* srdct_signs_u;   /* SRDCT: n signs of E for S_U / S_V (host or device; */
+  const int8_t* srdct_signs_v;   /* copied at init)                                   */
+  const int64_t* srdct_rows_u;   /* SRDCT: s row indices of D in [0, n) for S_U / S_V  */
+  const int64_t* srdct_rows_v;
 } sylv_config;
+
+enum { SYLV_SKETCH_SPARSE_SIGN = 0, SYLV_SKETCH_SRDCT = 1 };
 
 enum { SYLV_METHOD_SKETCHED = 0, SYLV_METHOD_TRUNCATED = 1, SYLV_METHOD_FULL = 2, SYLV_METHOD_SKETCHED_GS = 3 };
 

@@ -39,7 +39,9 @@ class Config(C.Structure):
     _fields_ = [("r", C.c_int32), ("k", C.c_int32), ("d_max", C.c_int32), ("zeta", C.c_int32),
                 ("s", C.c_int64), ("seed_u", C.c_uint64), ("seed_v", C.c_uint64), ("tol", C.c_double),
                 ("rank_tol", C.c_double), ("chunk", C.c_int32), ("flags", C.c_int32),
-                ("row_begin", C.c_int64), ("row_end", C.c_int64), ("method", C.c_int32)]
+                ("row_begin", C.c_int64), ("row_end", C.c_int64), ("method", C.c_int32),
+                ("sketch_kind", C.c_int32), ("srdct_signs_u", C.c_void_p), ("srdct_signs_v", C.c_void_p),
+                ("srdct_rows_u", C.c_void_p), ("srdct_rows_v", C.c_void_p)]
 
 
 METHODS = {"sketched": 0, "truncated": 1, "full": 2, "sketched_gs": 3}   # SYLV_METHOD_* (include/sylv_sketch.h)
@@ -204,7 +206,7 @@ class SylvSketch:
                  rank_tol: float = 1e-12, chunk: int = 0, timing: bool = False, stream=None,
                  keep=None, serial: bool = False, tma: bool = True, comm: "Comm" = None,
                  proj: str = "auto", method: str = "sketched",
-                 row_range: Optional[Tuple[int, int]] = None):
+                 row_range: Optional[Tuple[int, int]] = None, srdct=None):
         self.lib = load_library()
         self.cfg = Config(r=r, k=k, d_max=d_max, zeta=zeta, s=s, seed_u=seed_u, seed_v=seed_v, tol=tol,
                           rank_tol=rank_tol, chunk=chunk, flags=(1 if timing else 0) | (2 if serial else 0) | (0 if tma else 4)
@@ -212,6 +214,15 @@ class SylvSketch:
                           row_begin=row_range[0] if row_range else 0, row_end=row_range[1] if row_range else 0,
                           method=METHODS[method])
         self.method = method
+        if srdct is not None:     # ((signs_u, rows_u), (signs_v, rows_v)): the SRDCT sketch
+            (su, ru), (sv, rv) = srdct
+            self._srdct = [np.ascontiguousarray(a, dtype=t) for a, t in
+                           ((su, np.int8), (sv, np.int8), (ru, np.int64), (rv, np.int64))]
+            if any(a.shape != (int(A.n),) for a in self._srdct[:2]) or any(a.shape != (s,) for a in self._srdct[2:]):
+                raise ValueError("SRDCT: n signs and s rows per sequence")
+            self.cfg.sketch_kind = 1
+            self.cfg.srdct_signs_u, self.cfg.srdct_signs_v, self.cfg.srdct_rows_u, self.cfg.srdct_rows_v = (
+                a.ctypes.data for a in self._srdct)
         self.n, self.r, self.s = int(A.n), r, s     # n: this context's (local) rows, set below
         self._keep = [A, B, keep]
         n_loc = int(row_range[1] - row_range[0]) if row_range else int(A.n)
@@ -425,6 +436,9 @@ def from_config(cfg, C1=None, C2=None, csr_pair=None, timing=False, stream=None,
         from synth.inputs import make_rhs
         C1, C2 = make_rhs(cfg)
     A, B, keep = operators_for(cfg, csr_pair)
+    if getattr(cfg, "sketch", "sparse_sign") == "srdct" and "srdct" not in kw:
+        from synth.inputs import srdct_rows, srdct_signs     # the sketch's random numbers (inputs)
+        kw["srdct"] = tuple((srdct_signs(cfg.n, sd), srdct_rows(cfg.n, cfg.s, sd)) for sd in (cfg.seed_u, cfg.seed_v))
     return SylvSketch(A, B, C1, C2, r=cfg.r, k=cfg.k, d_max=cfg.d_max, s=cfg.s, zeta=cfg.zeta,
                       seed_u=cfg.seed_u, seed_v=cfg.seed_v, tol=cfg.tol, timing=timing, stream=stream,
                       keep=keep, **kw)

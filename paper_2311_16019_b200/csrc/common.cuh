@@ -12,7 +12,8 @@
 namespace sylv {
 
 constexpr int kMaxR = 8;
-constexpr int kMaxK = 4;
+constexpr int kMaxK = 10;      // k <= 4 for every r; 5..10 for r <= 2 (generic passes)
+constexpr int kMaxKTma = 4;    // window blocks of the 2.5-D TMA passes
 constexpr int kThreads = 256;            // CTA size of the streaming kernels
 constexpr int kSmallThreads = 1024;      // CTA size of the one-CTA coefficient kernels (sspace.cuh)
 constexpr int kWarps = kThreads / 32;

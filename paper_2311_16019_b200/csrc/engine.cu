@@ -33,6 +33,7 @@
 #include "proj_gpu.cuh"
 #include "full_arnoldi.cuh"
 #include "sketched_gs.cuh"
+#include "srdct.cuh"
 
 using namespace sylv;
 
@@ -112,22 +113,25 @@ void dfree(void* p) {
     case 4: { constexpr int R_ = 4; __VA_ARGS__; } break;               \
     default: break;                                                     \
   }
+// K = 5..10 only for R <= 2 (the generic row kernels; the TMA / DMMA paths stay at K <= 4)
+#define SYLV_KCASE_SMALL_R(KK, ...) \
+    case KK: { constexpr int K_ = KK; if constexpr (R_ <= 2) { __VA_ARGS__; } } break;
+#define SYLV_KCASES(...)                                                \
+    case 1: { constexpr int K_ = 1; __VA_ARGS__; } break;               \
+    case 2: { constexpr int K_ = 2; __VA_ARGS__; } break;               \
+    case 3: { constexpr int K_ = 3; __VA_ARGS__; } break;               \
+    case 4: { constexpr int K_ = 4; __VA_ARGS__; } break;               \
+    SYLV_KCASE_SMALL_R(5, __VA_ARGS__)                                  \
+    SYLV_KCASE_SMALL_R(6, __VA_ARGS__)                                  \
+    SYLV_KCASE_SMALL_R(7, __VA_ARGS__)                                  \
+    SYLV_KCASE_SMALL_R(8, __VA_ARGS__)                                  \
+    SYLV_KCASE_SMALL_R(9, __VA_ARGS__)                                  \
+    SYLV_KCASE_SMALL_R(10, __VA_ARGS__)                                 \
+    default: break;
 #define SYLV_DISPATCH_R124_K(Rv, Kv, ...)                               \
-  SYLV_DISPATCH_R124(Rv, switch (Kv) {                                  \
-    case 1: { constexpr int K_ = 1; __VA_ARGS__; } break;               \
-    case 2: { constexpr int K_ = 2; __VA_ARGS__; } break;               \
-    case 3: { constexpr int K_ = 3; __VA_ARGS__; } break;               \
-    case 4: { constexpr int K_ = 4; __VA_ARGS__; } break;               \
-    default: break;                                                     \
-  })
+  SYLV_DISPATCH_R124(Rv, switch (Kv) { SYLV_KCASES(__VA_ARGS__) })
 #define SYLV_DISPATCH_RK(Rv, Kv, ...)                                   \
-  SYLV_DISPATCH_R(Rv, switch (Kv) {                                     \
-    case 1: { constexpr int K_ = 1; __VA_ARGS__; } break;               \
-    case 2: { constexpr int K_ = 2; __VA_ARGS__; } break;               \
-    case 3: { constexpr int K_ = 3; __VA_ARGS__; } break;               \
-    case 4: { constexpr int K_ = 4; __VA_ARGS__; } break;               \
-    default: break;                                                     \
-  })
+  SYLV_DISPATCH_R(Rv, switch (Kv) { SYLV_KCASES(__VA_ARGS__) })
 
 struct TimedPair {
   cudaEvent_t a, b;
@@ -138,9 +142,9 @@ struct TimedPair {
 
 struct Sequence {
   // 2.5-D TMA passes (3-D stencil, r = 8, even N): tensor maps of the ring slots
-  CUtensorMap mapH[kMaxK + 1];   // halo boxes
+  CUtensorMap mapH[kMaxKTma + 1];   // halo boxes
   bool fused = false;            // pass 2 fused with the old-block part of the next pass 1
-  CUtensorMap mapW[kMaxK + 1];   // window boxes
+  CUtensorMap mapW[kMaxKTma + 1];   // window boxes
   bool tma = false;
   St25 st25{};
   int which = 0;
@@ -154,6 +158,13 @@ struct Sequence {
   double* Cdev = nullptr;     // SoA R x ld block (allocation; data at Cdev + gz)
   double* Yt = nullptr;       // CSR / sketched GS: A Z_d (SoA)
   double* skz = nullptr;      // sketched GS (f3): (K+1) ring of S Z_j, s x R row-major each
+  // SRDCT sketch (f4, srdct.cuh): signs (n), selected rows (s), FFT buffers and plan
+  bool srdct = false;
+  double* sr_sign = nullptr;
+  int64_t* sr_rows = nullptr;
+  double* sr_v = nullptr;                 // R x n (Makhoul-ordered, signed columns)
+  cufftDoubleComplex* sr_V = nullptr;     // R x (n/2 + 1)
+  cufftHandle sr_plan = 0;
   double* Zaos = nullptr;     // CSR, r even: row-interleaved copy of Z_d for the pass-1 gathers
   double* sk = nullptr;       // s x R (row-major)
   double* skpart = nullptr;   // nchunk x R x s sketch partials
@@ -409,7 +420,11 @@ void free_seq(Sequence& q) {
   for (cudaEvent_t e : q.ev_c2) cudaEventDestroy(e);
   for (cudaEvent_t e : q.ev_sk) cudaEventDestroy(e);
   double* dp[] = {q.ring, q.Cdev, q.Yt, q.Zaos, q.sk, q.skpart, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
-                  q.part1, q.part2, q.part_s, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv, q.skz};
+                  q.part1, q.part2, q.part_s, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv, q.skz, q.sr_sign,
+                  q.sr_v};
+  if (q.sr_plan) cufftDestroy(q.sr_plan);
+  dfree(q.sr_rows);
+  dfree(q.sr_V);
   for (double* p : dp) dfree(p);
   dfree(q.flags);
   dfree(q.pl_list);
@@ -519,7 +534,9 @@ void set_smem25f(sylv_ctx* c) {
 // Set up the TMA path for sequence q if eligible: 3-D stencil, r = 4 or 8, even N.
 void setup_tma(sylv_ctx* c, Sequence& q) {
   q.tma = false;
-  if ((c->cflags & 4) || q.op.kind != kStencil3D || (c->R != 8 && c->R != 4) || (q.op.N & 1) || q.op.N < 2) return;
+  if ((c->cflags & 4) || q.op.kind != kStencil3D || (c->R != 8 && c->R != 4) || (q.op.N & 1) || q.op.N < 2 ||
+      c->K > kMaxKTma)
+    return;
   const int N = q.op.N;
   const int nz = (int)(q.n / ((int64_t)N * N));
   for (int j = 0; j <= c->K; ++j) {
@@ -728,6 +745,21 @@ void launch_pass2(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, con
 // S X for an SoA block -> w (s x R row-major) = (S X) M  (M = nullptr: identity)
 void launch_sketch(sylv_ctx* c, Sequence& q, const double* X, int R, const double* M, double* w, cudaStream_t st) {
   const int red_grid = (int)std::min<int64_t>(4 * c->sm, (q.s + 255) / 256);
+  if (q.srdct) {                                   // S = sqrt(n/s) D N E (srdct.cuh)
+    if (R != q.R) throw Status{SYLV_E_INVALID, "SRDCT: the sketched block must have r columns"};
+    SYLV_DISPATCH_R(R, {
+      k_srdct_pre<R_><<<(int)std::min<int64_t>(8 * c->sm, (c->n + 255) / 256), 256, 0, st>>>(c->n, X, q.ld, q.sr_sign,
+                                                                                             q.sr_v);
+    });
+    if (cufftSetStream(q.sr_plan, st) != CUFFT_SUCCESS || cufftExecD2Z(q.sr_plan, q.sr_v, q.sr_V) != CUFFT_SUCCESS)
+      throw Status{SYLV_E_CUDA, "cufftExecD2Z (SRDCT)"};
+    SYLV_DISPATCH_R(R, {
+      k_srdct_post<R_><<<(int)std::min<int64_t>(4 * c->sm, (q.s + 255) / 256), 256, 0, st>>>(c->n, q.s, q.sr_V,
+                                                                                             q.sr_rows, M, w);
+    });
+    count(c, 2);
+    return;
+  }
   if (q.pl_list) {
     const int nw = (int)(q.sp.zeta * q.pl_wpb);
     SYLV_DISPATCH_R(R, {
@@ -854,7 +886,7 @@ void shard_csr(sylv_ctx* c, Sequence& q) {
 }
 
 void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, bool transpose,
-                   const double* C, uint64_t seed) {
+                   const double* C, uint64_t seed, const int8_t* sr_sign, const int64_t* sr_rows) {
   InitTrace tr;
   q.which = which;
   q.R = c->R;
@@ -890,9 +922,35 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   if (A->kind == SYLV_OP_CSR && R % 2 == 0) q.Zaos = dalloc<double>((size_t)(c->n + 2 * q.gz) * R);
   if (sketched) {
     q.sk = dalloc<double>(sR);
-    q.skpart = dalloc<double>((size_t)c->nchunk * sR);
-    if (c->sk_pull && q.sp.b >= 64) build_pull_lists(c, q, c->st);
     q.Q = dalloc<double>((size_t)c->s * ldT);
+    if (sr_sign) {
+      // SRDCT (f4): signs -> doubles, rows (checked), cuFFT D2Z plan batched over the R columns
+      q.srdct = true;
+      std::vector<int8_t> sg((size_t)c->n);
+      std::vector<int64_t> rw((size_t)c->s);
+      CK(cudaMemcpy(sg.data(), sr_sign, (size_t)c->n, is_device_ptr(sr_sign) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+      CK(cudaMemcpy(rw.data(), sr_rows, (size_t)c->s * sizeof(int64_t),
+                    is_device_ptr(sr_rows) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+      std::vector<double> sd((size_t)c->n);
+      for (int64_t i = 0; i < c->n; ++i) {
+        if (sg[i] != 1 && sg[i] != -1) throw Status{SYLV_E_INVALID, "SRDCT signs must be +1 or -1"};
+        sd[i] = (double)sg[i];
+      }
+      for (int64_t v : rw)
+        if (v < 0 || v >= c->n) throw Status{SYLV_E_INVALID, "SRDCT rows must lie in [0, n)"};
+      q.sr_sign = dalloc<double>(c->n);
+      q.sr_rows = reinterpret_cast<int64_t*>(dalloc<double>(c->s));
+      q.sr_v = dalloc<double>((size_t)c->n * R);
+      q.sr_V = reinterpret_cast<cufftDoubleComplex*>(dalloc<double>((size_t)2 * (c->n / 2 + 1) * R));
+      CK(cudaMemcpy(q.sr_sign, sd.data(), (size_t)c->n * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(q.sr_rows, rw.data(), (size_t)c->s * sizeof(int64_t), cudaMemcpyHostToDevice));
+      int nn = (int)c->n;
+      if (cufftPlanMany(&q.sr_plan, 1, &nn, nullptr, 1, nn, nullptr, 1, nn / 2 + 1, CUFFT_D2Z, R) != CUFFT_SUCCESS)
+        throw Status{SYLV_E_CUDA, "cufftPlanMany (SRDCT)"};
+    } else {
+      q.skpart = dalloc<double>((size_t)c->nchunk * sR);
+      if (c->sk_pull && q.sp.b >= 64) build_pull_lists(c, q, c->st);
+    }
   }
   // w, w2: the s x R sketched block (sketched) / the n x R applied block (full method)
   const int64_t wrows = full ? c->n : (sketched ? c->s : 0);
@@ -1529,16 +1587,24 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
   const int method = cfg->method;
   if (method < SYLV_METHOD_SKETCHED || method > SYLV_METHOD_SKETCHED_GS) return fail(c, SYLV_E_INVALID, "unknown method");
   const bool sketched = method == SYLV_METHOD_SKETCHED || method == SYLV_METHOD_SKETCHED_GS;
-  if (method != SYLV_METHOD_FULL && (cfg->k < 1 || cfg->k > kMaxK)) return fail(c, SYLV_E_INVALID, "k must be in [1, 4]");
+  if (method != SYLV_METHOD_FULL && (cfg->k < 1 || cfg->k > (r <= 2 ? kMaxK : 4)))
+    return fail(c, SYLV_E_INVALID, "k must be in [1, 4] (r = 4, 8) or [1, 10] (r = 1, 2)");
   if (cfg->d_max < 1) return fail(c, SYLV_E_INVALID, "d_max must be >= 1");
-  if (sketched && (cfg->zeta < 1 || cfg->s <= 0 || cfg->s % cfg->zeta)) return fail(c, SYLV_E_INVALID, "s must be a positive multiple of zeta");
+  const bool srdct = cfg->sketch_kind == SYLV_SKETCH_SRDCT;
+  if (cfg->sketch_kind != SYLV_SKETCH_SPARSE_SIGN && !srdct) return fail(c, SYLV_E_INVALID, "unknown sketch kind");
+  if (srdct && (!cfg->srdct_signs_u || !cfg->srdct_signs_v || !cfg->srdct_rows_u || !cfg->srdct_rows_v))
+    return fail(c, SYLV_E_INVALID, "SRDCT: signs and rows of both sketches are required");
+  if (srdct && nccl_comm) return fail(c, SYLV_E_INVALID, "SRDCT: single-rank only (the DCT mixes all rows)");
+  if (srdct && A->n > INT32_MAX) return fail(c, SYLV_E_INVALID, "SRDCT: n must fit the FFT length");
+  if (sketched && !srdct && (cfg->zeta < 1 || cfg->s <= 0 || cfg->s % cfg->zeta)) return fail(c, SYLV_E_INVALID, "s must be a positive multiple of zeta");
+  if (srdct && (cfg->s <= 0 || cfg->s > A->n)) return fail(c, SYLV_E_INVALID, "SRDCT: 0 < s <= n");
   if (sketched && cfg->s < (int64_t)(cfg->d_max + 1) * r) return fail(c, SYLV_E_INVALID, "s must be >= (d_max+1) r");
   if (method == SYLV_METHOD_FULL && nccl_comm) return fail(c, SYLV_E_INVALID, "the full method is single-rank only");
   if (A->n != B->n || A->n <= 0) return fail(c, SYLV_E_INVALID, "A and B must be n x n with equal n");
   Comm* comm = nccl_comm ? static_cast<sylv_comm*>(nccl_comm)->impl : nullptr;
   if (comm && (A->kind != B->kind || (A->kind != SYLV_OP_CSR && A->grid[0] != B->grid[0])))
     return fail(c, SYLV_E_INVALID, "sharded contexts need A and B of the same kind (and grid for stencils)");
-  if (sketched && (uint64_t)A->n * cfg->zeta >= (1ull << 32)) return fail(c, SYLV_E_INVALID, "n*zeta must be < 2^32");
+  if (sketched && !srdct && (uint64_t)A->n * cfg->zeta >= (1ull << 32)) return fail(c, SYLV_E_INVALID, "n*zeta must be < 2^32");
   for (const sylv_operator* o : {A, B}) {
     if (o->kind == SYLV_OP_STENCIL2D || o->kind == SYLV_OP_STENCIL3D) {
       const int64_t N = o->grid[0];
@@ -1557,7 +1623,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     c->method = method;
     c->K = method == SYLV_METHOD_FULL ? cfg->d_max : cfg->k;   // full: every block is in the window
     c->dmax = cfg->d_max;
-    c->zeta = sketched ? cfg->zeta : 8;
+    c->zeta = (sketched && cfg->sketch_kind == SYLV_SKETCH_SPARSE_SIGN) ? cfg->zeta : 8;
     c->n_global = A->n;
     c->row_begin = 0;
     c->row_end = A->n;
@@ -1614,7 +1680,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     c->sk_smem = (size_t)sketch_smem_doubles(c->s, c->zeta) * sizeof(double);
     int max_optin = 0;
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    if (sketched && c->sk_smem > (size_t)max_optin)
+    if (sketched && cfg->sketch_kind == SYLV_SKETCH_SPARSE_SIGN && c->sk_smem > (size_t)max_optin)
       throw Status{SYLV_E_INVALID, "s too large: the sketch column (8 s bytes) must fit in shared memory"};
     if (!sketched) c->sk_smem = 0;
     SYLV_DISPATCH_R(r, {
@@ -1639,8 +1705,11 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
     for (cudaEvent_t& e : c->join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (cudaEvent_t& e : c->phase) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    init_sequence(c, c->seq[0], 0, A, false, C1, cfg->seed_u);
-    init_sequence(c, c->seq[1], 1, B, true, C2, cfg->seed_v);
+    const bool srdct = cfg->sketch_kind == SYLV_SKETCH_SRDCT;
+    init_sequence(c, c->seq[0], 0, A, false, C1, cfg->seed_u, srdct ? cfg->srdct_signs_u : nullptr,
+                  srdct ? cfg->srdct_rows_u : nullptr);
+    init_sequence(c, c->seq[1], 1, B, true, C2, cfg->seed_v, srdct ? cfg->srdct_signs_v : nullptr,
+                  srdct ? cfg->srdct_rows_v : nullptr);
     return SYLV_OK;
   });
 }

@@ -45,7 +45,7 @@ constexpr int stages25() { return R >= 8 ? 3 : 4; }
 
 struct Tma25 {
   CUtensorMap zd;                // halo box map of Z_d's ring slot
-  CUtensorMap win[kMaxK];        // window-box maps of the window blocks, oldest first
+  CUtensorMap win[kMaxKTma];     // window-box maps of the window blocks, oldest first
 };
 
 struct St25 {

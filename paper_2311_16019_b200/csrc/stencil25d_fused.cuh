@@ -32,8 +32,8 @@ struct Geo25x {
 
 struct Tma25F {
   CUtensorMap zd;                // halo box (38 wide) of Z_d
-  CUtensorMap hx[kMaxK];         // extra halo boxes (Z_d's geometry) of the A^T window blocks, oldest first
-  CUtensorMap win[kMaxK];        // window boxes of the other window blocks, oldest first
+  CUtensorMap hx[kMaxKTma];         // extra halo boxes (Z_d's geometry) of the A^T window blocks, oldest first
+  CUtensorMap win[kMaxKTma];        // window boxes of the other window blocks, oldest first
 };
 
 template <int TY, int R, int K>

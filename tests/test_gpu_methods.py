@@ -250,3 +250,54 @@ def test_sketched_gs_sharded_equals_unsharded(kind, P):
         Dc = max(d for d in range(1, D + 1) if want[d - 1] >= 1e-9)
         m = (Dc + 1) * cfg.r
         assert np.linalg.norm(T[:m, :m] - Tw[:m, :m]) <= 1e-9 * np.linalg.norm(Tw[:m, :m])
+
+
+# ---- f4: the paper's workloads (variable-coefficient operators as CSR, k up to 10, SRDCT) -----
+
+def _paper_small(name, **kw):
+    return inputs.get_config(name).replace(**kw)
+
+
+@pytest.mark.parametrize("n,s", [(4096, 400), (90000, 1200), (20011, 500)])
+def test_srdct_sketch_of_fixed_block(n, s):
+    """S X on the GPU (cuFFT DCT-II + the selected rows) vs the oracle's scipy DCT (R2)."""
+    import paper_2311_16019_b200 as pkg
+    from oracle.srdct import SRDCT
+    N = int(round(n ** 0.5))
+    cfg = (inputs.get_config("ex61_nu0.1").replace(fd_N=N, n=N * N, s=s, d_max=s // 2 - 1)
+           if N * N == n else inputs.small_config("csr", n=n, r=1, k=2, d_max=s // 2 - 1, s=s, sketch="srdct"))
+    csr = inputs.config_csr(cfg)
+    C1, C2 = inputs.make_rhs(cfg)
+    gpu = pkg.from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr,
+                          stream=torch.cuda.current_stream().cuda_stream)
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((cfg.n, 1))
+    for which, sd in ((0, cfg.seed_u), (1, cfg.seed_v)):
+        S = SRDCT(cfg.n, s, inputs.srdct_signs(cfg.n, sd), inputs.srdct_rows(cfg.n, s, sd))
+        got = gpu.apply_sketch(which, torch.from_numpy(X).cuda())
+        want = S @ X
+        assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+    gpu.close()
+
+
+@pytest.mark.parametrize("case", [
+    dict(name="ex61_nu0.01", fd_N=45, n=45 * 45, s=480, d_max=100, k=10),                 # k = 10, SRDCT
+    dict(name="ex61_nu0.1", fd_N=40, n=1600, s=400, d_max=100, k=7, sketch="sparse_sign"),  # k = 7, sparse sign
+    dict(name="ex63_n125000", fd_N=14, n=14 ** 3, s=400, d_max=90, k=3),                  # 3-D variable w, SRDCT
+])
+def test_paper_workload_rho_matches_oracle(case):
+    import paper_2311_16019_b200 as pkg
+    case = dict(case)
+    cfg = _paper_small(case.pop("name"), **case)
+    csr = inputs.config_csr(cfg)
+    C1, C2 = inputs.make_rhs(cfg)
+    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2)
+    gpu = pkg.from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr,
+                          stream=torch.cuda.current_stream().cuda_stream)
+    D = 40
+    gpu.step(D)
+    orc.step(D)
+    bad = [(d, gpu.residual(d)[1], orc.residual(d).rho_rel) for d in range(1, D + 1)]
+    bad = [b for b in bad if not _rho_close(b[1], b[2])]
+    assert not bad, bad[:5]
+    gpu.close()
