@@ -2164,13 +2164,37 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
   // rho_rel monotone on the bracket this returns the same d* as bisection
   // the projected solution of the best passing check so far (host-solved checks), so the
   // final d* need not be solved again (c1: one m ~ 3100 solve ~ 12 s)
+  // (host-solved checks: a host copy of Y; device-solved checks: a device copy of the solver's Y)
   std::vector<double> best_Y;
   int best_d = -1;
+  bool best_on_dev = false;
+  struct DevBuf {
+    double* p = nullptr;
+    size_t cap = 0;
+    ~DevBuf() { dfree(p); }
+  } best_dev;
   auto keep_if_pass = [&](int d) {
-    if (c->y_d == d && !c->y_dev) {
+    if (c->y_d != d) return;
+    if (!c->y_dev) {
       best_Y = c->Y;
-      best_d = d;
+      best_on_dev = false;
+    } else {
+      const size_t mm = (size_t)d * c->R * d * c->R;
+      const sylv_status st = guard(c, [&]() -> sylv_status {
+        if (best_dev.cap < mm) {
+          dfree(best_dev.p);
+          best_dev.p = nullptr;
+          best_dev.p = dalloc<double>(mm);
+          best_dev.cap = mm;
+        }
+        CK(cudaMemcpyAsync(best_dev.p, c->gsolve->C, mm * sizeof(double), cudaMemcpyDeviceToDevice, c->rst));
+        CK(cudaStreamSynchronize(c->rst));
+        return SYLV_OK;
+      });
+      if (st != SYLV_OK) return;      // not kept: d* is re-solved at the end
+      best_on_dev = true;
     }
+    best_d = d;
   };
   keep_if_pass(d_pass);
   int lo = d_fail, hi = d_pass;
@@ -2216,10 +2240,18 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     slow = (2 * (hi - lo) > width) ? slow + 1 : 0;
   }
   if (c->y_d != hi) {
-    if (best_d == hi) {                 // restore the kept solution of d*
+    if (best_d == hi && !best_on_dev) {   // restore the kept solution of d* (no re-solve)
       c->Y.swap(best_Y);
       c->y_d = hi;
       c->y_dev = false;
+    } else if (best_d == hi && guard(c, [&]() -> sylv_status {
+                 const size_t mm = (size_t)hi * c->R * hi * c->R;
+                 CK(cudaMemcpyAsync(c->gsolve->C, best_dev.p, mm * sizeof(double), cudaMemcpyDeviceToDevice, c->rst));
+                 CK(cudaStreamSynchronize(c->rst));
+                 return SYLV_OK;
+               }) == SYLV_OK) {
+      c->y_d = hi;
+      c->y_dev = true;
     } else {
       double rho, rr;
       sylv_sketch_residual(c, hi, &rho, &rr);
@@ -2232,7 +2264,8 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
 
 sylv_status sylv_sketch_apply_sketch(sylv_ctx* c, int32_t which, const double* X, int32_t r, double* Yout) {
   if (!c || !X || !Yout || (which != 0 && which != 1)) return SYLV_E_INVALID;
-  if (c->method != SYLV_METHOD_SKETCHED) return fail(c, SYLV_E_STATE, "this context has no sketch (method 1 / 2)");
+  if (c->method == SYLV_METHOD_TRUNCATED || c->method == SYLV_METHOD_FULL)
+    return fail(c, SYLV_E_STATE, "this context has no sketch (method 1 / 2)");
   if (!(r == 1 || r == 2 || r == 4 || r == 8)) return fail(c, SYLV_E_INVALID, "r must be 1, 2, 4 or 8");
   return guard(c, [&]() -> sylv_status {
     Sequence& q = c->seq[which];
