@@ -50,7 +50,9 @@ def _context(cfg, csr):
     return g, C1, C2
 
 
-CFGS = ["c0", "c1", "c2", "c3", "c4"]
+CFGS = ["c0", "c1", "c2", "c3", "c4",
+        # the paper's own workloads (f4: Ex. 6.1, 6.3 with the SRDCT, R24-R26)
+        "ex61_nu0.1", "ex61_nu0.01", "ex61_nu0.001", "ex63_n125000"]
 
 
 @pytest.mark.parametrize("name", CFGS)
