@@ -82,10 +82,12 @@ def lapack_path() -> str:
 
 
 def load_library(path: str = LIB_PATH):
-    """Load libsylvsketch.so (no fallback: raises if absent)."""
+    """Load libsylvsketch.so (no fallback: raises if absent).  SYLV_LIB_PATH: a development
+    A/B build of the same library (build.build(out=..., extra=[...]))."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("SYLV_LIB_PATH", path)
     if not os.path.exists(path):
         raise SylvError(3, f"{path} missing: run `python -m paper_2311_16019_b200.build` "
                            "(or __graft_entry__.build())")

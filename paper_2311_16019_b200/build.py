@@ -31,17 +31,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in SOURCES + HEADERS + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = None, extra=()) -> str:
+    """Build the library (out / extra nvcc flags: development A/B variants, e.g.
+    build(out="build_ab/libsylvsketch_ns2.so", extra=["-DSYLV_ST25_NS8=2"]))."""
+    lib = os.path.abspath(out) if out else LIB
+    if not force and not out and up_to_date():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-cudart", "static", "-o", tmp, *SOURCES, "-ldl",
+    os.makedirs(os.path.dirname(os.path.abspath(lib)), exist_ok=True)
+    tmp = lib + ".tmp"
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-shared", "-cudart", "static", "-o", tmp, *SOURCES, "-ldl",
            "-L/usr/local/cuda/lib64", "-lcublas", "-lcusolver", "-lcufft", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=HERE)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

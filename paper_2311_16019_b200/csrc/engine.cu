@@ -667,7 +667,7 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cud
     const bool one = q.fused && j >= 2;
     const Tma25 tm = tma_args(q, j, one ? 1 : nwin);
     const int nw1 = one ? 1 : nwin, slot0 = one ? nwin - 1 : -1;
-#define SYLV_ST3D_P1(RR, KK) k_st3d<kTY25, RR, KK, 1, false><<<c->G25, 32 * kTY25, c->smem25_1, st>>>(tm, q.st25, nw1, nullptr, nullptr, q.part1, slot0)
+#define SYLV_ST3D_P1(RR, KK) k_st3d<kTY25, RR, KK, 1, false><<<c->G25, 32 * kTY25 * kWpl25, c->smem25_1, st>>>(tm, q.st25, nw1, nullptr, nullptr, q.part1, slot0)
     if (R == 8) {
       switch (K) {
         case 1: SYLV_ST3D_P1(8, 1); break;
@@ -710,7 +710,7 @@ void launch_pass2(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, con
   const int R = c->R, K = c->K;
   if (q.tma && allow_tma) {
     const Tma25 tm = tma_args(q, j, nwin);
-#define SYLV_ST3D_P2(RR, KK) k_st3d<kTY25, RR, KK, 2, GRAM><<<c->G25, 32 * kTY25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2)
+#define SYLV_ST3D_P2(RR, KK) k_st3d<kTY25, RR, KK, 2, GRAM><<<c->G25, 32 * kTY25 * kWpl25, c->smem25_2, st>>>(tm, q.st25, nwin, coef, out, q.part2)
     if (R == 8) {
       switch (K) {
         case 1: SYLV_ST3D_P2(8, 1); break;
@@ -1970,7 +1970,7 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
               Tma25 tm;
               tm.zd = rmapH[jp % (K + C)];
               for (int i = 0; i < nwin - 1; ++i) tm.win[i] = rmapW[(jp - nwin + 1 + i) % (K + C)];
-#define SYLV_ST3D_R(RR, KK) k_st3d<kTY25, RR, KK, 2, false><<<c->G25, 32 * kTY25, c->smem25_2, c->st>>>(tm, q.st25, nwin, coef, rslot(j), q.part2)
+#define SYLV_ST3D_R(RR, KK) k_st3d<kTY25, RR, KK, 2, false><<<c->G25, 32 * kTY25 * kWpl25, c->smem25_2, c->st>>>(tm, q.st25, nwin, coef, rslot(j), q.part2)
               if (r == 8) {
                 switch (K) {
                   case 1: SYLV_ST3D_R(8, 1); break;

@@ -40,8 +40,17 @@ namespace sylv {
 constexpr int kTx = 32;          // tile width in x (points)
 // pipeline stages (planes in flight): enough bytes in flight per SM to cover HBM latency
 // (r = 4 tiles carry half the bytes of r = 8 ones)
+#ifndef SYLV_ST25_NS8
+#define SYLV_ST25_NS8 3        // stages for r = 8 (development A/B: -DSYLV_ST25_NS8=2)
+#endif
 template <int R>
-constexpr int stages25() { return R >= 8 ? 3 : 4; }
+constexpr int stages25() { return R >= 8 ? SYLV_ST25_NS8 : 4; }
+// warps per tile line: 2 splits a line's 32 points between two warps (each half the elements,
+// twice the warps per SM to hide the shared-memory / DMMA latency chains)
+#ifndef SYLV_ST25_WPL
+#define SYLV_ST25_WPL 2
+#endif
+constexpr int kWpl25 = SYLV_ST25_WPL;
 
 struct Tma25 {
   CUtensorMap zd;                // halo box map of Z_d's ring slot
@@ -139,7 +148,7 @@ __device__ __forceinline__ void issue_plane(const Tma25& tm, int nwin, double* s
 // ---------------------------------------------------------------------------------------
 #define DMMA25(...) do { if (!(p.dbg & 2)) dmma(__VA_ARGS__); } while (0)
 template <int TY, int R, int K, int PASS, bool GRAM>
-__global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
+__global__ void __launch_bounds__(32 * TY * kWpl25, (TY <= 4 ? 2 : 1))
     k_st3d(const __grid_constant__ Tma25 tm, St25 p, int nwin, const double* __restrict__ coef,
            double* __restrict__ Wout, double* __restrict__ partial, int slot0 = -1) {
   static_assert(R == 4 || R == 8, "R = 4 or 8");
@@ -149,9 +158,11 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
   double* stages = reinterpret_cast<double*>(smraw);
   constexpr int kStageD = Gm::HCOL * R + (K - 1) * Gm::WCOL * R;   // doubles per stage
   uint64_t* bars = reinterpret_cast<uint64_t*>(smraw + (size_t)kNS * kStageD * 8);
-  __shared__ double red[TY][64 * (PASS == 1 ? K : 1)];
+  constexpr int EL = 8 / kWpl25;                // elements per lane (of the line's 8)
+  __shared__ double red[TY * kWpl25][64 * (PASS == 1 ? K : 1)];
 
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warp = wid / kWpl25, half = wid % kWpl25;   // warp = tile line; half = element range
   const int N = p.N;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kNS; ++s) mbar_init(&bars[s], 1);
@@ -159,17 +170,19 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
   }
   __syncthreads();
 
-  // element coordinates inside the tile (point offset px in [0,32), column col)
-  int px[8], col[8];
-  bool cok[8];                                  // column < R (else the element is zero)
+  // element coordinates inside the tile (point offset px in [0,32), column col); this warp owns
+  // elements half*EL .. half*EL + EL - 1 of its line
+  int px[EL], col[EL];
+  bool cok[EL];                                 // column < R (else the element is zero)
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
+  for (int e = 0; e < EL; ++e) {
+    const int eg = half * EL + e;
     if (PASS == 1) {
-      px[e] = 4 * e + (lane & 3);
+      px[e] = 4 * eg + (lane & 3);
       col[e] = lane >> 2;
     } else {
-      px[e] = 8 * (e >> 1) + (lane >> 2);
-      col[e] = (lane & 3) + 4 * (e & 1);
+      px[e] = 8 * (eg >> 1) + (lane >> 2);
+      col[e] = (lane & 3) + 4 * (eg & 1);
     }
     cok[e] = col[e] < R;
     if (!cok[e]) col[e] = 0;                    // keeps the (unused) addresses in range
@@ -214,11 +227,11 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
     const int yrow = warp + sy;                // line inside the halo box
     const bool yok = (y0 + warp) < NN;
     const bool has_ym = (y0 + warp) > 0;       // y-1 neighbour exists
-    double zm[8], zc[8], zp[8];
-    auto read_centers = [&](int q, double (&dst)[8]) {
+    double zm[EL], zc[EL], zp[EL];
+    auto read_centers = [&](int q, double (&dst)[EL]) {
       if (q < 0) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) dst[e] = 0.0;
+        for (int e = 0; e < EL; ++e) dst[e] = 0.0;
         return;
       }
       const int s = stage_of(q);
@@ -226,7 +239,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       phase ^= 1u << s;
       const double* H = stages + (size_t)s * kStageD;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) dst[e] = cok[e] ? H[(col[e] * Gm::HY + yrow) * Gm::HX + px[e] + sx] : 0.0;
+      for (int e = 0; e < EL; ++e) dst[e] = cok[e] ? H[(col[e] * Gm::HY + yrow) * Gm::HX + px[e] + sx] : 0.0;
     };
     read_centers(z0 - 1, zm);
     read_centers(z0, zc);
@@ -241,9 +254,9 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       read_centers(z + 1, zp);                  // waits for plane z+1 (plane z is ready since z-1)
       const double* H = stages + (size_t)stage_of(z) * kStageD;
       const double* Wb = H + Gm::HCOL * R;
-      double y[8];
+      double y[EL];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < EL; ++e) {
         if (!cok[e]) {
           y[e] = 0.0;
           continue;
@@ -263,7 +276,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       if (PASS == 1) {
         // P_i += Z_i^T Y over the 4-point slices e (pattern A: lane (col L>>2, point L&3))
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+        for (int e = 0; e < EL; ++e) {
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             if (i < nwin - 1) {
@@ -277,19 +290,20 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       } else {
         const int64_t rowbase = ((int64_t)(z - 1) * NN + (y0 + warp)) * NN + x0;   // local row
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int ql = 0; ql < EL / 2; ++ql) {
+          const int q = half * (EL / 2) + ql;     // 8-point slice of the line (pair of elements 2ql, 2ql+1)
           double D[2] = {0.0, 0.0};
-          DMMA25(D, aR[0], y[2 * q]);
-          if (R == 8) DMMA25(D, aR[1], y[2 * q + 1]);
+          DMMA25(D, aR[0], y[2 * ql]);
+          if (R == 8) DMMA25(D, aR[1], y[2 * ql + 1]);
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             if (i < nwin - 1) {
               const double* wi = Wb + i * Gm::WCOL * R;
-              DMMA25(D, aK[i][0], cok[2 * q] ? wi[(col[2 * q] * TY + warp) * Gm::WX + px[2 * q]] : 0.0);
-              if (R == 8) DMMA25(D, aK[i][1], wi[(col[2 * q + 1] * TY + warp) * Gm::WX + px[2 * q + 1]]);
+              DMMA25(D, aK[i][0], cok[2 * ql] ? wi[(col[2 * ql] * TY + warp) * Gm::WX + px[2 * ql]] : 0.0);
+              if (R == 8) DMMA25(D, aK[i][1], wi[(col[2 * ql + 1] * TY + warp) * Gm::WX + px[2 * ql + 1]]);
             } else if (i == nwin - 1) {
-              DMMA25(D, aK[i][0], zc[2 * q]);
-              if (R == 8) DMMA25(D, aK[i][1], zc[2 * q + 1]);
+              DMMA25(D, aK[i][0], zc[2 * ql]);
+              if (R == 8) DMMA25(D, aK[i][1], zc[2 * ql + 1]);
             }
           }
           // D: lane holds W'[point 8q + 2(L&3) + e][column L>>2]
@@ -317,7 +331,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
         }
       }
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < EL; ++e) {
         zm[e] = zc[e];
         zc[e] = zp[e];
       }
@@ -338,8 +352,8 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
     constexpr int NA = (PASS == 1 ? K : 1);
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
-      red[warp][i * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = acc[i][0] + acc2[i][0];
-      red[warp][i * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc[i][1] + acc2[i][1];
+      red[wid][i * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = acc[i][0] + acc2[i][0];
+      red[wid][i * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc[i][1] + acc2[i][1];
     }
     __syncthreads();
     // slot0 >= 0 (pass 1 with nwin = 1 after the fused pass, stencil25d_fused.cuh): only
@@ -350,7 +364,7 @@ __global__ void __launch_bounds__(32 * TY, (TY <= 4 ? 2 : 1))
       const int i = e / (R * R), a = (e / R) % R, c = e % R;      // R x R blocks of the 8 x 8 D
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < TY; ++w) s += red[w][i * 64 + a * 8 + c];
+      for (int w = 0; w < TY * kWpl25; ++w) s += red[w][i * 64 + a * 8 + c];
       partial[(int64_t)blockIdx.x * NA * R * R + (slot0 >= 0 ? slot0 * R * R + e : e)] = s;
     }
   }
