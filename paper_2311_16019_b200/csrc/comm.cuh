@@ -44,6 +44,9 @@ struct Comm {
   virtual ~Comm() {}
   // in-place sum over ranks; identical result on every rank
   virtual void allreduce(double* buf, size_t n, cudaStream_t st, int chan) = 0;
+  // recv[e] = sum over ranks of send[rank * n + e], e < n (send: nranks * n values): the rows of
+  // the summed sketch that this rank's shard of the sketch space owns
+  virtual void reduce_scatter(const double* send, double* recv, size_t n, cudaStream_t st, int chan) = 0;
   // fill the ghost rows of an SoA block (data = local row 0 of column 0): the gz rows
   // before each column from the lower neighbour's last gz rows, the gz rows after it from
   // the upper neighbour's first gz rows.  Ranks without a neighbour leave the ghosts alone.
@@ -68,6 +71,7 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -93,6 +97,7 @@ inline NcclApi& nccl_api() {
     SYLV_NCCL_SYM(CommDestroy);
     SYLV_NCCL_SYM(AllReduce);
     SYLV_NCCL_SYM(AllGather);
+    SYLV_NCCL_SYM(ReduceScatter);
     SYLV_NCCL_SYM(Send);
     SYLV_NCCL_SYM(Recv);
     SYLV_NCCL_SYM(GroupStart);
@@ -141,6 +146,11 @@ struct NcclComm : Comm {
   void allreduce(double* buf, size_t n, cudaStream_t st, int chan) override {
     if (n == 0) return;   // (also at world size 1: keeps the transport exercised)
     nccl_check(nccl_api().AllReduce(buf, buf, n, ncclFloat64, ncclSum, ch[chan], st), "ncclAllReduce");
+  }
+  void reduce_scatter(const double* send, double* recv, size_t n, cudaStream_t st, int chan) override {
+    if (n == 0) return;
+    if (!nccl_api().ReduceScatter) throw CommError{"ncclReduceScatter not found"};
+    nccl_check(nccl_api().ReduceScatter(send, recv, n, ncclFloat64, ncclSum, ch[chan], st), "ncclReduceScatter");
   }
   void halo(double* data, int R, int64_t ld, int64_t gz, cudaStream_t st, int chan) override {
     if (nranks == 1 || gz == 0) return;
@@ -295,6 +305,26 @@ struct LocalComm : Comm {
       if (r != rank) ck(cudaStreamWaitEvent(st, g->ev2[r], 0), "cudaStreamWaitEvent");
     ck(cudaMemcpyAsync(buf, sc, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
     g->barrier();                                        // nobody re-records ev/ev2 early
+  }
+  void reduce_scatter(const double* send, double* recv, size_t n, cudaStream_t st, int) override {
+    if (n == 0) return;
+    ++seq;
+    tr("reduce_scatter", n);
+    g->ptr[rank] = const_cast<double*>(send);
+    ck(cudaEventRecord(g->ev[rank], st), "cudaEventRecord");
+    g->barrier();
+    PtrPack pk{};
+    for (int r = 0; r < nranks; ++r) {
+      pk.p[r] = g->ptr[r] + (size_t)rank * n;      // this rank's slice of every rank's send buffer
+      if (r != rank) ck(cudaStreamWaitEvent(st, g->ev[r], 0), "cudaStreamWaitEvent");
+    }
+    k_sum_ranks<<<(int)std::min<size_t>(1024, (n + 255) / 256), 256, 0, st>>>(pk, nranks, n, recv);
+    ck(cudaGetLastError(), "k_sum_ranks");
+    ck(cudaEventRecord(g->ev2[rank], st), "cudaEventRecord");
+    g->barrier();                                        // every rank has read the send buffers
+    for (int r = 0; r < nranks; ++r)
+      if (r != rank) ck(cudaStreamWaitEvent(st, g->ev2[r], 0), "cudaStreamWaitEvent");
+    g->barrier();
   }
   void halo(double* data, int R, int64_t ld, int64_t gz, cudaStream_t st, int) override {
     if (nranks == 1 || gz == 0) return;

@@ -150,6 +150,9 @@ struct Sequence {
   int which = 0;
   int R = 1, K = 1, dmax = 0;
   int64_t n = 0, s = 0, ldT = 0, ld = 0;   // n: local rows; ld: SoA column stride
+  int64_t sq = 0;                         // rows of the sketch-space QR on this rank: s, or s / P
+                                          // when the sketch space is sharded
+  double* skfull = nullptr;               // sharded sketch space: the s x R partial sketch
   int64_t gz = 0;                         // ghost rows before/after a column (N^2 3-D, N 2-D, 0 CSR)
   OpParams op{};
   SketchParams sp{};
@@ -228,6 +231,7 @@ struct sylv_ctx {
   int R = 1, K = 1, dmax = 0, zeta = 8, chunk = 0, cflags = 0;
   int method = SYLV_METHOD_SKETCHED;   // sylv_config.method
   int RTn = 1, tpcN = 1, CCn = 1;      // full method: n-space Q^T w row chunks / tiles per CTA, Q c chunks
+  int64_t sq = 0;                      // sketch-space rows per rank (s, or s / P: sharded sketch space)
   int64_t n = 0, s = 0;
   double tol = 1e-6, rank_tol = 1e-12;
   int sm = 148;
@@ -421,7 +425,7 @@ void free_seq(Sequence& q) {
   for (cudaEvent_t e : q.ev_sk) cudaEventDestroy(e);
   double* dp[] = {q.ring, q.Cdev, q.Yt, q.Zaos, q.sk, q.skpart, q.w, q.w2, q.Q, q.Tdev, q.Rall, q.Kc, q.Hc, q.hn2,
                   q.part1, q.part2, q.part_s, q.cpart, q.csum, q.c2, q.qcpart, q.small, q.cv, q.skz, q.sr_sign,
-                  q.sr_v};
+                  q.sr_v, q.skfull};
   if (q.sr_plan) cufftDestroy(q.sr_plan);
   dfree(q.sr_rows);
   dfree(q.sr_V);
@@ -441,21 +445,39 @@ void free_seq(Sequence& q) {
 
 // CholQR2 of the s x R block `in` (destroyed): q written to Q[:, col0:col0+R]
 // (column-major), R-factor tau (positive diagonal) to `tau_out` (device, R x R).
+// out[e] = sum of the nparts per-CTA partials (block_sum_parts order), one CTA
+__global__ void __launch_bounds__(kSmallThreads) k_sum_partials(const double* __restrict__ partial, int nparts, int len, double* __restrict__ out) {
+  block_sum_parts(partial, nparts, len, len, out);
+}
+
 // General form: `rows` x R row-major `in` (destroyed; q.w2 holds rows x R scratch) -> `out`
 // column-major with column stride out_ld.
+// gram_chan >= 0: the rows are this rank's shard of a sketch-space block (sharded sketch space),
+// the Gram is summed over the ranks (partials -> one vector -> allreduce on that channel).
 void cholqr2_into(sylv_ctx* c, Sequence& q, double* in, int64_t rows, double* out, int64_t out_ld,
-                  double* tau_out, int flag_slot, cudaStream_t st) {
+                  double* tau_out, int flag_slot, cudaStream_t st, int gram_chan = -1) {
   const int R = c->R;
-  const int gs = (int)std::min<int64_t>(c->G, (rows + 255) / 256);
+  const int gs = (int)std::max<int64_t>(1, std::min<int64_t>(c->G, (rows + 255) / 256));
   double* ta = q.small;            // R^2
   double* tai = q.small + 64;      // R^2
   double* tbi = q.small + 128;     // R^2
+  double* gsum = q.small + 448;    // R^2: the rank-summed Gram (sharded)
+  auto gram = [&](const double* x) -> std::pair<const double*, int> {
+    SYLV_DISPATCH_R(R, { k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(rows, x, q.part_s); });
+    if (gram_chan < 0 || !c->comm) return {q.part_s, gs};
+    k_sum_partials<<<1, kSmallThreads, 0, st>>>(q.part_s, gs, R * R, gsum);
+    c->comm->allreduce(gsum, (size_t)R * R, st, gram_chan);
+    count(c);
+    return {gsum, 1};
+  };
+  auto g1 = gram(in);
   SYLV_DISPATCH_R(R, {
-    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(rows, in, q.part_s);
-    k_chol_small<R_><<<1, kSmallThreads, 0, st>>>(q.part_s, gs, ta, tai, nullptr, q.flags, flag_slot);
+    k_chol_small<R_><<<1, kSmallThreads, 0, st>>>(g1.first, g1.second, ta, tai, nullptr, q.flags, flag_slot);
     k_rmul<R_><<<gs, kThreads, 0, st>>>(rows, in, tai, q.w2, 0);
-    k_gram_rowmajor<R_><<<gs, kThreads, 0, st>>>(rows, q.w2, q.part_s);
-    k_chol_small<R_><<<1, kSmallThreads, 0, st>>>(q.part_s, gs, tau_out, tbi, ta, q.flags, flag_slot);
+  });
+  auto g2 = gram(q.w2);
+  SYLV_DISPATCH_R(R, {
+    k_chol_small<R_><<<1, kSmallThreads, 0, st>>>(g2.first, g2.second, tau_out, tbi, ta, q.flags, flag_slot);
     k_rmul<R_><<<gs, kThreads, 0, st>>>(rows, q.w2, tbi, out, out_ld);
   });
   count(c, 6);
@@ -464,7 +486,9 @@ void cholqr2_into(sylv_ctx* c, Sequence& q, double* in, int64_t rows, double* ou
 
 void cholqr2(sylv_ctx* c, Sequence& q, double* in, int64_t col0, double* tau_out, int flag_slot,
              cudaStream_t st) {
-  cholqr2_into(c, q, in, q.s, q.Q + col0 * q.s, q.s, tau_out, flag_slot, st);
+  const bool shard = q.sq != q.s;
+  const int chan = q.which == 0 ? kChanUSide : kChanVSide;
+  cholqr2_into(c, q, in, q.sq, q.Q + col0 * q.sq, q.sq, tau_out, flag_slot, st, shard ? chan : -1);
 }
 
 // ---- 2.5-D TMA passes ------------------------------------------------------------------
@@ -636,10 +660,6 @@ Tma25F tma_args_fused(const Sequence& q, int j, int nwin) {
 // Partials written by the pass kernels of sequence q (the coefficient kernels' nparts)
 int pass_parts(const sylv_ctx* c, const Sequence& q) { return q.tma ? c->G25 : c->G; }
 
-// out[e] = sum of the nparts per-CTA partials (block_sum_parts order), one CTA
-__global__ void __launch_bounds__(kSmallThreads) k_sum_partials(const double* __restrict__ partial, int nparts, int len, double* __restrict__ out) {
-  block_sum_parts(partial, nparts, len, len, out);
-}
 
 // Multi-rank: reduce this rank's per-CTA partials to one vector of `len` values, sum it
 // over the ranks (bit-identical on every rank), and return it as a single "partial" for
@@ -894,6 +914,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.dmax = c->dmax;
   q.n = c->n;
   q.s = c->s;
+  q.sq = c->sq;
   q.op = make_op(A, transpose);
   q.op.n = c->n;   // this rank's rows
   q.gz = (A->kind == SYLV_OP_STENCIL3D) ? (int64_t)A->grid[0] * A->grid[0]
@@ -922,7 +943,8 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   if (A->kind == SYLV_OP_CSR && R % 2 == 0) q.Zaos = dalloc<double>((size_t)(c->n + 2 * q.gz) * R);
   if (sketched) {
     q.sk = dalloc<double>(sR);
-    q.Q = dalloc<double>((size_t)c->s * ldT);
+    q.Q = dalloc<double>((size_t)q.sq * ldT);            // this rank's rows of Q (sharded: s / P)
+    if (q.sq != q.s) q.skfull = dalloc<double>(sR);
     if (sr_sign) {
       // SRDCT (f4): signs -> doubles, rows (checked), cuFFT D2Z plan batched over the R columns
       q.srdct = true;
@@ -953,7 +975,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     }
   }
   // w, w2: the s x R sketched block (sketched) / the n x R applied block (full method)
-  const int64_t wrows = full ? c->n : (sketched ? c->s : 0);
+  const int64_t wrows = full ? c->n : (sketched ? c->s : 0);   // (sharded sketch space: only sq rows used)
   if (wrows) {
     q.w = dalloc<double>((size_t)wrows * R);
     q.w2 = dalloc<double>((size_t)wrows * R);
@@ -978,7 +1000,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     q.cpart = dalloc<double>((size_t)(full ? c->RTn : c->RT) * ldT * R);
     q.csum = dalloc<double>(ldT * R);
     q.c2 = dalloc<double>(ldT * R);
-    q.qcpart = dalloc<double>(full ? (size_t)c->CCn * c->n * R : (size_t)c->CC * sR);
+    q.qcpart = dalloc<double>(full ? (size_t)c->CCn * c->n * R : (size_t)c->CC * q.sq * R);
   }
   q.small = dalloc<double>(512);
   CK(cudaMemsetAsync(q.ring, 0, (size_t)(K + 1) * blk * sizeof(double), c->st));
@@ -1045,8 +1067,13 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     if (q.flags_h[0]) throw Status{SYLV_E_INVALID, "C1 or C2 is rank deficient"};
     return;
   }
-  launch_sketch(c, q, q.cdata(), R, nullptr, q.sk, c->st);
-  if (c->comm) c->comm->allreduce(q.sk, (size_t)q.s * R, c->st, kChanSetup);
+  if (q.sq != q.s) {          // sharded sketch space: this rank keeps rows [rank sq, rank sq + sq) of S C
+    launch_sketch(c, q, q.cdata(), R, nullptr, q.skfull, c->st);
+    c->comm->reduce_scatter(q.skfull, q.sk, (size_t)q.sq * R, c->st, kChanSetup);
+  } else {
+    launch_sketch(c, q, q.cdata(), R, nullptr, q.sk, c->st);
+    if (c->comm) c->comm->allreduce(q.sk, (size_t)q.s * R, c->st, kChanSetup);
+  }
   CK(cudaGetLastError());
   tr.mark("sketch of C", c->st);
   // sketched GS (f3): S Z_1 = S C kept (the s-space ring), ell = R(S C) = beta, so U_1 = C beta^{-1}
@@ -1152,8 +1179,13 @@ void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t 
   // ---- a4: w = (S W') R_{j+1}   (a5 timing includes the sketch)
   if (timing) { t3 = ev_get(c, 2); CK(cudaEventRecord(t3.a, st)); }
   if (timing) { t4 = ev_get(c, 3); CK(cudaEventRecord(t4.a, st)); }
-  launch_sketch(c, q, q.slot(j + 1), R, q.Rall + (int64_t)(j + 1) * R * R, q.w, st);
-  if (c->comm) c->comm->allreduce(q.w, (size_t)q.s * R, st, chan);   // S linear in rows
+  if (q.sq != q.s) {   // sharded sketch space: reduce-scatter of the partial sketches (S linear in rows)
+    launch_sketch(c, q, q.slot(j + 1), R, q.Rall + (int64_t)(j + 1) * R * R, q.skfull, st);
+    c->comm->reduce_scatter(q.skfull, q.w, (size_t)q.sq * R, st, chan);
+  } else {
+    launch_sketch(c, q, q.slot(j + 1), R, q.Rall + (int64_t)(j + 1) * R * R, q.w, st);
+    if (c->comm) c->comm->allreduce(q.w, (size_t)q.s * R, st, chan);   // S linear in rows
+  }
   if (timing) { CK(cudaEventRecord(t4.b, st)); c->timed.push_back(t4); }
   if (side != st) {                                           // pull: QR on the side stream
     CK(cudaEventRecord(q.ev_c2[j % ne], st));
@@ -1172,25 +1204,35 @@ void step_sketch(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, cudaStream_t 
 void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
   const int R = c->R;
   const int m = j * R;
+  const int64_t rows = q.sq;                 // this rank's rows of w and Q (sharded: s / P)
+  const bool shard = rows != q.s;
+  const int chan = q.which == 0 ? kChanUSide : kChanVSide;
   const dim3 gq((m + kQtwCols - 1) / kQtwCols, c->RT);
   const int cols_per_chunk = (m + c->CC - 1) / c->CC;
   const int ncc = (m + cols_per_chunk - 1) / cols_per_chunk;
-  const dim3 gc((unsigned)((q.s + kThreads - 1) / kThreads), ncc);
+  const dim3 gc((unsigned)((rows + kThreads - 1) / kThreads), ncc);
   const int64_t mR = (int64_t)m * R;
   const int gr = (int)std::min<int64_t>(1024, (mR + 255) / 256);
-  const int gw = (int)std::min<int64_t>(1024, (q.s * R + 255) / 256);
+  const int gw = (int)std::min<int64_t>(1024, (rows * R + 255) / 256);
   SYLV_DISPATCH_R(R, {
-    // pass A: c1 = Q^T w
-    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, q.s, q.s, m, q.w, c->tileQ, 1, q.cpart);
+    // pass A: c1 = Q^T w (sharded: local rows, then the m R coefficients summed over the ranks)
+    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, c->tileQ, 1, q.cpart);
     k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.csum, nullptr);
+    if (shard) c->comm->allreduce(q.csum, (size_t)mR, st, chan);
     // w -= Q c1
-    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, q.s, q.s, m, q.csum, cols_per_chunk, q.qcpart);
-    k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, q.s * R);
+    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, rows, rows, m, q.csum, cols_per_chunk, q.qcpart);
+    k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, rows * R);
     // pass B: c2 = Q^T w, csum += c2
-    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, q.s, q.s, m, q.w, c->tileQ, 1, q.cpart);
-    k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.c2, q.csum);
-    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, q.s, q.s, m, q.c2, cols_per_chunk, q.qcpart);
-    k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, q.s * R);
+    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, c->tileQ, 1, q.cpart);
+    if (shard) {
+      k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.c2, nullptr);
+      c->comm->allreduce(q.c2, (size_t)mR, st, chan);
+      k_axpy_inplace<<<gr, 256, 0, st>>>(q.c2, q.csum, mR);
+    } else {
+      k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.c2, q.csum);
+    }
+    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, rows, rows, m, q.c2, cols_per_chunk, q.qcpart);
+    k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, rows * R);
   });
   count(c, 8);
   CK(cudaGetLastError());
@@ -1664,11 +1706,16 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     const int64_t rows_per_cta = (int64_t)kWarps * (32 / r);
     c->G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sm * 4, (c->n + rows_per_cta - 1) / rows_per_cta));
     // Q^T w: (ceil(m / kQtwCols) x RT) CTAs, row tiles of qtw_tile<R>() rows
+    // sketch space sharded by rows over the ranks: Alg. 1 with the hashed sparse
+    // sign, several ranks, s a multiple of the rank count; else replicated on every rank
+    c->sq = (comm && comm->nranks > 1 && method == SYLV_METHOD_SKETCHED && !srdct && c->s % comm->nranks == 0 &&
+             !std::getenv("SYLV_SKETCH_REPLICATED"))
+                ? c->s / comm->nranks : c->s;
     SYLV_DISPATCH_R(r, { c->tileQ = qtw_tile<R_>(); });
-    c->RT = (int)((c->s + c->tileQ - 1) / c->tileQ);
+    c->RT = (int)((c->sq + c->tileQ - 1) / c->tileQ);
     // Q c: (ceil(s/256) x CC) CTAs, ~4 per SM at the full width (each thread streams a row
     // of its column chunk with 8 loads in flight)
-    c->CC = (int)std::max<int64_t>(1, std::min<int64_t>(16, (4 * c->sm + (c->s / 256)) / std::max<int64_t>(1, c->s / 256)));
+    c->CC = (int)std::max<int64_t>(1, std::min<int64_t>(16, (4 * c->sm + (c->sq / 256)) / std::max<int64_t>(1, c->sq / 256)));
     if (method == SYLV_METHOD_FULL) {
       // n-space Q^T w over the retained basis: ~2 CTAs per SM of row chunks, each `tpcN` tiles
       const int64_t tiles = (c->n + c->tileQ - 1) / c->tileQ;

@@ -334,6 +334,12 @@ __global__ void k_red_parts(const double* __restrict__ partial, int nparts, int6
   }
 }
 
+// acc[e] += x[e]  (sharded sketch space: csum += the rank-summed c2)
+__global__ void k_axpy_inplace(const double* __restrict__ x, double* __restrict__ acc, int64_t len) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x)
+    acc[e] += x[e];
+}
+
 // partial2[(cc*s + row)*R + c] = sum_{j in chunk cc} Q[j*s + row] cvec[j*R + c]
 template <int R>
 __global__ void __launch_bounds__(kThreads) k_qc_part(const double* __restrict__ Q, int64_t s, int64_t ldq, int m,

@@ -10,7 +10,12 @@ comm.cuh):
   * Gram-Schmidt inner products and the Gram of W' are allreduced (sum), the r x r
     normalisation (CholQR) is then identical on every rank;
   * the partial sketch S[:, rows_loc] W_loc uses GLOBAL row indices and is allreduced
-    (S is linear in rows), the sketch-space QR is replicated.
+    (S is linear in rows), the sketch-space QR is replicated (mode "replicated"), or
+    reduce-scattered so each rank keeps s/P rows of Q and w, with the CGS2 coefficient vectors
+    and the CholQR Gram allreduced (mode "sharded_sketch": the engine's default for several
+    ranks when P divides s);
+  * mode "sketched_gs" (f3): the Gram-Schmidt coefficients and the normalisation come
+    from the allreduced sketch of the matvec (no inner product over the n rows at all).
 The assembled H_und_d, T_d and beta must equal the single-process oracle's (which never
 splits rows) to rounding (1e-10), on every rank.  This pins the decomposition itself
 (which data crosses ranks, and global hashing) without a GPU.
@@ -82,12 +87,24 @@ def _halo(Z, plane, rank, world):
     return lo, hi
 
 
+def _cholqr2_sharded(w):
+    """CholQR2 of a row-sharded s x r block: Grams allreduced, each rank keeps its rows."""
+    G = _allreduce(w.T @ w)
+    t1 = np.linalg.cholesky(G).T
+    w1 = np.linalg.solve(t1.T, w.T).T
+    G2 = _allreduce(w1.T @ w1)
+    t2 = np.linalg.cholesky(G2).T
+    return np.linalg.solve(t2.T, w1.T).T, t2 @ t1
+
+
 class ShardedSequence:
     """One Krylov sequence of Alg. 1 on this rank's slab (lines 1 and 3-9)."""
 
-    def __init__(self, M, C, rows, plane, seed, cfg, rank, world):
+    def __init__(self, M, C, rows, plane, seed, cfg, rank, world, mode="replicated"):
         b, e = rows
+        self.mode = mode
         self.rows, self.plane, self.rank, self.world, self.k, self.r = rows, plane, rank, world, cfg.k, cfg.r
+        self.sl = slice(rank * cfg.s // world, (rank + 1) * cfg.s // world)   # this rank's sketch rows
         n = M.shape[0]
         ext = np.arange(max(0, b - plane), min(n, e + plane))
         self.M_loc = M[b:e][:, ext].toarray()                 # slab rows, columns incl. ghost planes
@@ -98,11 +115,18 @@ class ShardedSequence:
             row, val = sparse_sign.entries(j, t, cfg.s, cfg.zeta, seed)
             self.S_loc[row, np.arange(e - b)] = val
         Cl = C[b:e]
-        G = _allreduce(Cl.T @ Cl)
-        ell = np.linalg.cholesky(G).T                         # U_1 ell = C (CholQR)
+        SC = _allreduce(self.S_loc @ Cl)
+        _, self.beta = alg1.qr_pos(SC)
+        if mode == "sketched_gs":                             # U_1 = C R(S C)^{-1}: S-orthonormal
+            ell = self.beta
+        else:
+            G = _allreduce(Cl.T @ Cl)
+            ell = np.linalg.cholesky(G).T                     # U_1 ell = C (CholQR)
         self.U = {1: np.linalg.solve(ell.T, Cl.T).T}
-        _, self.beta = alg1.qr_pos(_allreduce(self.S_loc @ Cl))
-        self.Q, self.T = alg1.qr_pos(_allreduce(self.S_loc @ self.U[1]))
+        if mode == "sharded_sketch":                          # this rank's rows of Q_1
+            self.Q, self.T = _cholqr2_sharded(_allreduce(self.S_loc @ self.U[1])[self.sl])
+        else:
+            self.Q, self.T = alg1.qr_pos(_allreduce(self.S_loc @ self.U[1]))
         self.H = {}
         self.d = 0
 
@@ -114,20 +138,42 @@ class ShardedSequence:
     def step(self):
         d = self.d + 1
         W = self.apply(self.U[d])
-        for i in range(max(1, d - self.k + 1), d + 1):
-            h = _allreduce(self.U[i].T @ W)
-            W = W - self.U[i] @ h
-            self.H[(i, d)] = h
-        G = _allreduce(W.T @ W)
-        hs = np.linalg.cholesky(G).T
+        window = range(max(1, d - self.k + 1), d + 1)
+        if self.mode == "sketched_gs":
+            # coefficients from sketches only (one allreduce of the sketch of the matvec)
+            SW = _allreduce(self.S_loc @ W)
+            SU = {i: _allreduce(self.S_loc @ self.U[i]) for i in window}
+            for i in window:
+                h = SU[i].T @ SW
+                W = W - self.U[i] @ h
+                SW = SW - SU[i] @ h
+                self.H[(i, d)] = h
+            _, hs = alg1.qr_pos(SW)
+        else:
+            for i in window:
+                h = _allreduce(self.U[i].T @ W)
+                W = W - self.U[i] @ h
+                self.H[(i, d)] = h
+            G = _allreduce(W.T @ W)
+            hs = np.linalg.cholesky(G).T
         self.H[(d + 1, d)] = hs
         Unew = np.linalg.solve(hs.T, W.T).T
         w = _allreduce(self.S_loc @ Unew)
-        c1 = self.Q.T @ w
-        w = w - self.Q @ c1
-        c2 = self.Q.T @ w
-        w = w - self.Q @ c2
-        q, tau = alg1.qr_pos(w)
+        if self.mode == "sharded_sketch":
+            # reduce-scatter: this rank's rows of the summed sketch; CGS2 over the local rows of Q
+            # with the m r coefficients allreduced, CholQR2 with the Gram allreduced
+            w = w[self.sl]
+            c1 = _allreduce(self.Q.T @ w)
+            w = w - self.Q @ c1
+            c2 = _allreduce(self.Q.T @ w)
+            w = w - self.Q @ c2
+            q, tau = _cholqr2_sharded(w)
+        else:
+            c1 = self.Q.T @ w
+            w = w - self.Q @ c1
+            c2 = self.Q.T @ w
+            w = w - self.Q @ c2
+            q, tau = alg1.qr_pos(w)
         m, r = self.T.shape[0], self.r
         T = np.zeros((m + r, m + r))
         T[:m, :m], T[:m, m:], T[m:, m:] = self.T, c1 + c2, tau
@@ -144,7 +190,7 @@ class ShardedSequence:
         return Hb
 
 
-def _worker(rank, world, port, q, kind):
+def _worker(rank, world, port, q, kind, mode):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -153,8 +199,8 @@ def _worker(rank, world, port, q, kind):
         rows = pkg.partition(cfg, world, rank)               # the library's host partition
         A, Bt, _ = operators.operator_pair(cfg)
         C1, C2 = inputs.make_rhs(cfg)
-        U = ShardedSequence(A, C1, rows, _halo_width(cfg, A), cfg.seed_u, cfg, rank, world)
-        V = ShardedSequence(Bt, C2, rows, _halo_width(cfg, Bt), cfg.seed_v, cfg, rank, world)
+        U = ShardedSequence(A, C1, rows, _halo_width(cfg, A), cfg.seed_u, cfg, rank, world, mode)
+        V = ShardedSequence(Bt, C2, rows, _halo_width(cfg, Bt), cfg.seed_v, cfg, rank, world, mode)
         for _ in range(NSTEPS):
             U.step()
             V.step()
@@ -163,12 +209,15 @@ def _worker(rank, world, port, q, kind):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,world", [("stencil3d", 2), ("stencil3d", 3), ("csr", 2), ("csr", 3)])
-def test_sharded_decomposition_matches_oracle(kind, world):
+@pytest.mark.parametrize("kind,world,mode", [("stencil3d", 2, "replicated"), ("stencil3d", 3, "replicated"),
+                                             ("csr", 2, "replicated"), ("csr", 3, "replicated"),
+                                             ("stencil3d", 2, "sharded_sketch"), ("csr", 4, "sharded_sketch"),
+                                             ("stencil3d", 2, "sketched_gs"), ("csr", 3, "sketched_gs")])
+def test_sharded_decomposition_matches_oracle(kind, world, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, kind)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, kind, mode)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -176,7 +225,7 @@ def test_sharded_decomposition_matches_oracle(kind, world):
         p.join(timeout=60)
         assert p.exitcode == 0
     cfg = inputs.small_config(**CFGS[kind])
-    orc = alg1.SylvesterSketchedKrylov.from_config(cfg)
+    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, sketched_gs=mode == "sketched_gs")
     orc.step(NSTEPS)
     res.sort()
     assert res[0][1][0] == 0 and res[-1][1][1] == cfg.n
