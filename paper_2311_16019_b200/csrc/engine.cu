@@ -153,6 +153,11 @@ struct Sequence {
   int64_t sq = 0;                         // rows of the sketch-space QR on this rank: s, or s / P
                                           // when the sketch space is sharded
   double* skfull = nullptr;               // sharded sketch space: the s x R partial sketch
+  // CSR pass 1 with the band window of Z_d in shared memory (k_pass1_csr_win): tile rows T
+  // (0 = not eligible: the window of T + 2 band rows does not fit), band, grid, smem bytes
+  int64_t csrT = 0, band = 0;
+  int csr_grid = 0;
+  size_t csr_smem = 0;
   int64_t gz = 0;                         // ghost rows before/after a column (N^2 3-D, N 2-D, 0 CSR)
   OpParams op{};
   SketchParams sp{};
@@ -659,6 +664,8 @@ Tma25F tma_args_fused(const Sequence& q, int j, int nwin) {
 
 // Partials written by the pass kernels of sequence q (the coefficient kernels' nparts)
 int pass_parts(const sylv_ctx* c, const Sequence& q) { return q.tma ? c->G25 : c->G; }
+// partials written by pass 1 (the windowed CSR pass 1 runs its own grid)
+int pass1_parts(const sylv_ctx* c, const Sequence& q) { return q.csrT > 0 ? q.csr_grid : pass_parts(c, q); }
 
 
 // Multi-rank: reduce this rank's per-CTA partials to one vector of `len` values, sum it
@@ -704,6 +711,13 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cud
       }
     }
 #undef SYLV_ST3D_P1
+  } else if (q.op.kind == kCSR && q.csrT > 0) {
+    // band window of Z_d staged in shared memory (no AoS copy, gathers from shared memory)
+    SYLV_DISPATCH_R124_K(R, K, {
+      k_pass1_csr_win<R_, K_><<<q.csr_grid, kCsrWinThreads, q.csr_smem, st>>>(q.op, win, nwin, q.ld, q.gz, q.band,
+                                                                              q.csrT, q.Yt, q.part1);
+    });
+    count(c);
   } else if (q.op.kind == kCSR && R <= 4) {
     if (R % 2 == 0) {   // AoS copy of Z_d for the gathers
       // rows -gz .. n+gz-1 (ghost rows of a sharded CSR operator included)
@@ -905,6 +919,41 @@ void shard_csr(sylv_ctx* c, Sequence& q) {
   q.gz = band;
 }
 
+// Windowed CSR pass 1 (nspace.cuh k_pass1_csr_win) when the band window of a row tile fits in
+// shared memory: tiles of T rows (multiple of 512), one CTA of 512 threads per SM.
+void setup_csr_window(sylv_ctx* c, Sequence& q) {
+  q.csrT = 0;
+  const char* e = std::getenv("SYLV_CSR_WINDOW");      // "0": the global-gather kernel (A/B)
+  if (e && std::strcmp(e, "0") == 0) return;
+  int64_t band = q.gz;                                  // sharded: the halo width is the band
+  if (!c->comm) {
+    int* band_d = dalloc<int>(1);
+    CK(cudaMemsetAsync(band_d, 0, sizeof(int), c->st));
+    k_csr_band<<<1024, 256, 0, c->st>>>(q.rp, q.ci, c->n, band_d);
+    count(c);
+    int b = 0;
+    CK(cudaMemcpyAsync(&b, band_d, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    dfree(band_d);
+    band = b;
+  }
+  q.band = band;
+  const int R = c->R, K = c->K;
+  int dev = 0, max_optin = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int64_t rows_fit = ((int64_t)max_optin - (int64_t)kCsrWinWarps * K * R * R * 8 - 256) / (8 * R);
+  int64_t T = (rows_fit - 2 * band - 2) / 512 * 512;
+  if (T < 1024) return;
+  T = std::min<int64_t>(T, (c->n + 511) / 512 * 512);
+  q.csrT = T;
+  q.csr_smem = (size_t)R * (T + 2 * band + 2) * 8 + 16;
+  q.csr_grid = (int)std::min<int64_t>(c->sm, (c->n + T - 1) / T);
+  SYLV_DISPATCH_R124_K(R, K, {
+    CK(cudaFuncSetAttribute(k_pass1_csr_win<R_, K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.csr_smem));
+  });
+}
+
 void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, bool transpose,
                    const double* C, uint64_t seed, const int8_t* sr_sign, const int64_t* sr_rows) {
   InitTrace tr;
@@ -924,6 +973,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     if (c->comm) shard_csr(c, q);                // this rank's rows; q.gz = band
   }
   q.ld = (c->n + 2 * q.gz + 63) / 64 * 64;
+  if (A->kind == SYLV_OP_CSR && c->method != SYLV_METHOD_FULL) setup_csr_window(c, q);
   q.ldT = (int64_t)(c->dmax + 1) * c->R;
   q.sp.seed = (uint32_t)(seed ^ (seed >> 32));
   q.sp.zeta = (uint32_t)c->zeta;
@@ -936,7 +986,8 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   const bool sgs = c->method == SYLV_METHOD_SKETCHED_GS;
   const bool sketched = c->method == SYLV_METHOD_SKETCHED || sgs;
   const bool full = c->method == SYLV_METHOD_FULL;
-  q.ring = dalloc<double>((size_t)(K + 1) * blk);     // full method: the retained basis (d_max + 1 slots)
+  // (+64: the windowed CSR pass 1 may read one element past the last column, see k_pass1_csr_win)
+  q.ring = dalloc<double>((size_t)(K + 1) * blk + 64);   // full method: the retained basis (d_max + 1 slots)
   q.Cdev = dalloc<double>(blk);
   if (A->kind == SYLV_OP_CSR || sgs) q.Yt = dalloc<double>(blk);
   if (sgs) q.skz = dalloc<double>((size_t)(K + 1) * sR);
@@ -1003,7 +1054,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     q.qcpart = dalloc<double>(full ? (size_t)c->CCn * c->n * R : (size_t)c->CC * q.sq * R);
   }
   q.small = dalloc<double>(512);
-  CK(cudaMemsetAsync(q.ring, 0, (size_t)(K + 1) * blk * sizeof(double), c->st));
+  CK(cudaMemsetAsync(q.ring, 0, ((size_t)(K + 1) * blk + 64) * sizeof(double), c->st));
   tr.mark("device allocations + memsets", c->st);
   if (!full) setup_tma(c, q);
   tr.mark("tensor maps", c->st);
@@ -1106,6 +1157,7 @@ void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, bool sketch_o
   for (int i = 0; i < nwin; ++i) win.p[i] = q.slot(j - nwin + 1 + i);
   const bool timing = (c->cflags & 1) != 0;
   const int G = pass_parts(c, q);
+  const int G1 = pass1_parts(c, q);
   TimedPair t1{}, t2{};
   // ---- a1 + a2 coefficients: pass 1
   if (timing) { t1 = ev_get(c, 0); CK(cudaEventRecord(t1.a, st)); }
@@ -1113,8 +1165,8 @@ void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, bool sketch_o
   if (timing) { CK(cudaEventRecord(t1.b, st)); c->timed.push_back(t1); }
   const int chan_main = q.which == 0 ? kChanUMain : kChanVMain;
   double* red = c->red ? c->red + (int64_t)q.which * (K + 1) * R * R : nullptr;
-  int np1 = G;
-  const double* p1 = reduce_partials(c, q.part1, G, K * R * R, red, st, chan_main, &np1);
+  int np1 = G1;
+  const double* p1 = reduce_partials(c, q.part1, G1, K * R * R, red, st, chan_main, &np1);
   SYLV_DISPATCH_RK(R, K, {
     k_coef1<R_, K_><<<1, kSmallThreads, 0, st>>>(p1, np1, nwin, j, q.Rall, q.Kc, q.Hc, q.hn2);
   });

@@ -746,3 +746,167 @@ __global__ void k_soa_mul_rowmajor(int64_t n, const double* __restrict__ Z, int6
 constexpr int kMaxChunk = 16;
 
 }  // namespace sylv
+
+namespace sylv {
+
+// =====================================================================================
+// CSR pass 1 with the band window of Z_d in shared memory (c4: band = max |col - row| = 4096)
+// =====================================================================================
+// A CTA owns tiles of T consecutive rows.  Every column index of rows [i0, i1) lies in
+// [i0 - band, i1 + band), so the window Z_d[w0, w1) (all R columns, SoA) arrives in shared
+// memory by bulk copies (cp.async.bulk, one mbarrier) and the 21 gathers per row read shared
+// memory instead of L1/L2 (which the global-gather kernel above is bound by).  The CSR
+// values / indices stream from HBM once.  4 lanes per row, CGS inner products with the window
+// blocks as in k_pass1_csr; the same per-row arithmetic order (parity with k_pass1_csr is exact
+// up to the order of the 4-lane shuffle sums, which is the same).
+constexpr int kCsrWinThreads = 1024;   // 32 warps: the CSR streams are latency-bound per warp
+constexpr int kCsrWinWarps = kCsrWinThreads / 32;
+constexpr int kCsrWinRows = kCsrWinThreads / kCsrLanes;   // rows per sweep of the CTA
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+template <int R, int K>
+__global__ void __launch_bounds__(kCsrWinThreads, 1)
+    k_pass1_csr_win(OpParams op, Win win, int nwin, int64_t ld, int64_t gz, int64_t band, int64_t T,
+                    double* __restrict__ Yt, double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char csr_smraw[];
+  const int64_t Wcap = T + 2 * band + 2;
+  double* zw = reinterpret_cast<double*>(csr_smraw);                       // R x Wcap
+  uint64_t* bar = reinterpret_cast<uint64_t*>(zw + (int64_t)R * Wcap);
+  __shared__ double red[kCsrWinWarps * K * R * R];
+  double acc[K * R * R];
+#pragma unroll
+  for (int e = 0; e < K * R * R; ++e) acc[e] = 0.0;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int sub = threadIdx.x & (kCsrLanes - 1);
+  const int rsub = threadIdx.x / kCsrLanes;
+  const double* __restrict__ Zd = win.p[nwin - 1];
+  const int64_t n = op.n;
+  const int64_t ntiles = (n + T - 1) / T;
+  uint32_t phase = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i0 = tile * T, i1 = min(n, i0 + T);
+    int64_t w0 = max(-gz, i0 - band);
+    if ((gz + w0) & 1) --w0;                   // 16-byte aligned source (column data start is)
+    int64_t w1 = min(n + gz, i1 + band);
+    if ((w1 - w0) & 1) ++w1;                   // whole 16-byte units (the ring is padded)
+    __syncthreads();                           // the previous tile's gathers are done
+    if (threadIdx.x == 0) {
+      const uint64_t bytes = (uint64_t)(w1 - w0) * 8;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(bar)),
+                   "r"((uint32_t)(bytes * R))
+                   : "memory");
+      for (int c = 0; c < R; ++c)
+        for (uint64_t off = 0; off < bytes; off += 32768)
+          bulk_g2s(reinterpret_cast<char*>(zw + c * Wcap) + off, reinterpret_cast<const char*>(Zd + c * ld + w0) + off,
+                   (uint32_t)min((uint64_t)32768, bytes - off), bar);
+    }
+    {
+      uint32_t ok = 0;
+      while (!ok) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(phase)
+            : "memory");
+      }
+      phase ^= 1u;
+    }
+    // row pointers one sweep ahead (the value / index loads of a row depend on them)
+    int64_t q0 = (i0 + rsub < i1) ? __ldg(op.rp + i0 + rsub) : 0;
+    int64_t q1 = (i0 + rsub < i1) ? __ldg(op.rp + i0 + rsub + 1) : 0;
+    for (int64_t rb = i0; rb < i1; rb += kCsrWinRows) {        // block-uniform trip count
+      const int64_t row = rb + rsub;
+      const bool valid = row < i1;
+      const int64_t p0 = q0, p1 = q1;
+      {
+        const int64_t rn = row + kCsrWinRows;
+        q0 = rn < i1 ? __ldg(op.rp + rn) : 0;
+        q1 = rn < i1 ? __ldg(op.rp + rn + 1) : 0;
+      }
+      double y[R];
+#pragma unroll
+      for (int c = 0; c < R; ++c) y[c] = 0.0;
+      // the older window blocks' values of this row, issued with the CSR loads (independent of
+      // them: one memory latency per sweep instead of two)
+      double zo[K > 1 ? K - 1 : 1][R];
+#pragma unroll
+      for (int i = 0; i < K - 1; ++i)
+#pragma unroll
+        for (int a = 0; a < R; ++a) zo[i][a] = (sub == 0 && valid && i < nwin - 1) ? __ldg(win.p[i] + a * ld + row) : 0.0;
+      constexpr int kCsrU = 6;
+      double av[kCsrU];
+      int32_t cl[kCsrU];
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) {
+        const int64_t p = p0 + sub + u * kCsrLanes;
+        av[u] = p < p1 ? __ldg(op.cv + p) : 0.0;
+        cl[u] = p < p1 ? __ldg(op.ci + p) : (int32_t)w0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) {
+        if (p0 + sub + u * kCsrLanes < p1) {
+          const int64_t off = cl[u] - w0;
+#pragma unroll
+          for (int c = 0; c < R; ++c) y[c] = fma(av[u], zw[c * Wcap + off], y[c]);
+        }
+      }
+      for (int64_t p = p0 + sub + kCsrU * kCsrLanes; p < p1; p += kCsrLanes) {
+        const double a = __ldg(op.cv + p);
+        const int64_t off = __ldg(op.ci + p) - w0;
+#pragma unroll
+        for (int c = 0; c < R; ++c) y[c] = fma(a, zw[c * Wcap + off], y[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+#pragma unroll
+        for (int o = kCsrLanes / 2; o > 0; o >>= 1) y[c] += __shfl_xor_sync(SYLV_FULL_MASK, y[c], o);
+      }
+      if (sub == 0 && valid) {
+        if (Yt) {
+#pragma unroll
+          for (int c = 0; c < R; ++c) Yt[c * ld + row] = y[c];
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          if (i < nwin) {
+            double z[R];
+#pragma unroll
+            for (int a = 0; a < R; ++a) z[a] = (i == nwin - 1) ? zw[a * Wcap + (row - w0)] : zo[i < K - 1 ? i : 0][a];
+#pragma unroll
+            for (int a = 0; a < R; ++a)
+#pragma unroll
+              for (int c = 0; c < R; ++c) acc[(i * R + a) * R + c] = fma(z[a], y[c], acc[(i * R + a) * R + c]);
+          }
+        }
+      }
+    }
+  }
+  // deterministic CTA reduction (fixed warp order)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int e = 0; e < K * R * R; ++e) {
+    double s = acc[e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(SYLV_FULL_MASK, s, o);
+    if (lane == 0) red[warp * K * R * R + e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < K * R * R; e += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < kCsrWinWarps; ++w) s += red[w * K * R * R + e];
+    partial[(int64_t)blockIdx.x * K * R * R + e] = s;
+  }
+}
+
+}  // namespace sylv
