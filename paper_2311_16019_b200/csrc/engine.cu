@@ -158,6 +158,9 @@ struct Sequence {
   int64_t csrT = 0, band = 0;
   int csr_grid = 0;
   size_t csr_smem = 0;
+  int64_t* sell_ptr = nullptr;            // SELL-32 copy of the operator (k_pass1_sell_win)
+  int32_t* sell_ci = nullptr;
+  double* sell_cv = nullptr;
   int64_t gz = 0;                         // ghost rows before/after a column (N^2 3-D, N 2-D, 0 CSR)
   OpParams op{};
   SketchParams sp{};
@@ -434,6 +437,9 @@ void free_seq(Sequence& q) {
   if (q.sr_plan) cufftDestroy(q.sr_plan);
   dfree(q.sr_rows);
   dfree(q.sr_V);
+  dfree(q.sell_ptr);
+  dfree(q.sell_ci);
+  dfree(q.sell_cv);
   for (double* p : dp) dfree(p);
   dfree(q.flags);
   dfree(q.pl_list);
@@ -713,10 +719,17 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cud
 #undef SYLV_ST3D_P1
   } else if (q.op.kind == kCSR && q.csrT > 0) {
     // band window of Z_d staged in shared memory (no AoS copy, gathers from shared memory)
-    SYLV_DISPATCH_R124_K(R, K, {
-      k_pass1_csr_win<R_, K_><<<q.csr_grid, kCsrWinThreads, q.csr_smem, st>>>(q.op, win, nwin, q.ld, q.gz, q.band,
-                                                                              q.csrT, q.Yt, q.part1);
-    });
+    if (q.sell_cv) {
+      SYLV_DISPATCH_R124_K(R, K, {
+        k_pass1_sell_win<R_, K_><<<q.csr_grid, kCsrWinThreads, q.csr_smem, st>>>(
+            q.op, win, nwin, q.ld, q.gz, q.band, q.csrT, q.sell_ptr, q.sell_ci, q.sell_cv, q.Yt, q.part1);
+      });
+    } else {
+      SYLV_DISPATCH_R124_K(R, K, {
+        k_pass1_csr_win<R_, K_><<<q.csr_grid, kCsrWinThreads, q.csr_smem, st>>>(q.op, win, nwin, q.ld, q.gz, q.band,
+                                                                                q.csrT, q.Yt, q.part1);
+      });
+    }
     count(c);
   } else if (q.op.kind == kCSR && R <= 4) {
     if (R % 2 == 0) {   // AoS copy of Z_d for the gathers
@@ -951,7 +964,32 @@ void setup_csr_window(sylv_ctx* c, Sequence& q) {
   q.csr_grid = (int)std::min<int64_t>(c->sm, (c->n + T - 1) / T);
   SYLV_DISPATCH_R124_K(R, K, {
     CK(cudaFuncSetAttribute(k_pass1_csr_win<R_, K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.csr_smem));
+    CK(cudaFuncSetAttribute(k_pass1_sell_win<R_, K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.csr_smem));
   });
+  // SELL-32 copy (SYLV_SELL=0: the CSR-stream kernel k_pass1_csr_win)
+  const char* se = std::getenv("SYLV_SELL");
+  if (se && std::strcmp(se, "0") == 0) return;
+  const int64_t ns = (c->n + 31) / 32;
+  int64_t* w = dalloc<int64_t>(ns + 1);
+  q.sell_ptr = dalloc<int64_t>(ns + 1);
+  CK(cudaMemsetAsync(w + ns, 0, sizeof(int64_t), c->st));
+  k_sell_widths<<<(int)std::min<int64_t>(4096, (ns + 255) / 256), 256, 0, c->st>>>(q.rp, c->n, w);
+  size_t tb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, w, q.sell_ptr, (int)(ns + 1), c->st));
+  void* tmp = dalloc<char>(tb);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tb, w, q.sell_ptr, (int)(ns + 1), c->st));
+  int64_t total = 0;
+  CK(cudaMemcpyAsync(&total, q.sell_ptr + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  dfree(w);
+  dfree(tmp);
+  q.sell_ci = dalloc<int32_t>(std::max<int64_t>(1, total));
+  q.sell_cv = dalloc<double>(std::max<int64_t>(1, total));
+  k_sell_fill<<<(int)std::min<int64_t>(4096, (ns * 32 + 255) / 256), 256, 0, c->st>>>(q.rp, q.ci, q.cv, c->n, q.sell_ptr,
+                                                                                     q.sell_ci, q.sell_cv);
+  count(c, 2);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->st));
 }
 
 void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, bool transpose,
@@ -2189,11 +2227,18 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     // past the every-10 regime: when the log-linear extrapolation of the last two checks puts
     // the crossing well before the next scheduled check, check just past the prediction
     // instead (same first crossing after the search below; fewer large projected solves)
-    if (seen.size() >= 2 && (int64_t)sched[idx] * c->R > 800) {
+    // (round 2) and in any regime a scheduled check (not the last) is skipped while the
+    // predicted crossing lies more than 10 steps past it — the extrapolation underestimates the
+    // crossing when convergence slows, and the search below brackets the first crossing anyway
+    if (seen.size() >= 2) {
       const auto& a = seen[seen.size() - 2];
       const auto& b = seen.back();
       const double dh = predict(a.first, a.second, b.first, b.second);
-      if (std::isfinite(dh) && dh + 2 < sched[idx]) sched[idx] = std::max(b.first + 1, (int)std::ceil(dh) + 2);
+      if (std::isfinite(dh) && (int64_t)sched[idx] * c->R > 800 && dh + 2 < sched[idx]) {
+        sched[idx] = std::max(b.first + 1, (int)std::ceil(dh) + 2);
+      } else if (std::isfinite(dh) && dh - 10 > sched[idx] && idx + 1 < sched.size()) {
+        continue;
+      }
     }
     const int dc = sched[idx];
     if (dc > c->dmax) break;

@@ -910,3 +910,164 @@ __global__ void __launch_bounds__(kCsrWinThreads, 1)
 }
 
 }  // namespace sylv
+
+namespace sylv {
+
+// =====================================================================================
+// SELL-32 copy of a CSR operator (built once at init) for the windowed pass 1
+// =====================================================================================
+// Slice s holds rows 32 s .. 32 s + 31; its width w_s = max nnz of those rows; entry k of the
+// slice's row (32 s + l) is at sptr[s] + 32 k + l (padding: value 0, column = the row itself,
+// which always lies in the band window).  A warp then streams a slice with one coalesced
+// 256-byte value load and one 128-byte index load per k, lane = row: no per-row shuffles.
+__global__ void k_sell_widths(const int64_t* __restrict__ rp, int64_t n, int64_t* __restrict__ width) {
+  const int64_t ns = (n + 31) / 32;
+  for (int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sl < ns; sl += (int64_t)gridDim.x * blockDim.x) {
+    int64_t w = 0;
+    for (int64_t r = sl * 32; r < min(n, sl * 32 + 32); ++r) w = max(w, rp[r + 1] - rp[r]);
+    width[sl] = w * 32;
+  }
+}
+
+__global__ void k_sell_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ cv, int64_t n, const int64_t* __restrict__ sptr,
+                            int32_t* __restrict__ sci, double* __restrict__ scv) {
+  const int64_t ns = (n + 31) / 32;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < ns * 32; row += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = row / 32, l = row % 32;
+    const int64_t w = (sptr[sl + 1] - sptr[sl]) / 32;
+    const int64_t p0 = row < n ? rp[row] : 0, p1 = row < n ? rp[row + 1] : 0;
+    for (int64_t k = 0; k < w; ++k) {
+      const int64_t p = p0 + k;
+      const bool ok = p < p1;
+      sci[sptr[sl] + 32 * k + l] = ok ? ci[p] : (int32_t)min(row, n - 1);
+      scv[sptr[sl] + 32 * k + l] = ok ? cv[p] : 0.0;
+    }
+  }
+}
+
+// Windowed pass 1 on the SELL-32 copy: CTA = tiles of T rows (T multiple of 32), band window of
+// Z_d in shared memory (bulk copies, as k_pass1_csr_win), warp = slice, lane = row.
+template <int R, int K>
+__global__ void __launch_bounds__(kCsrWinThreads, 1)
+    k_pass1_sell_win(OpParams op, Win win, int nwin, int64_t ld, int64_t gz, int64_t band, int64_t T,
+                     const int64_t* __restrict__ sptr, const int32_t* __restrict__ sci,
+                     const double* __restrict__ scv, double* __restrict__ Yt, double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char sell_smraw[];
+  const int64_t Wcap = T + 2 * band + 2;
+  double* zw = reinterpret_cast<double*>(sell_smraw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(zw + (int64_t)R * Wcap);
+  __shared__ double red[kCsrWinWarps * K * R * R];
+  double acc[K * R * R];
+#pragma unroll
+  for (int e = 0; e < K * R * R; ++e) acc[e] = 0.0;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* __restrict__ Zd = win.p[nwin - 1];
+  const int64_t n = op.n;
+  const int64_t ntiles = (n + T - 1) / T;
+  uint32_t phase = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i0 = tile * T, i1 = min(n, i0 + T);
+    int64_t w0 = max(-gz, i0 - band);
+    if ((gz + w0) & 1) --w0;
+    int64_t w1 = min(n + gz, i1 + band);
+    if ((w1 - w0) & 1) ++w1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t bytes = (uint64_t)(w1 - w0) * 8;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(bar)),
+                   "r"((uint32_t)(bytes * R))
+                   : "memory");
+      for (int c = 0; c < R; ++c)
+        for (uint64_t off = 0; off < bytes; off += 32768)
+          bulk_g2s(reinterpret_cast<char*>(zw + c * Wcap) + off, reinterpret_cast<const char*>(Zd + c * ld + w0) + off,
+                   (uint32_t)min((uint64_t)32768, bytes - off), bar);
+    }
+    {
+      uint32_t ok = 0;
+      while (!ok) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(phase)
+            : "memory");
+      }
+      phase ^= 1u;
+    }
+    for (int64_t sl = i0 / 32 + warp; sl * 32 < i1; sl += kCsrWinWarps) {
+      const int64_t row = sl * 32 + lane;
+      const bool valid = row < i1;
+      // window blocks' values of this row (independent of the slice stream)
+      double zo[K > 1 ? K - 1 : 1][R];
+#pragma unroll
+      for (int i = 0; i < K - 1; ++i)
+#pragma unroll
+        for (int a = 0; a < R; ++a) zo[i][a] = (valid && i < nwin - 1) ? __ldg(win.p[i] + a * ld + row) : 0.0;
+      const int64_t b0 = __ldg(sptr + sl), b1 = __ldg(sptr + sl + 1);
+      double y[R];
+#pragma unroll
+      for (int c = 0; c < R; ++c) y[c] = 0.0;
+      int64_t p = b0 + lane;
+      for (; p + 3 * 32 < b1; p += 4 * 32) {       // 4 entries in flight
+        double v[4];
+        int32_t cl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v[u] = __ldg(scv + p + 32 * u);
+          cl[u] = __ldg(sci + p + 32 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t off = cl[u] - w0;
+#pragma unroll
+          for (int c = 0; c < R; ++c) y[c] = fma(v[u], zw[c * Wcap + off], y[c]);
+        }
+      }
+      for (; p < b1; p += 32) {
+        const double v = __ldg(scv + p);
+        const int64_t off = __ldg(sci + p) - w0;
+#pragma unroll
+        for (int c = 0; c < R; ++c) y[c] = fma(v, zw[c * Wcap + off], y[c]);
+      }
+      if (valid) {
+        if (Yt) {
+#pragma unroll
+          for (int c = 0; c < R; ++c) Yt[c * ld + row] = y[c];
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          if (i < nwin) {
+            double z[R];
+#pragma unroll
+            for (int a = 0; a < R; ++a) z[a] = (i == nwin - 1) ? zw[a * Wcap + (row - w0)] : zo[i < K - 1 ? i : 0][a];
+#pragma unroll
+            for (int a = 0; a < R; ++a)
+#pragma unroll
+              for (int c = 0; c < R; ++c) acc[(i * R + a) * R + c] = fma(z[a], y[c], acc[(i * R + a) * R + c]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < K * R * R; ++e) {
+    double s = acc[e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(SYLV_FULL_MASK, s, o);
+    if (lane == 0) red[warp * K * R * R + e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < K * R * R; e += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < kCsrWinWarps; ++w) s += red[w * K * R * R + e];
+    partial[(int64_t)blockIdx.x * K * R * R + e] = s;
+  }
+}
+
+}  // namespace sylv

@@ -159,6 +159,10 @@ __global__ void __launch_bounds__(32 * TY * kWpl25, (TY <= 4 ? 2 : 1))
   constexpr int kStageD = Gm::HCOL * R + (K - 1) * Gm::WCOL * R;   // doubles per stage
   uint64_t* bars = reinterpret_cast<uint64_t*>(smraw + (size_t)kNS * kStageD * 8);
   constexpr int EL = 8 / kWpl25;                // elements per lane (of the line's 8)
+  // pass 1 with R = 4: two 4-point slices per DMMA (lanes 0-15 slice a, lanes 16-31 slice b:
+  // P_a and P_b are the diagonal 4 x 4 blocks of the 8 x 8 product), half the elements
+  constexpr bool kPack = PASS == 1 && R == 4;
+  constexpr int NE = kPack ? EL / 2 : EL;
   __shared__ double red[TY * kWpl25][64 * (PASS == 1 ? K : 1)];
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -172,12 +176,15 @@ __global__ void __launch_bounds__(32 * TY * kWpl25, (TY <= 4 ? 2 : 1))
 
   // element coordinates inside the tile (point offset px in [0,32), column col); this warp owns
   // elements half*EL .. half*EL + EL - 1 of its line
-  int px[EL], col[EL];
-  bool cok[EL];                                 // column < R (else the element is zero)
+  int px[NE], col[NE];
+  bool cok[NE];                                 // column < R (else the element is zero)
 #pragma unroll
-  for (int e = 0; e < EL; ++e) {
-    const int eg = half * EL + e;
-    if (PASS == 1) {
+  for (int e = 0; e < NE; ++e) {
+    const int eg = half * NE + e;
+    if (kPack) {
+      px[e] = 4 * (2 * eg + (lane >> 4)) + (lane & 3);
+      col[e] = (lane >> 2) & 3;
+    } else if (PASS == 1) {
       px[e] = 4 * eg + (lane & 3);
       col[e] = lane >> 2;
     } else {
@@ -227,11 +234,11 @@ __global__ void __launch_bounds__(32 * TY * kWpl25, (TY <= 4 ? 2 : 1))
     const int yrow = warp + sy;                // line inside the halo box
     const bool yok = (y0 + warp) < NN;
     const bool has_ym = (y0 + warp) > 0;       // y-1 neighbour exists
-    double zm[EL], zc[EL], zp[EL];
-    auto read_centers = [&](int q, double (&dst)[EL]) {
+    double zm[NE], zc[NE], zp[NE];
+    auto read_centers = [&](int q, double (&dst)[NE]) {
       if (q < 0) {
 #pragma unroll
-        for (int e = 0; e < EL; ++e) dst[e] = 0.0;
+        for (int e = 0; e < NE; ++e) dst[e] = 0.0;
         return;
       }
       const int s = stage_of(q);
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(32 * TY * kWpl25, (TY <= 4 ? 2 : 1))
       phase ^= 1u << s;
       const double* H = stages + (size_t)s * kStageD;
 #pragma unroll
-      for (int e = 0; e < EL; ++e) dst[e] = cok[e] ? H[(col[e] * Gm::HY + yrow) * Gm::HX + px[e] + sx] : 0.0;
+      for (int e = 0; e < NE; ++e) dst[e] = cok[e] ? H[(col[e] * Gm::HY + yrow) * Gm::HX + px[e] + sx] : 0.0;
     };
     read_centers(z0 - 1, zm);
     read_centers(z0, zc);
@@ -254,9 +261,9 @@ __global__ void __launch_bounds__(32 * TY * kWpl25, (TY <= 4 ? 2 : 1))
       read_centers(z + 1, zp);                  // waits for plane z+1 (plane z is ready since z-1)
       const double* H = stages + (size_t)stage_of(z) * kStageD;
       const double* Wb = H + Gm::HCOL * R;
-      double y[EL];
+      double y[NE];
 #pragma unroll
-      for (int e = 0; e < EL; ++e) {
+      for (int e = 0; e < NE; ++e) {
         if (!cok[e]) {
           y[e] = 0.0;
           continue;
@@ -276,7 +283,7 @@ __global__ void __launch_bounds__(32 * TY * kWpl25, (TY <= 4 ? 2 : 1))
       if (PASS == 1) {
         // P_i += Z_i^T Y over the 4-point slices e (pattern A: lane (col L>>2, point L&3))
 #pragma unroll
-        for (int e = 0; e < EL; ++e) {
+        for (int e = 0; e < NE; ++e) {
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             if (i < nwin - 1) {
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(32 * TY * kWpl25, (TY <= 4 ? 2 : 1))
         }
       }
 #pragma unroll
-      for (int e = 0; e < EL; ++e) {
+      for (int e = 0; e < NE; ++e) {
         zm[e] = zc[e];
         zc[e] = zp[e];
       }
@@ -364,7 +371,10 @@ __global__ void __launch_bounds__(32 * TY * kWpl25, (TY <= 4 ? 2 : 1))
       const int i = e / (R * R), a = (e / R) % R, c = e % R;      // R x R blocks of the 8 x 8 D
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < TY * kWpl25; ++w) s += red[w][i * 64 + a * 8 + c];
+      for (int w = 0; w < TY * kWpl25; ++w) {
+        s += red[w][i * 64 + a * 8 + c];
+        if (kPack) s += red[w][i * 64 + (a + 4) * 8 + (c + 4)];   // slice b's diagonal block
+      }
       partial[(int64_t)blockIdx.x * NA * R * R + (slot0 >= 0 ? slot0 * R * R + e : e)] = s;
     }
   }
