@@ -94,3 +94,39 @@ def test_bench_reference_arm_contract():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_buffer_checks_refuse_wrong_dtype_shape_and_copies():
+    """The binding passes raw double* to the library: a wrong dtype, a wrong shape or a
+    non-contiguous numpy output (which would be silently copied and the result lost) must be
+    refused before the C call."""
+    import numpy as np
+    from paper_2311_16019_b200.api import _ptr
+    good = np.zeros((10, 4))
+    assert _ptr(good, shape=(10, 4), out=True)[0] == good.ctypes.data
+    with pytest.raises(ValueError):
+        _ptr(np.zeros((10, 4), dtype=np.float32), shape=(10, 4), out=True)
+    with pytest.raises(ValueError):
+        _ptr(np.zeros((10, 3)), shape=(10, 4), out=True)
+    with pytest.raises(ValueError):
+        _ptr(np.zeros((4, 10)).T, shape=(10, 4), out=True)          # non-contiguous output
+    with pytest.raises(ValueError):
+        _ptr(np.zeros((9, 4)), shape=(10, 4))                       # input of the wrong shape
+    p, keep = _ptr(np.zeros((4, 10)).T, shape=(10, 4))              # inputs may be copied
+    assert keep.flags.c_contiguous and keep.shape == (10, 4)
+    torch = pytest.importorskip("torch")
+    with pytest.raises(TypeError):
+        _ptr(torch.zeros((10, 4), dtype=torch.float32), shape=(10, 4))
+    with pytest.raises(ValueError):
+        _ptr(torch.zeros((4, 10), dtype=torch.float64).t(), shape=(10, 4))
+
+
+def test_config_struct_layout_matches_header():
+    """sylv_config fields in the ctypes mirror appear in the header in the same order (the
+    struct is passed by pointer: a missing or reordered field corrupts every later one)."""
+    from paper_2311_16019_b200.api import Config
+    txt = open(os.path.join(ROOT, "include", "sylv_sketch.h")).read()
+    body = txt[txt.index("typedef struct {\n  int32_t r;"):txt.index("} sylv_config;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"\b([a-z_0-9]+)\s*;", body)
+    assert fields == [f for f, _ in Config._fields_]
