@@ -1,7 +1,7 @@
 """Summarise ncu outputs into small JSON files for profiles/ (development tool).
 
   python tools/ncu_summary.py launches <launches.csv> <out.json>
-  python tools/ncu_summary.py full <report.ncu-rep> <out.json>
+  python tools/ncu_summary.py full <report.ncu-rep | raw.csv> <out.json>
 """
 import collections
 import csv
@@ -48,8 +48,15 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__shared_mem_per_block_dynamic"]
 
 
+WANT += ["lts__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+         "l1tex__throughput.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+
+
 def full(path, out):
-    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):                     # `ncu -i rep --page raw --csv` exported on the box
+        txt = open(path).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, u = rows[0], rows[1]
     res = {"source": path, "kernels": []}
