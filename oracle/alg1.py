@@ -328,11 +328,10 @@ def solve(obj: SylvesterSketchedKrylov, tol: float, d_max: int, keep_Y=True) -> 
 
     Schedule: check_schedule(); past its every-10 regime, when the log-linear extrapolation of
     the last two valid checks puts the crossing d_hat before the next scheduled check, the
-    next check is at max(d_last + 1, ceil(d_hat) + 2) instead; in any regime, a scheduled check
-    (not the last) is skipped while d_hat lies more than 10 steps past it (round 2: the
-    extrapolation underestimates the crossing when convergence slows, so a skipped check would
-    have failed; with faster-than-predicted convergence the search below still brackets the
-    first crossing).  Search on the bracket
+    next check is at max(d_last + 1, ceil(d_hat) + 2) instead; inside the every-10 regime a
+    check is skipped while d_hat lies more than 10 steps past it and the next check is still in
+    that regime (round 2: the cheap early checks; skipping into the geometric regime overshot
+    c1's crossing by 250 steps in a simulation on the goldens' rho(d), so it is not done).  Search on the bracket
     (d_fail, d_pass]: regula falsi on log rho_rel (x = lo + (log r_lo - log tol) /
     (log r_lo - log r_hi) (hi - lo), checked at ceil(x) clamped into the bracket, or at hi - 1 when
 that is within 2 of hi), a bisection
@@ -351,8 +350,9 @@ that is within 2 of hi), a bisection
             dh = _predict_crossing(d1, r1, d2, r2, tol)
             if math.isfinite(dh) and sched[idx] * obj.r > 800 and dh + 2 < sched[idx]:
                 sched[idx] = max(d2 + 1, math.ceil(dh) + 2)
-            elif math.isfinite(dh) and dh - 10 > sched[idx] and idx + 1 < len(sched):
-                continue          # crossing predicted > 10 steps past this check: skip it (R9)
+            elif (math.isfinite(dh) and dh - 10 > sched[idx] and idx + 1 < len(sched)
+                  and sched[idx + 1] * obj.r <= 800):
+                continue          # every-10 regime: crossing predicted > 10 steps past: skip (R9)
         dc = sched[idx]
         t0 = time.perf_counter()
         while obj.d < dc and not obj.breakdown:

@@ -2227,16 +2227,17 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     // past the every-10 regime: when the log-linear extrapolation of the last two checks puts
     // the crossing well before the next scheduled check, check just past the prediction
     // instead (same first crossing after the search below; fewer large projected solves)
-    // (round 2) and in any regime a scheduled check (not the last) is skipped while the
-    // predicted crossing lies more than 10 steps past it — the extrapolation underestimates the
-    // crossing when convergence slows, and the search below brackets the first crossing anyway
+    // (round 2) inside the every-10 regime a check is skipped while the predicted crossing lies
+    // more than 10 steps past it and the next check is still in that regime (skipping into the
+    // geometric regime overshot c1's crossing by 250 steps: one m = 4148 solve, ~20 s)
     if (seen.size() >= 2) {
       const auto& a = seen[seen.size() - 2];
       const auto& b = seen.back();
       const double dh = predict(a.first, a.second, b.first, b.second);
       if (std::isfinite(dh) && (int64_t)sched[idx] * c->R > 800 && dh + 2 < sched[idx]) {
         sched[idx] = std::max(b.first + 1, (int)std::ceil(dh) + 2);
-      } else if (std::isfinite(dh) && dh - 10 > sched[idx] && idx + 1 < sched.size()) {
+      } else if (std::isfinite(dh) && dh - 10 > sched[idx] && idx + 1 < sched.size() &&
+                 (int64_t)sched[idx + 1] * c->R <= 800) {
         continue;
       }
     }
