@@ -87,6 +87,8 @@ typedef struct {
   const int32_t* col_idx;
   const double* val;
   int64_t nnz;
+  int32_t is_transposed; /* CSR operator B only: 1 = the arrays already hold B^T (no
+                            transpose at init); 0 = B (transposed on the device at init) */
 } sylv_operator;
 
 typedef struct {
@@ -256,6 +258,11 @@ sylv_status sylv_partition(int32_t kind, int32_t N, int64_t n, int32_t nranks, i
  * sylv_comm_create_nccl collectively.  libnccl.so.2 is dlopen'ed (SYLV_E_NCCL if absent). */
 sylv_status sylv_comm_nccl_unique_id(uint8_t id[128]);
 sylv_status sylv_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id[128], sylv_comm** out);
+/* NCCL transport over a communicator the CALLER owns (an ncclComm_t, passed as void*): the
+ * library splits its per-channel communicators from it (collective over its ranks) and
+ * destroys only those splits in sylv_comm_destroy; the caller's communicator stays the
+ * caller's (destroy it after sylv_comm_destroy). */
+sylv_status sylv_comm_wrap_nccl(void* nccl_comm, sylv_comm** out);
 
 /* In-process transport: nranks virtual ranks of ONE process on one GPU, one host thread per
  * rank calling the context functions collectively (parity tests of the sharded path on a

@@ -6,4 +6,4 @@ this package is a thin ctypes binding (api.py) plus its build script (build.py).
 """
 from .api import (SylvSketch, SylvError, Operator, Config, Stats, stencil_operator,  # noqa: F401
                   csr_operator, operators_for, from_config, load_library, version, LIB_PATH, SYMBOLS,
-                  partition, Comm, LocalGroup, nccl_comm)
+                  partition, Comm, LocalGroup, nccl_comm, wrap_nccl)

@@ -32,7 +32,7 @@ class SylvError(RuntimeError):
 class Operator(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n", C.c_int64), ("grid", C.c_int32 * 3), ("nu", C.c_double),
                 ("w", C.c_double * 3), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p),
-                ("val", C.c_void_p), ("nnz", C.c_int64)]
+                ("val", C.c_void_p), ("nnz", C.c_int64), ("is_transposed", C.c_int32)]
 
 
 class Config(C.Structure):
@@ -66,7 +66,8 @@ SYMBOLS = ["sylv_sketch_init", "sylv_sketch_step", "sylv_sketch_residual", "sylv
            "sylv_sketch_get_block", "sylv_sketch_history", "sylv_sketch_stats",
            "sylv_sketch_reset_stats", "sylv_sketch_last_error", "sylv_sketch_destroy",
            "sylv_set_lapack_path", "sylv_version", "sylv_host_projected", "sylv_host_sylvester",
-           "sylv_partition", "sylv_comm_nccl_unique_id", "sylv_comm_create_nccl", "sylv_local_group_create",
+           "sylv_partition", "sylv_comm_nccl_unique_id", "sylv_comm_create_nccl", "sylv_comm_wrap_nccl",
+           "sylv_local_group_create",
            "sylv_local_group_destroy", "sylv_comm_create_local", "sylv_comm_destroy"]
 
 
@@ -123,6 +124,8 @@ def load_library(path: str = LIB_PATH):
     lib.sylv_comm_nccl_unique_id.restype = C.c_int
     lib.sylv_comm_create_nccl.argtypes = [C.c_int32, C.c_int32, P, C.POINTER(P)]
     lib.sylv_comm_create_nccl.restype = C.c_int
+    lib.sylv_comm_wrap_nccl.argtypes = [P, C.POINTER(P)]
+    lib.sylv_comm_wrap_nccl.restype = C.c_int
     lib.sylv_local_group_create.argtypes = [C.c_int32, C.POINTER(P)]
     lib.sylv_local_group_create.restype = C.c_int
     lib.sylv_local_group_destroy.argtypes = [P]
@@ -187,10 +190,13 @@ def stencil_operator(kind: str, N: int, w, nu: float = 1.0) -> Operator:
     return op
 
 
-def csr_operator(n: int, row_ptr, col_idx, val):
+def csr_operator(n: int, row_ptr, col_idx, val, is_transposed: bool = False):
+    """CSR descriptor (host or device arrays).  For the operator B, is_transposed = True means the
+    arrays already hold B^T (no device transpose at init)."""
     op = Operator()
     op.kind = OP_CSR
     op.n = n
+    op.is_transposed = 1 if is_transposed else 0
     keep = []
     for name, arr, dt in (("row_ptr", row_ptr, np.int64), ("col_idx", col_idx, np.int32), ("val", val, np.float64)):
         p, k = _ptr(arr, dtype=dt)
@@ -430,6 +436,17 @@ def nccl_comm(group=None) -> Comm:
     st = lib.sylv_comm_create_nccl(world, rank, uid2, C.byref(h))
     if st != OK:
         raise SylvError(st, "sylv_comm_create_nccl")
+    return Comm(h)
+
+
+def wrap_nccl(nccl_comm_ptr: int) -> Comm:
+    """NCCL transport over a communicator the caller owns (an ncclComm_t address): the library
+    splits its channels from it and never destroys it (sylv_comm_wrap_nccl)."""
+    lib = load_library()
+    h = C.c_void_p()
+    st = lib.sylv_comm_wrap_nccl(C.c_void_p(nccl_comm_ptr), C.byref(h))
+    if st != OK:
+        raise SylvError(st, "sylv_comm_wrap_nccl")
     return Comm(h)
 
 

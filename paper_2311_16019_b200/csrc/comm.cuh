@@ -69,6 +69,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
@@ -95,6 +97,8 @@ inline NcclApi& nccl_api() {
     SYLV_NCCL_SYM(CommInitRank);
     SYLV_NCCL_SYM(CommSplit);
     SYLV_NCCL_SYM(CommDestroy);
+    SYLV_NCCL_SYM(CommCount);
+    SYLV_NCCL_SYM(CommUserRank);
     SYLV_NCCL_SYM(AllReduce);
     SYLV_NCCL_SYM(AllGather);
     SYLV_NCCL_SYM(ReduceScatter);
@@ -136,11 +140,26 @@ struct NcclComm : Comm {
       throw;
     }
   }
+  // over a caller-owned communicator: the channels are split from it, it is never destroyed here
+  explicit NcclComm(ncclComm_t caller) {
+    NcclApi& a = nccl_api();
+    if (!a.CommSplit || !a.AllReduce || !a.Send || !a.CommCount || !a.CommUserRank)
+      throw CommError{"libnccl not loadable"};
+    nccl_check(a.CommCount(caller, &nranks), "ncclCommCount");
+    nccl_check(a.CommUserRank(caller, &rank), "ncclCommUserRank");
+    try {
+      for (int i = 0; i < kNumChan; ++i) nccl_check(a.CommSplit(caller, 0, rank, &ch[i], nullptr), "ncclCommSplit");
+    } catch (...) {
+      for (auto& c : ch)
+        if (c) a.CommDestroy(c), c = nullptr;
+      throw;
+    }
+  }
   ~NcclComm() override {
     NcclApi& a = nccl_api();
     for (auto& c : ch)
       if (c) a.CommDestroy(c);
-    if (base) a.CommDestroy(base);
+    if (base) a.CommDestroy(base);   // only the library's own base communicator
     if (dscratch) cudaFree(dscratch);
   }
   void allreduce(double* buf, size_t n, cudaStream_t st, int chan) override {

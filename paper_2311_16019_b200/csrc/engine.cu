@@ -1007,7 +1007,7 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
   q.gz = (A->kind == SYLV_OP_STENCIL3D) ? (int64_t)A->grid[0] * A->grid[0]
          : (A->kind == SYLV_OP_STENCIL2D) ? (int64_t)A->grid[0] : 0;
   if (A->kind == SYLV_OP_CSR) {
-    upload_csr(q, A, transpose, c->st);          // the global matrix (A, or B^T); sets q.op's arrays
+    upload_csr(q, A, transpose && !A->is_transposed, c->st);   // the global matrix (A, or B^T); sets q.op's arrays
     if (c->comm) shard_csr(c, q);                // this rank's rows; q.gz = band
   }
   q.ld = (c->n + 2 * q.gz + 63) / 64 * 64;
@@ -1657,6 +1657,20 @@ sylv_status sylv_comm_create_nccl(int32_t nranks, int32_t rank, const uint8_t id
     return SYLV_OK;
   } catch (const CommError& e) {
     std::fprintf(stderr, "sylv_comm_create_nccl: %s\n", e.what.c_str());
+    return SYLV_E_NCCL;
+  }
+}
+
+sylv_status sylv_comm_wrap_nccl(void* nccl_comm, sylv_comm** out) {
+  if (!out || !nccl_comm) return SYLV_E_INVALID;
+  *out = nullptr;
+  try {
+    std::unique_ptr<sylv_comm> c(new sylv_comm());
+    c->impl = new NcclComm(static_cast<ncclComm_t>(nccl_comm));
+    *out = c.release();
+    return SYLV_OK;
+  } catch (const CommError& e) {
+    std::fprintf(stderr, "sylv_comm_wrap_nccl: %s\n", e.what.c_str());
     return SYLV_E_NCCL;
   }
 }

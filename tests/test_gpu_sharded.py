@@ -182,3 +182,63 @@ def test_nccl_transport_world_size_one():
     a.close()
     b.close()
     comm.close()
+
+
+def test_csr_operator_passed_already_transposed():
+    """sylv_operator.is_transposed: passing B^T's CSR arrays (no device transpose) gives the same
+    iteration as passing B (the library transposes on the device)."""
+    import scipy.sparse as sp
+    pkg = _pkg()
+    cfg = inputs.small_config(kind="csr", n=5003, nnz_off=6, band=40, r=2, k=2, d_max=30)
+    (ra, ca, va), (rb, cb, vb) = inputs.config_csr(cfg)
+    C1, C2 = inputs.make_rhs(cfg)
+    Bt = sp.csr_matrix((vb, cb.astype(np.int64), rb), shape=(cfg.n, cfg.n)).T.tocsr()
+    Bt.sort_indices()
+    runs = []
+    for transposed in (False, True):
+        A = pkg.csr_operator(cfg.n, ra, ca, va)
+        Bop = (pkg.csr_operator(cfg.n, Bt.indptr.astype(np.int64), Bt.indices.astype(np.int32), Bt.data,
+                                is_transposed=True) if transposed else pkg.csr_operator(cfg.n, rb, cb, vb))
+        g = pkg.SylvSketch(A[0], Bop[0], torch.from_numpy(C1).cuda(), torch.from_numpy(C2).cuda(), r=cfg.r, k=cfg.k,
+                           d_max=cfg.d_max, s=cfg.s, keep=[A[1], Bop[1]])
+        g.step(15)
+        runs.append([g.residual(d)[1] for d in range(1, 16)])
+        g.close()
+    np.testing.assert_allclose(runs[1], runs[0], rtol=1e-12, atol=1e-18)
+
+
+def test_wrap_caller_owned_nccl_communicator(tmp_path):
+    """sylv_comm_wrap_nccl over torch's own NCCL communicator (world size 1): a sharded-path
+    context runs on it, and destroying the library's comm leaves torch's usable."""
+    import os
+    import torch.distributed as dist
+    pkg = _pkg()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        t = torch.ones(1, device="cuda")
+        dist.all_reduce(t)                                   # creates torch's communicator
+        pg = dist.distributed_c10d._get_default_group()
+        try:
+            ptr = pg._get_backend(torch.device("cuda"))._comm_ptr()
+        except Exception as e:                               # pragma: no cover (older torch)
+            pytest.skip(f"torch does not expose its ncclComm_t: {e}")
+        comm = pkg.wrap_nccl(ptr)
+        cfg = inputs.small_config(kind="stencil3d", N=16, r=4, k=2, d_max=20)
+        C1, C2 = inputs.make_rhs(cfg)
+        g = pkg.from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), comm=comm,
+                            row_range=(0, cfg.n))
+        g.step(8)
+        rr = g.residual(8)[1]
+        g.close()
+        comm.close()
+        ref = pkg.from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda())
+        ref.step(8)
+        assert rr == pytest.approx(ref.residual(8)[1], rel=1e-12)
+        ref.close()
+        dist.all_reduce(t)                                   # torch's communicator still works
+        torch.cuda.synchronize()
+        assert t.item() == 1.0
+    finally:
+        dist.destroy_process_group()
