@@ -101,7 +101,8 @@ typedef struct {
   uint64_t seed_v;       /* hash seed of S_V                                   */
   double tol;            /* stop when rho_rel < tol (strict)                   */
   double rank_tol;       /* Y ~ Y1 Y2^T keeps sigma_i > rank_tol * sigma_1     */
-  int32_t chunk;         /* second pass: blocks per X accumulation (0 = k+1)   */
+  int32_t chunk;         /* second pass: blocks per X accumulation (0 = auto:   
+                            up to 32, within half the free device memory)     */
   int32_t flags;         /* bit 0: time the n-space passes with CUDA events;
                             bit 1: run everything on one stream (isolated kernel
                             timings; default: U and V passes on two streams, each

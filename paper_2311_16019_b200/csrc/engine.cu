@@ -1805,7 +1805,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     c->s = sketched ? cfg->s : (int64_t)(cfg->d_max + 1) * r;   // unsketched: s only sizes unused scratch
     c->tol = cfg->tol;
     c->rank_tol = cfg->rank_tol > 0 ? cfg->rank_tol : 1e-12;
-    c->chunk = cfg->chunk > 0 ? std::min(cfg->chunk, kMaxChunk) : std::min(cfg->k + 1, kMaxChunk);
+    c->chunk = cfg->chunk > 0 ? std::min(cfg->chunk, kMaxChunk) : 0;   // 0: auto (second pass)
     c->cflags = cfg->flags;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -2055,8 +2055,8 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
     if (rank) *rank = l;
     double* Xout[2] = {X1, X2};
     std::vector<double>* Ys[2] = {&Y1, &Y2};
-    const int C = c->chunk;
     for (int qi = 0; qi < 2; ++qi) {
+      int C = c->chunk;   // 0: chosen below from the free device memory
       Sequence& q = c->seq[qi];
       // Z = T_d^{-1} Y_q ; M_b = R_b Z[b-block]  (U_b = Z_b R_b)
       trsm_left_upper(m, l, q.Th, q.ldT, Ys[qi]->data());
@@ -2094,6 +2094,15 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
         dfree(Md);
       } else if (l > 0) {
         double* Md = dalloc<double>(M.size());
+        if (C <= 0) {
+          // replay chunk: every chunk of C blocks is one pass over X (n x l) — with the default
+          // C = k + 1 the X traffic dominated the second pass (c3 at rank 216: 58 passes over
+          // 29 GB per sequence); use up to half the free memory for up to kMaxChunk blocks
+          size_t fr = 0, tot = 0;
+          CK(cudaMemGetInfo(&fr, &tot));
+          const int64_t blkb = q.ld * r * (int64_t)sizeof(double);
+          C = (int)std::max<int64_t>(c->K + 1, std::min<int64_t>(kMaxChunk, (int64_t)(fr / 2) / blkb - K));
+        }
         double* rbuf = dalloc<double>((size_t)(K + C) * q.ld * r);
         CK(cudaMemsetAsync(rbuf, 0, (size_t)(K + C) * q.ld * r * sizeof(double), c->st));   // ghosts = 0
         CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));

@@ -743,7 +743,7 @@ __global__ void k_soa_mul_rowmajor(int64_t n, const double* __restrict__ Z, int6
 
 // Second pass (a7): blocks per X accumulation (the replay keeps k + chunk blocks; the
 // accumulation X += [U_j0 .. U_j] M is a cuBLAS DGEMM per run of adjacent replay slots, engine.cu)
-constexpr int kMaxChunk = 16;
+constexpr int kMaxChunk = 32;   // replay blocks per X accumulation chunk (second pass)
 
 }  // namespace sylv
 
