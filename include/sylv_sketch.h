@@ -111,9 +111,9 @@ typedef struct {
                             even N) and use the generic pass kernels;
                             bit 3: projected solves on the device for every d;
                             bit 4: projected solves on the host for every d
-                            (default: device when d r >= 512, host below);
-                            bit 5: fused pass 2 + old-block pass 1 for the 3-D TMA
-                            path (k >= 2; opt-in, slower on B200) */
+                            (default: device when d r >= 512, host below).
+                            (Round 1's bit 5, a fused pass 2 + old-block pass 1,
+                            measured slower and was removed in round 2: DESIGN.md §9) */
   int64_t row_begin;     /* sharded contexts: this rank's global rows [row_begin, */
   int64_t row_end;       /* row_end); 0, 0 = sylv_partition's balanced split.     */
                          /* Single-rank contexts: 0, 0 (or 0, n).                  */

@@ -27,7 +27,6 @@
 #include "nspace.cuh"
 #include "sspace.cuh"
 #include "stencil25d.cuh"
-#include "stencil25d_fused.cuh"
 #include "sketch_pull.cuh"
 #include "comm.cuh"
 #include "proj_gpu.cuh"
@@ -143,7 +142,6 @@ struct TimedPair {
 struct Sequence {
   // 2.5-D TMA passes (3-D stencil, r = 8, even N): tensor maps of the ring slots
   CUtensorMap mapH[kMaxKTma + 1];   // halo boxes
-  bool fused = false;            // pass 2 fused with the old-block part of the next pass 1
   CUtensorMap mapW[kMaxKTma + 1];   // window boxes
   bool tma = false;
   St25 st25{};
@@ -245,7 +243,7 @@ struct sylv_ctx {
   int sm = 148;
   int G = 0;          // grid of the n-space passes
   int G25 = 0;        // grid of the 2.5-D TMA passes (0: not used)
-  size_t smem25_1 = 0, smem25_2 = 0, smem25_f = 0;
+  size_t smem25_1 = 0, smem25_2 = 0;
   int RT = 1;         // row tiles of Q^T w
   int64_t tileQ = 0;
   int CC = 1;         // column chunks of Q c
@@ -555,17 +553,6 @@ void set_smem25(sylv_ctx* c) {
   CK(cudaFuncSetAttribute(k_st3d<kTY25, R, K, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_2));
 }
 
-template <int R, int K>
-size_t smem25f_bytes() {
-  return (size_t)3 * fused_stage_doubles<kTY25, R, K>() * 8 + 3 * 8;
-}
-
-template <int R, int K>
-void set_smem25f(sylv_ctx* c) {
-  c->smem25_f = smem25f_bytes<R, K>();
-  CK(cudaFuncSetAttribute(k_st3d_fused<kTY25, R, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem25_f));
-}
-
 // Set up the TMA path for sequence q if eligible: 3-D stencil, r = 4 or 8, even N.
 void setup_tma(sylv_ctx* c, Sequence& q) {
   q.tma = false;
@@ -601,32 +588,6 @@ void setup_tma(sylv_ctx* c, Sequence& q) {
   p.czm = q.op.czm; p.czp = q.op.czp;
   p.dbg = getenv("SYLV_DBG") ? atoi(getenv("SYLV_DBG")) : 0;
   c->G25 = (int)std::min<int64_t>(p.items, grid);
-  // fused pass 2 + old-block pass 1 (stencil25d_fused.cuh; opt-in: flags bit 5 or SYLV_FUSED=1).
-  // Correct (parity-tested) but slower on B200: the 2.5-D passes are bound by per-plane latency,
-  // and the fused pass's extra per-plane work (transpose stencils, shuffles, DMMAs, a third halo
-  // box) costs more than the block reads it saves (c3: pass 1 + pass 2 = 0.61 + 0.79 ms;
-  // one-block pass 1 + fused pass = 0.37 + 1.39 ms).  k >= 2; two CTAs per SM must fit.
-  const char* fe = std::getenv("SYLV_FUSED");
-  q.fused = c->K >= 2 && ((c->cflags & 32) || (fe && std::strcmp(fe, "1") == 0));
-  if (q.fused) {
-    if (c->R == 8) {
-      switch (c->K) {
-        case 2: set_smem25f<8, 2>(c); break;
-        case 3: set_smem25f<8, 3>(c); break;
-        case 4: set_smem25f<8, 4>(c); break;
-      }
-    } else {
-      switch (c->K) {
-        case 2: set_smem25f<4, 2>(c); break;
-        case 3: set_smem25f<4, 3>(c); break;
-        case 4: set_smem25f<4, 4>(c); break;
-      }
-    }
-    int smem_sm = 0, dev = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-    if (2 * (c->smem25_f + 2048) > (size_t)smem_sm) q.fused = false;   // + static + reserved
-  }
   if (c->R == 8) {
     switch (c->K) {
       case 1: set_smem25<8, 1>(c); break;
@@ -650,21 +611,6 @@ Tma25 tma_args(const Sequence& q, int j, int nwin) {
   const int ns = q.K + 1;
   tm.zd = q.mapH[j % ns];
   for (int i = 0; i < nwin - 1; ++i) tm.win[i] = q.mapW[(j - nwin + 1 + i) % ns];
-  return tm;
-}
-
-// Fused pass maps: Z_d halo, halo boxes (same geometry) of the extra A^T blocks (window slots nw ..
-// nwin-2), window boxes of the oldest nw blocks (stencil25d_fused.cuh)
-Tma25F tma_args_fused(const Sequence& q, int j, int nwin) {
-  Tma25F tm;
-  const int ns = q.K + 1;
-  const int na = std::min(q.K - 1, nwin), ne = na - 1, nw = nwin - 1 - ne;
-  tm.zd = q.mapH[j % ns];
-  for (int i = 0; i < nwin - 1; ++i) {
-    const int slot = (j - nwin + 1 + i) % ns;
-    if (i < nw) tm.win[i] = q.mapW[slot];
-    else tm.hx[i - nw] = q.mapH[slot];     // same geometry as Z_d's halo box
-  }
   return tm;
 }
 
@@ -696,10 +642,8 @@ const double* reduce_partials(sylv_ctx* c, const double* partial, int nparts, in
 void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cudaStream_t st) {
   const int R = c->R, K = c->K;
   if (q.tma) {
-    // after a fused pass (j >= 2): only P_j = Z_j^T A Z_j is left, into slot nwin-1
-    const bool one = q.fused && j >= 2;
-    const Tma25 tm = tma_args(q, j, one ? 1 : nwin);
-    const int nw1 = one ? 1 : nwin, slot0 = one ? nwin - 1 : -1;
+    const Tma25 tm = tma_args(q, j, nwin);
+    const int nw1 = nwin, slot0 = -1;
 #define SYLV_ST3D_P1(RR, KK) k_st3d<kTY25, RR, KK, 1, false><<<c->G25, 32 * kTY25 * kWpl25, c->smem25_1, st>>>(tm, q.st25, nw1, nullptr, nullptr, q.part1, slot0)
     if (R == 8) {
       switch (K) {
@@ -1212,29 +1156,7 @@ void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, bool sketch_o
   //      sketch of step j-K-1 read: earlier on this stream, or on the side stream)
   if (sketch_on_side && j - K - 1 >= 1) CK(cudaStreamWaitEvent(st, q.ev_sk[(j - K - 1) % (K + 2)], 0));
   if (timing) { t2 = ev_get(c, 1); CK(cudaEventRecord(t2.a, st)); }
-  if (q.fused) {
-    const Tma25F tm = tma_args_fused(q, j, nwin);
-    const double* coef = q.Kc + (int64_t)j * (1 + K) * R * R;
-    double* out = q.slot(j + 1);
-#define SYLV_ST3D_F(RR, KK) k_st3d_fused<kTY25, RR, KK><<<c->G25, 32 * kTY25, c->smem25_f, st>>>(tm, q.st25, nwin, coef, out, q.part2, q.part1)
-    if (R == 8) {
-      switch (K) {
-        case 2: SYLV_ST3D_F(8, 2); break;
-        case 3: SYLV_ST3D_F(8, 3); break;
-        case 4: SYLV_ST3D_F(8, 4); break;
-      }
-    } else {
-      switch (K) {
-        case 2: SYLV_ST3D_F(4, 2); break;
-        case 3: SYLV_ST3D_F(4, 3); break;
-        case 4: SYLV_ST3D_F(4, 4); break;
-      }
-    }
-#undef SYLV_ST3D_F
-    count(c);
-  } else {
-    launch_pass2<true>(c, q, win, nwin, j, q.Yt, q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1), st);
-  }
+  launch_pass2<true>(c, q, win, nwin, j, q.Yt, q.Kc + (int64_t)j * (1 + K) * R * R, q.slot(j + 1), st);
   if (timing) { CK(cudaEventRecord(t2.b, st)); c->timed.push_back(t2); }
   int np2 = G;
   const double* p2 = reduce_partials(c, q.part2, G, R * R, red ? red + K * R * R : nullptr, st, chan_main, &np2);

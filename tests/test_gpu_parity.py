@@ -233,31 +233,6 @@ def test_tma_passes_match_generic_passes(name):
             assert _rel(a.get_block(which, j), b.get_block(which, j)) <= 1e-12, (which, j)
 
 
-@pytest.mark.parametrize("name", ["3d-r8k3-tma", "3d-r8k4-tma", "3d-r8k2-tma", "3d-r4k2-tma", "3d-r4k3-tma"])
-def test_fused_pass_matches_unfused(name, monkeypatch):
-    """The opt-in fused pass (stencil25d_fused.cuh: pass 2 of step j with the old-block inner
-    products of step j+1 as (A^T Z_i)^T W', then a one-block pass 1) gives the same recurrence
-    as the separate passes: rho per step and window blocks to rounding over 20 steps, and rho
-    against the oracle (1e-8)."""
-    cfg = inputs.small_config(**CASES[name])
-    C1, C2 = inputs.make_rhs(cfg)
-    st = torch.cuda.current_stream().cuda_stream
-    monkeypatch.setenv("SYLV_FUSED", "1")
-    a = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), stream=st)
-    monkeypatch.setenv("SYLV_FUSED", "0")
-    b = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), stream=st)
-    orc = alg1.SylvesterSketchedKrylov.from_config(cfg, C1=C1, C2=C2)
-    for d in range(1, 21):
-        a.step(1)
-        b.step(1)
-        orc.step(1)
-        ra, rb = a.residual(d)[1], b.residual(d)[1]
-        assert abs(ra - rb) <= 1e-11 * rb + 1e-15, (d, ra, rb)
-        assert _rho_close(ra, orc.residual(d).rho_rel), d
-    for which in (0, 1):
-        for j in range(22 - cfg.k, 22):
-            assert _rel(a.get_block(which, j), b.get_block(which, j)) <= 1e-11, (which, j)
-
 
 @pytest.mark.parametrize("name,ds", [("2d-r1", (20, 40, 55)), ("3d-r8k3", (10, 30, 50)), ("csr-r4k4", (3, 5))])
 def test_device_projected_solve_matches_host(name, ds):
