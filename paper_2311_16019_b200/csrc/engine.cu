@@ -1492,6 +1492,68 @@ sylv_status finish_steps(sylv_ctx* c, int first, int last) {
   return SYLV_OK;
 }
 
+
+// f1 (round 2): an APPROXIMATE rho_rel(d) from the device sign iteration, accepted off the
+// identity (c1: M_V has eigenvalues with Re < 0 near the crossing, so the iteration solves a
+// neighbouring equation; measured 0.25-8 % off).  Used only to choose WHERE the exact checks of
+// the solve driver go; no decision rests on it, nothing is recorded (hist, y_d).  NaN on failure.
+double probe_rho(sylv_ctx* c, int d) {
+  const int r = c->R, m = d * r;
+  if (d < 1 || d > c->d_done || m < 64) return NAN;
+  try {
+    Sequence& U = c->seq[0];
+    Sequence& V = c->seq[1];
+    double hhat[kMaxR * kMaxR], ghat[kMaxR * kMaxR], Bm[kMaxR * kMaxR];
+    sync_T(c, U, m + r);
+    sync_T(c, V, m + r);
+    hat_coefficient(d, r, c->K, U.Th, U.ldT, U.Hh, hhat);
+    hat_coefficient(d, r, c->K, V.Th, V.ldT, V.Hh, ghat);
+    double bn = 0.0;
+    for (int a = 0; a < r; ++a)
+      for (int b = 0; b < r; ++b) {
+        double sacc = 0.0;
+        for (int p = 0; p < r; ++p) sacc += U.beta[a * r + p] * V.beta[b * r + p];
+        Bm[a * r + b] = sacc;
+        bn += sacc * sacc;
+      }
+    bn = std::sqrt(bn);
+    if (!c->gsolve) {
+      c->gsolve = new GpuSylv();
+      c->gsolve->mcap = (c->dmax + 1) * r;
+    }
+    GpuSylv& gs = *c->gsolve;
+    gs.allow_approx = true;
+    const bool ok = gs.solve(U.Tdev, U.Hc, V.Tdev, V.Hc, U.ldT, d, r, c->K, Bm, c->rst);
+    gs.allow_approx = false;
+    if (!ok) return NAN;
+    std::vector<double> lrow((size_t)m * r), lcol((size_t)m * r);
+    CK(cudaMemcpy2DAsync(lrow.data(), (size_t)r * sizeof(double), gs.C + (m - r), (size_t)m * sizeof(double),
+                         (size_t)r * sizeof(double), m, cudaMemcpyDeviceToHost, c->rst));
+    CK(cudaMemcpyAsync(lcol.data(), gs.C + (size_t)(m - r) * m, (size_t)m * r * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->rst));
+    CK(cudaStreamSynchronize(c->rst));
+    if (c->y_dev) c->y_d = -1;              // the device Y buffer was overwritten by the probe
+    double s1 = 0.0, s2 = 0.0;
+    for (int col = 0; col < m; ++col)
+      for (int a = 0; a < r; ++a) {
+        double v = 0.0;
+        for (int p = 0; p < r; ++p) v += hhat[a * r + p] * lrow[(size_t)col * r + p];
+        s1 += v * v;
+      }
+    for (int row = 0; row < m; ++row)
+      for (int a = 0; a < r; ++a) {
+        double v = 0.0;
+        for (int p = 0; p < r; ++p) v += lcol[(size_t)p * m + row] * ghat[a * r + p];
+        s2 += v * v;
+      }
+    c->stats.gpu_approx_checks++;
+    return std::sqrt(s1 + s2) / bn;
+  } catch (const ProjError&) {
+    cudaGetLastError();
+    return NAN;
+  }
+}
+
 }  // namespace
 
 // ====================================================================================
@@ -2159,6 +2221,7 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     const double slope = (std::log(r2) - std::log(r1)) / (d2 - d1);
     return d2 + (std::log(c->tol) - std::log(r2)) / slope;
   };
+  bool probe_walk = false;   // the last check was placed by approximate probes (f1, round 2)
   // schedule phase: approximate device checks may decide clear fails (rho_rel > 3 tol); the
   // search for the first crossing below uses exact solves only
   // (opt-in, SYLV_APPROX_CHECKS=1: an off-identity sign iteration solves a different
@@ -2184,6 +2247,45 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
       const double dh = predict(a.first, a.second, b.first, b.second);
       if (std::isfinite(dh) && (int64_t)sched[idx] * c->R > 800 && dh + 2 < sched[idx]) {
         sched[idx] = std::max(b.first + 1, (int)std::ceil(dh) + 2);
+        // f1 (round 2): when that check will be a host Bartels-Stewart solve (the device sign
+        // iteration failed at or below it: c1), refine where it goes with approximate device
+        // solves around the predicted crossing (they only move the check; SYLV_PROBE=0: off)
+        const char* pe = std::getenv("SYLV_PROBE");
+        if (!(pe && std::strcmp(pe, "0") == 0) && !device_solve(c, sched[idx]) && sched[idx] * c->R >= 512 &&
+            c->d_done >= b.first) {
+          const int target = std::min(c->dmax, sched[idx] + 12);
+          if (c->d_done < target && !c->halted) {
+            const sylv_status s0 = finish_pending();
+            if (!ok_step(s0) && s0 != SYLV_E_LOST_INDEP) return s0;
+            int dd = 0;
+            if (c->d_done < target && !c->halted) sylv_sketch_step(c, target - c->d_done, &dd);
+          }
+          // probes at the predicted crossing and 10 steps on: log-linear through them (and the
+          // last exact check) -> the first d predicted below tol, checked one step above it
+          double xs[3], ys[3];
+          int np = 0;
+          xs[np] = b.first;
+          ys[np++] = std::log(b.second);
+          for (int pd : {std::max(b.first + 1, (int)std::ceil(dh)), std::max(b.first + 2, (int)std::ceil(dh) + 10)}) {
+            const int pdc = std::min(pd, c->d_done);
+            const double pr = probe_rho(c, pdc);
+            if (std::isfinite(pr) && pr > 0.0) {
+              xs[np] = pdc;
+              ys[np++] = std::log(pr);
+            }
+          }
+          if (np == 3) {
+            // least-squares line through the last two (the probes): the local slope near the crossing
+            const double sl = (ys[2] - ys[1]) / (xs[2] - xs[1]);
+            if (sl < 0.0) {
+              const double x = xs[1] + (std::log(c->tol) - ys[1]) / sl;
+              if (std::isfinite(x)) {
+                sched[idx] = std::max(b.first + 1, std::min(c->dmax, (int)std::ceil(x)));
+                probe_walk = true;      // the exact checks walk one step at a time from here
+              }
+            }
+          }
+        }
       } else if (std::isfinite(dh) && dh - 10 > sched[idx] && idx + 1 < sched.size() &&
                  (int64_t)sched[idx + 1] * c->R <= 800) {
         continue;
@@ -2241,6 +2343,10 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     }
     d_fail = dchk;
     if (c->halted && c->d_done <= dchk) break;   // lost independence: no later d to check
+    // a probe-placed check that failed: the crossing is just above it (walk up by 2, not to the
+    // next geometric point)
+    if (probe_walk && idx + 1 < sched.size()) sched[idx + 1] = std::min(sched[idx + 1], std::min(c->dmax, dchk + 2));
+    probe_walk = false;
   }
   c->approx_thr = 0.0;
   {
@@ -2295,9 +2401,13 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
   for (const auto& e : seen)
     if (e.first == lo) rlo = e.second;
   int slow = 0;
+  int walk = probe_walk ? 3 : 0;   // after a probe-placed pass: step down one d at a time (<= 3)
   while (hi - lo > 1 && !pass_by_breakdown) {
     int mid0 = (lo + hi) / 2;
-    if (slow < 2 && std::isfinite(rlo) && std::isfinite(rhi) && rlo > rhi && rhi > 0) {
+    if (walk > 0) {
+      mid0 = hi - 1;
+      --walk;
+    } else if (slow < 2 && std::isfinite(rlo) && std::isfinite(rhi) && rlo > rhi && rhi > 0) {
       const double x = lo + (std::log(rlo) - std::log(c->tol)) / (std::log(rlo) - std::log(rhi)) * (hi - lo);
       mid0 = std::min(hi - 1, std::max(lo + 1, (int)std::ceil(x)));
       if (hi - mid0 <= 2) mid0 = hi - 1;   // crossing predicted just below hi: settle it at once
@@ -2329,8 +2439,10 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
     } else {
       lo = mid;
       rlo = rr;
+      walk = 0;
     }
-    slow = (2 * (hi - lo) > width) ? slow + 1 : 0;
+    slow = (walk > 0 || 2 * (hi - lo) > width) ? 0 : slow;
+    if (walk == 0 && 2 * (hi - lo) > width) ++slow;
   }
   if (c->y_d != hi) {
     if (best_d == hi && !best_on_dev) {   // restore the kept solution of d* (no re-solve)
