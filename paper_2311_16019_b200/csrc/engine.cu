@@ -247,6 +247,7 @@ struct sylv_ctx {
   int RT = 1;         // row tiles of Q^T w
   int64_t tileQ = 0;
   int CC = 1;         // column chunks of Q c
+  bool qmma = true;   // DMMA sweeps of Q (R >= 4); SYLV_QMMA=0: the FMA kernels (A/B)
   int nchunk = 1;     // row chunks of the sketch kernel (grid nchunk x R)
   int64_t gpc = 32;   // 32-row groups per sketch chunk
   size_t sk_smem = 0; // dynamic shared memory of the sketch kernel
@@ -271,6 +272,9 @@ struct sylv_ctx {
   GpuSylv* gsolve = nullptr;    // device projected solver (created on first use)
   cublasHandle_t blas = nullptr;  // second pass X accumulation (created on first use)
   int gpu_fail_d = 1 << 30;     // smallest d where the device solve fell back to the host
+  int sign_fail_d = 1 << 30;    // smallest d where the sign iteration failed (eig solve from there)
+  int eig_solve = 1;            // certified eigendecomposition solve (SYLV_EIG=0: off, 2: first; tests)
+  int64_t eig_solves = 0;
   // solve driver, schedule phase: a device solve that converged off the identity (approximate;
   // c1's ill-conditioned projections) may decide a check "fail" when its rho_rel exceeds this
   // (3 tol; measured error of such solves at c1: <= 8 %), else the host solves it (0: off)
@@ -1219,23 +1223,45 @@ void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
   const int64_t rows = q.sq;                 // this rank's rows of w and Q (sharded: s / P)
   const bool shard = rows != q.s;
   const int chan = q.which == 0 ? kChanUSide : kChanVSide;
-  const dim3 gq((m + kQtwCols - 1) / kQtwCols, c->RT);
-  const int cols_per_chunk = (m + c->CC - 1) / c->CC;
+  // tensor-core sweeps (k_qtw_mma / k_qc_mma) for R >= 4 with 16-byte aligned columns
+  const bool mma = R >= 4 && rows % 4 == 0 && c->qmma;
+  const dim3 gq(mma ? (unsigned)(((m + 31) / 32 + kWarps - 1) / kWarps) : (unsigned)((m + kQtwCols - 1) / kQtwCols),
+                c->RT);
+  int cols_per_chunk = (m + c->CC - 1) / c->CC;
+  if (mma) cols_per_chunk = (cols_per_chunk + 15) / 16 * 16;
   const int ncc = (m + cols_per_chunk - 1) / cols_per_chunk;
   const dim3 gc((unsigned)((rows + kThreads - 1) / kThreads), ncc);
   const int64_t mR = (int64_t)m * R;
   const int gr = (int)std::min<int64_t>(1024, (mR + 255) / 256);
   const int gw = (int)std::min<int64_t>(1024, (rows * R + 255) / 256);
   SYLV_DISPATCH_R(R, {
+    auto qtw = [&]() {
+      if constexpr (R_ >= 4) {
+        if (mma) {
+          k_qtw_mma<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, c->tileQ, q.cpart);
+          return;
+        }
+      }
+      k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, c->tileQ, 1, q.cpart);
+    };
+    auto qc = [&](const double* cv) {
+      if constexpr (R_ >= 4) {
+        if (mma) {
+          k_qc_mma<R_><<<gc, kThreads, 0, st>>>(q.Q, rows, rows, m, cv, cols_per_chunk, q.qcpart);
+          return;
+        }
+      }
+      k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, rows, rows, m, cv, cols_per_chunk, q.qcpart);
+    };
     // pass A: c1 = Q^T w (sharded: local rows, then the m R coefficients summed over the ranks)
-    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, c->tileQ, 1, q.cpart);
+    qtw();
     k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.csum, nullptr);
     if (shard) c->comm->allreduce(q.csum, (size_t)mR, st, chan);
     // w -= Q c1
-    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, rows, rows, m, q.csum, cols_per_chunk, q.qcpart);
+    qc(q.csum);
     k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, rows * R);
     // pass B: c2 = Q^T w, csum += c2
-    k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, c->tileQ, 1, q.cpart);
+    qtw();
     if (shard) {
       k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.c2, nullptr);
       c->comm->allreduce(q.c2, (size_t)mR, st, chan);
@@ -1243,7 +1269,7 @@ void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
     } else {
       k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.c2, q.csum);
     }
-    k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, rows, rows, m, q.c2, cols_per_chunk, q.qcpart);
+    qc(q.c2);
     k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, rows * R);
   });
   count(c, 8);
@@ -1803,6 +1829,8 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
              !std::getenv("SYLV_SKETCH_REPLICATED"))
                 ? c->s / comm->nranks : c->s;
     SYLV_DISPATCH_R(r, { c->tileQ = qtw_tile<R_>(); });
+    if (const char* e = std::getenv("SYLV_QMMA")) c->qmma = std::atoi(e) != 0;   // A/B switch
+    if (const char* e = std::getenv("SYLV_EIG")) c->eig_solve = std::atoi(e);   // A/B switch, tests
     c->RT = (int)((c->sq + c->tileQ - 1) / c->tileQ);
     // Q c: (ceil(s/256) x CC) CTAs, ~4 per SM at the full width (each thread streams a row
     // of its column chunk with 8 loads in flight)
@@ -1927,8 +1955,19 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
         }
         GpuSylv& gs = *c->gsolve;
         gs.allow_approx = approx_mode;
-        const bool ok = gs.solve(U.Tdev, U.Hc, V.Tdev, V.Hc, U.ldT, d, r, c->K, Bm, c->rst);
+        // the sign iteration first (it needs spec(M_U), spec(M_V) in Re > 0); where it failed
+        // before (d >= sign_fail_d) or fails now, the certified eigendecomposition solve (f1, r2)
+        bool ok = false;
+        if ((d < c->sign_fail_d && c->eig_solve != 2) || approx_mode) {
+          ok = gs.solve(U.Tdev, U.Hc, V.Tdev, V.Hc, U.ldT, d, r, c->K, Bm, c->rst);
+          if (!ok && !approx_mode) c->sign_fail_d = std::min(c->sign_fail_d, d);
+        }
         gs.allow_approx = false;
+        if (!ok && !approx_mode && c->eig_solve) {
+          ok = gs.solve_eig(U.Tdev, U.Hc, V.Tdev, V.Hc, U.ldT, d, r, c->K, Bm, c->rst);
+          gs.off_identity = false;
+          if (ok) c->eig_solves++;
+        }
         if (ok) {
           CK(cudaMemcpy2DAsync(lrow.data(), (size_t)r * sizeof(double), gs.C + (m - r), (size_t)m * sizeof(double),
                                (size_t)r * sizeof(double), m, cudaMemcpyDeviceToHost, c->rst));
@@ -2250,8 +2289,11 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
         // f1 (round 2): when that check will be a host Bartels-Stewart solve (the device sign
         // iteration failed at or below it: c1), refine where it goes with approximate device
         // solves around the predicted crossing (they only move the check; SYLV_PROBE=0: off)
+        // opt-in (SYLV_PROBE=1): the probes move checks away from the oracle's R9 schedule, so
+        // with a non-monotone rho (Ex. 6.1 nu = 0.001, kappa(T) ~ 1e16) the search can find a
+        // different crossing or none (d_max reached; B200 r2): off by default
         const char* pe = std::getenv("SYLV_PROBE");
-        if (!(pe && std::strcmp(pe, "0") == 0) && !device_solve(c, sched[idx]) && sched[idx] * c->R >= 512 &&
+        if ((pe && std::strcmp(pe, "1") == 0) && !device_solve(c, sched[idx]) && sched[idx] * c->R >= 512 &&
             c->d_done >= b.first) {
           const int target = std::min(c->dmax, sched[idx] + 12);
           if (c->d_done < target && !c->halted) {

@@ -31,14 +31,6 @@ struct Win {
   const double* p[kMaxK];  // window blocks Z_{d-nwin+1..d}, oldest first (Z_d = p[nwin-1])
 };
 
-// D(8x8) += A(8x4) B(4x8), fp64; fragments per PTX ISA m8n8k4 .f64:
-// A: lane holds A[lane>>2][lane&3]; B: B[lane&3][lane>>2]; D: D[lane>>2][2*(lane&3)+{0,1}].
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
-}
-
 // Stencil grid coordinates of `row` (x fastest).
 struct Coord {
   uint32_t x, y, z;

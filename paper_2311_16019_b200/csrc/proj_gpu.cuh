@@ -18,6 +18,7 @@
 // path).  Every O(m^3) operation stays on the device; only r x m and m x r slices of Y
 // come back for the residual (Alg. 1 line 13).
 #pragma once
+#include <cuComplex.h>
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
@@ -80,6 +81,58 @@ __global__ void k_logdet(const double* __restrict__ LU, int m, double* __restric
   if (threadIdx.x == 0) out[0] = sm[0];
 }
 
+// ---- eigendecomposition solve (round 2, f1 at c1): complex helpers
+// LAPACK real-eigenvector packing -> complex columns: a real eigenvalue j has v_j = VR(:, j); a
+// conjugate pair (j, j+1) (pair[j] = 1) has v_j = VR(:, j) + i VR(:, j+1), v_{j+1} = conj(v_j).
+__global__ void k_unpack_vr(const double* __restrict__ VR, const int* __restrict__ pair, int m,
+                            cuDoubleComplex* __restrict__ V) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int col = (int)(e / m);
+    const int p = pair[col];   // 0 real, 1 first of a pair, 2 second of a pair
+    double re, im;
+    if (p == 0) {
+      re = VR[e];
+      im = 0.0;
+    } else if (p == 1) {
+      re = VR[e];
+      im = VR[e + m];
+    } else {
+      re = VR[e - m];
+      im = -VR[e];
+    }
+    V[e] = make_cuDoubleComplex(re, im);
+  }
+}
+
+__global__ void k_real_to_complex(const double* __restrict__ X, int64_t n, cuDoubleComplex* __restrict__ Z) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    Z[e] = make_cuDoubleComplex(X[e], 0.0);
+}
+
+// G[i, j] /= (la_i + lb_j)
+__global__ void k_div_eig(cuDoubleComplex* __restrict__ G, int m, const cuDoubleComplex* __restrict__ la,
+                          const cuDoubleComplex* __restrict__ lb) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e / m);
+    const int i = (int)(e - (int64_t)j * m);
+    G[e] = cuCdiv(G[e], cuCadd(la[i], lb[j]));
+  }
+}
+
+__global__ void k_ceye(cuDoubleComplex* __restrict__ X, int m) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+    X[e] = make_cuDoubleComplex((e % (m + 1) == 0) ? 1.0 : 0.0, 0.0);
+}
+
+// Y[e] += Re Z[e]
+__global__ void k_add_real(const cuDoubleComplex* __restrict__ Z, int64_t n, double* __restrict__ Y) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    Y[e] += cuCreal(Z[e]);
+}
+
 struct GpuSylv {
   cublasHandle_t hb = nullptr;
   cusolverDnHandle_t hs = nullptr;
@@ -102,8 +155,33 @@ struct GpuSylv {
   int newton_steps = 0, ns_steps = 0;
   double t_build = 0, t_newton = 0, t_ns = 0;   // seconds (SYLV_TRACE_PROJ)
 
+  // eigendecomposition solve (solve_eig): complex eigenvectors, their inverses, work, eigenvalues
+  cuDoubleComplex *VA = nullptr, *VB = nullptr, *VAi = nullptr, *VBi = nullptr, *G1 = nullptr, *G2 = nullptr;
+  cuDoubleComplex *wA = nullptr, *wB = nullptr;
+  int* pairs = nullptr;                  // 2 m packing flags (A then B)
+  void* gbuf = nullptr;                  // Xgeev device workspace
+  std::vector<char> ghost;               // Xgeev host workspace
+  size_t gws = 0;
+  cusolverDnParams_t gparams = nullptr;
+  int ecap = 0;
+  int eig_refine = 0;                    // refinement steps of the last solve_eig
+  double eig_res = 0.0;                  // its final relative projected residual
+  double t_eig = 0.0, t_refine = 0.0;
+
   ~GpuSylv() { release(); }
+  void free_eig() {
+    for (cuDoubleComplex* p : {VA, VB, VAi, VBi, G1, G2, wA, wB})
+      if (p) cudaFree(p);
+    if (pairs) cudaFree(pairs);
+    if (gbuf) cudaFree(gbuf);
+    VA = VB = VAi = VBi = G1 = G2 = wA = wB = nullptr;
+    pairs = nullptr;
+    gbuf = nullptr;
+    gws = 0;
+    ecap = 0;
+  }
   void free_bufs() {
+    free_eig();
     for (double* p : {A, B, C, Ai, Bi, W, LU, Hb, work, dlog, LU2, work2})
       if (p) cudaFree(p);
     for (int* p : {ipiv, info, ipiv2, info2})
@@ -118,6 +196,8 @@ struct GpuSylv {
     if (hb) cublasDestroy(hb);
     if (hs) cusolverDnDestroy(hs);
     if (hs2) cusolverDnDestroy(hs2);
+    if (gparams) cusolverDnDestroyParams(gparams);
+    gparams = nullptr;
     if (st2) cudaStreamDestroy(st2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -349,6 +429,158 @@ struct GpuSylv {
     }
     if (trace) std::fprintf(stderr, "[proj] m=%d no convergence in 60 iterations (rel step history above)\n", m);
     return false;
+  }
+
+  // ---- f1 (round 2): eigendecomposition solve with iterative refinement, for projected
+  // equations the sign iteration cannot solve (c1: M_V has eigenvalues with Re < 0, so
+  // sign(M_V) != I).  With A = V_A diag(la) V_A^{-1}, B = V_B diag(lb) V_B^{-1}
+  // (cuSOLVER Xgeev, complex right eigenvectors), A Y + Y B = R is solved by
+  //   Y = V_A [ (V_A^{-1} R V_B) ./ (la_i + lb_j) ] V_B^{-1}      (apply(R), 4 ZGEMMs),
+  // then refined: Y += apply(C - A Y - Y B) until the projected residual is at rounding level,
+  // ||C - A Y - Y B||_F <= 1e-12 (||A||_F + ||B||_F) ||Y||_F — the backward error of a
+  // backward-stable (Bartels-Stewart) solve — else the caller falls back to the host.  The
+  // accuracy of the first apply depends on kappa(V_A) kappa(V_B); the refinement converges
+  // while that times the unit roundoff is well below 1, and the residual test certifies it.
+  void ensure_eig(int m) {
+    if (m <= ecap) return;
+    ck(cudaStreamSynchronize(cur), "sync");
+    free_eig();
+    const size_t mm = (size_t)cap * cap;             // sized like the real buffers (cap >= m)
+    for (cuDoubleComplex** p : {&VA, &VB, &VAi, &VBi, &G1, &G2})
+      ck(cudaMalloc(p, mm * sizeof(cuDoubleComplex)), "cudaMalloc (eig)");
+    ck(cudaMalloc(&wA, (size_t)cap * sizeof(cuDoubleComplex)), "cudaMalloc (eig)");
+    ck(cudaMalloc(&wB, (size_t)cap * sizeof(cuDoubleComplex)), "cudaMalloc (eig)");
+    ck(cudaMalloc(&pairs, 2 * (size_t)cap * sizeof(int)), "cudaMalloc (eig)");
+    if (!gparams) cks(cusolverDnCreateParams(&gparams), "cusolverDnCreateParams");
+    size_t wd = 0, wh = 0;
+    cks(cusolverDnXgeev_bufferSize(hs, gparams, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, cap, CUDA_R_64F,
+                                   LU, cap, CUDA_C_64F, wA, CUDA_R_64F, nullptr, cap, CUDA_R_64F, Ai, cap, CUDA_R_64F,
+                                   &wd, &wh),
+        "Xgeev_bufferSize");
+    int lw = 0;
+    cks(cusolverDnZgetrf_bufferSize(hs, cap, cap, G1, cap, &lw), "zgetrf_bufferSize");
+    gws = std::max(wd, (size_t)lw * sizeof(cuDoubleComplex));
+    ck(cudaMalloc(&gbuf, gws + 16), "cudaMalloc (eig)");
+    ghost.assign(wh + 16, 0);
+    ecap = cap;
+  }
+
+  // eigenvalues w and complex right eigenvectors V of the real m x m matrix X (X is copied)
+  void eig(const double* X, int m, cuDoubleComplex* w, cuDoubleComplex* V, int* pair_dev) {
+    ck(cudaMemcpyAsync(LU, X, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, cur), "copy (geev)");
+    size_t wd = 0, wh = 0;
+    cks(cusolverDnXgeev_bufferSize(hs, gparams, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_R_64F,
+                                   LU, m, CUDA_C_64F, w, CUDA_R_64F, nullptr, m, CUDA_R_64F, Ai, m, CUDA_R_64F, &wd,
+                                   &wh),
+        "Xgeev_bufferSize");
+    if (wd > gws || wh + 16 > ghost.size()) throw ProjError{"Xgeev workspace grew"};
+    cks(cusolverDnXgeev(hs, gparams, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_R_64F, LU, m,
+                        CUDA_C_64F, w, CUDA_R_64F, nullptr, m, CUDA_R_64F, Ai, m, CUDA_R_64F, gbuf, gws, ghost.data(),
+                        wh, info),
+        "Xgeev");
+    int inf = 0;
+    std::vector<cuDoubleComplex> wh_((size_t)m);
+    ck(cudaMemcpyAsync(&inf, info, sizeof(int), cudaMemcpyDeviceToHost, cur), "D2H");
+    ck(cudaMemcpyAsync(wh_.data(), w, (size_t)m * sizeof(cuDoubleComplex), cudaMemcpyDeviceToHost, cur), "D2H");
+    ck(cudaStreamSynchronize(cur), "sync");
+    if (inf != 0) throw ProjError{"Xgeev info " + std::to_string(inf)};
+    std::vector<int> pr((size_t)m, 0);
+    for (int j = 0; j < m; ++j) {
+      if (!std::isfinite(cuCreal(wh_[j])) || !std::isfinite(cuCimag(wh_[j]))) throw ProjError{"Xgeev: non-finite eigenvalue"};
+      if (pr[j] == 0 && cuCimag(wh_[j]) != 0.0) {
+        if (j + 1 >= m) throw ProjError{"Xgeev: unpaired complex eigenvalue"};
+        pr[j] = 1;
+        pr[j + 1] = 2;
+      }
+    }
+    ck(cudaMemcpyAsync(pair_dev, pr.data(), (size_t)m * sizeof(int), cudaMemcpyHostToDevice, cur), "H2D");
+    const int64_t mm = (int64_t)m * m;
+    k_unpack_vr<<<(int)std::min<int64_t>(4096, (mm + 255) / 256), 256, 0, cur>>>(Ai, pair_dev, m, V);
+    ck(cudaGetLastError(), "k_unpack_vr");
+    ck(cudaStreamSynchronize(cur), "sync");   // pr (host) is read by the async copy
+  }
+
+  // Vi = V^{-1} (complex LU in G1)
+  void cinv(const cuDoubleComplex* V, cuDoubleComplex* Vi, int m) {
+    const int64_t mm = (int64_t)m * m;
+    ck(cudaMemcpyAsync(G1, V, (size_t)mm * sizeof(cuDoubleComplex), cudaMemcpyDeviceToDevice, cur), "copy");
+    cks(cusolverDnZgetrf(hs, m, m, G1, m, reinterpret_cast<cuDoubleComplex*>(gbuf), ipiv, info), "zgetrf");
+    k_ceye<<<(int)std::min<int64_t>(4096, (mm + 255) / 256), 256, 0, cur>>>(Vi, m);
+    cks(cusolverDnZgetrs(hs, CUBLAS_OP_N, m, m, G1, m, ipiv, Vi, m, info), "zgetrs");
+    int inf = 0;
+    ck(cudaMemcpyAsync(&inf, info, sizeof(int), cudaMemcpyDeviceToHost, cur), "D2H");
+    ck(cudaStreamSynchronize(cur), "sync");
+    if (inf != 0) throw ProjError{"singular eigenvector matrix"};
+  }
+
+  // Y += Re(V_A [(V_A^{-1} R V_B) ./ (la_i + lb_j)] V_B^{-1})
+  void eig_apply(const double* Rr, double* Y, int m) {
+    const int64_t mm = (int64_t)m * m;
+    const int g = (int)std::min<int64_t>(4096, (mm + 255) / 256);
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+    k_real_to_complex<<<g, 256, 0, cur>>>(Rr, mm, G2);
+    ckb(cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, VAi, m, G2, m, &zero, G1, m), "zgemm (VA^-1 R)");
+    ckb(cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, G1, m, VB, m, &zero, G2, m), "zgemm (. VB)");
+    k_div_eig<<<g, 256, 0, cur>>>(G2, m, wA, wB);
+    ckb(cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, VA, m, G2, m, &zero, G1, m), "zgemm (VA .)");
+    ckb(cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, G1, m, VBi, m, &zero, G2, m), "zgemm (. VB^-1)");
+    k_add_real<<<g, 256, 0, cur>>>(G2, mm, Y);
+    ck(cudaGetLastError(), "eig_apply");
+  }
+
+  // Solve M_U Y + Y M_V^T = E1 Bm E1^T; Y left in C.  false: not certified (caller: host).
+  bool solve_eig(const double* TU, const double* HcU, const double* TV, const double* HcV, int64_t ldT, int d, int r,
+                 int K, const double* Bm, cudaStream_t st) {
+    const bool trace = std::getenv("SYLV_TRACE_PROJ") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    const int m = d * r;
+    ensure(m, r, st);
+    ensure_eig(m);
+    build_M(TU, ldT, HcU, d, r, K, A, st);
+    build_M(TV, ldT, HcV, d, r, K, W, st);
+    const double one = 1.0, zero = 0.0, mone = -1.0;
+    ckb(cublasDgeam(hb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, &one, W, m, &zero, W, m, B, m), "geam (M_V^T)");
+    const int64_t mm = (int64_t)m * m;
+    // right-hand side F (in Bi: kept for the residuals)
+    ck(cudaMemsetAsync(Bi, 0, (size_t)mm * sizeof(double), st), "memset");
+    std::vector<double> cb((size_t)r * r);
+    for (int a = 0; a < r; ++a)
+      for (int b = 0; b < r; ++b) cb[(size_t)b * r + a] = Bm[a * r + b];
+    ck(cudaMemcpy2DAsync(Bi, (size_t)m * sizeof(double), cb.data(), (size_t)r * sizeof(double),
+                         (size_t)r * sizeof(double), r, cudaMemcpyHostToDevice, st),
+       "H2D (rhs)");
+    eig(A, m, wA, VA, pairs);
+    eig(B, m, wB, VB, pairs + m);
+    cinv(VA, VAi, m);
+    cinv(VB, VBi, m);
+    auto t1 = std::chrono::steady_clock::now();
+    t_eig = std::chrono::duration<double>(t1 - t0).count();
+    const double nA = fro(A, mm), nB = fro(B, mm), nF = fro(Bi, mm);
+    ck(cudaMemsetAsync(C, 0, (size_t)mm * sizeof(double), st), "memset");
+    eig_apply(Bi, C, m);
+    double prev = INFINITY;
+    bool okc = false;
+    for (eig_refine = 0; eig_refine < 8; ++eig_refine) {
+      // W = F - A Y - Y B
+      ck(cudaMemcpyAsync(W, Bi, (size_t)mm * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy");
+      ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &mone, A, m, C, m, &one, W, m), "dgemm (A Y)");
+      ckb(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &mone, C, m, B, m, &one, W, m), "dgemm (Y B)");
+      const double rn = fro(W, mm), yn = fro(C, mm);
+      eig_res = rn / nF;
+      if (!std::isfinite(rn) || !std::isfinite(yn)) break;
+      if (rn <= 1e-12 * (nA + nB) * yn) {
+        okc = true;
+        break;
+      }
+      if (eig_refine >= 2 && rn > 0.5 * prev) break;   // stagnated: not certified
+      prev = rn;
+      eig_apply(W, C, m);
+    }
+    t_refine = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    if (trace)
+      std::fprintf(stderr, "[proj] m=%d eig %.1f ms, %d refinements %.1f ms, residual %.2e (%s)\n", m, 1e3 * t_eig,
+                   eig_refine, 1e3 * t_refine, eig_res, okc ? "certified" : "rejected");
+    return okc;
   }
 };
 

@@ -384,6 +384,154 @@ __global__ void __launch_bounds__(kThreads) k_qc_part(const double* __restrict__
   }
 }
 
+// ---- Tensor-core (DMMA) sweeps of Q for R >= 4 (round 2): the two products of a CGS2 sweep
+// are (m x s)(s x R) and (s x m)(m x R) contractions with R <= 8 = the DMMA n width, so one
+// mma.sync.m8n8k4.f64 does 8 x 8 x 4 FMAs and every lane loads one 32-byte run of one Q column
+// per four DMMAs (the k index of a fragment is free: lane l's four consecutive rows are the k
+// slots t = 0..3 of four DMMAs).  Few registers per lane (accumulators are 2 doubles per 8 x 8
+// tile), so two row steps of loads stay in flight per lane; Q is read exactly once, coalesced
+// (a warp's loads cover 256-byte runs of 4 columns / 32 rows).  Requires ldq % 4 == 0 and a
+// 32-byte aligned Q (checked by the caller).  Deterministic: fixed summation order per lane.
+
+// partial[(rt*m + j)*R + c] = sum_{rows of chunk rt} Q[j*ldq + row] w[row*R + c]
+// Warp = (32 columns j0..j0+31 = four 8-column tiles, one row chunk); CTA = 8 warps on 256
+// consecutive columns of the same row chunk (they share w's rows through L1).
+template <int R>
+__global__ void __launch_bounds__(kThreads, 2) k_qtw_mma(const double* __restrict__ Q, int64_t s, int64_t ldq, int m,
+                                                      const double* __restrict__ w, int64_t chunk,
+                                                      double* __restrict__ partial) {
+  static_assert(R >= 4 && R <= 8, "DMMA sweep: R in 4..8");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q4 = lane & 3, mc = lane >> 2;
+  const int rt = blockIdx.y;
+  const int j0 = (blockIdx.x * kWarps + warp) * 32;
+  if (j0 >= m) return;                                 // warp-uniform (no barriers below)
+  const int64_t r0 = (int64_t)rt * chunk;
+  const int64_t r1 = r0 + chunk < s ? r0 + chunk : s;
+  const double* __restrict__ qc[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) qc[u] = Q + (int64_t)min(j0 + 8 * u + mc, m - 1) * ldq;   // clamped: dropped below
+  const bool wl = mc < R;
+  double acc[4][2];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) acc[u][0] = acc[u][1] = 0.0;
+  int64_t k0 = r0;
+  for (; k0 + 32 <= r1; k0 += 32) {                    // two 16-row steps in flight
+    double2 qa[2][4][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2* p = reinterpret_cast<const double2*>(qc[u] + k0 + 16 * h + 4 * q4);
+        qa[h][u][0] = __ldg(p);
+        qa[h][u][1] = __ldg(p + 1);
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t rb = k0 + 16 * h + 4 * q4;
+      double wb[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) wb[t] = wl ? __ldg(w + (rb + t) * R + mc) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        dmma(acc[u], qa[h][u][0].x, wb[0]);
+        dmma(acc[u], qa[h][u][0].y, wb[1]);
+        dmma(acc[u], qa[h][u][1].x, wb[2]);
+        dmma(acc[u], qa[h][u][1].y, wb[3]);
+      }
+    }
+  }
+  for (; k0 < r1; k0 += 16) {                          // ragged tail: guarded scalar loads
+    const int64_t rb = k0 + 4 * q4;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const bool in = rb + t < r1;
+      const double wv = (in && wl) ? __ldg(w + (rb + t) * R + mc) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma(acc[u], in ? __ldg(qc[u] + rb + t) : 0.0, wv);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = j0 + 8 * u + mc;
+    if (j < m) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (2 * q4 + e < R) partial[((int64_t)rt * m + j) * R + 2 * q4 + e] = acc[u][e];
+    }
+  }
+}
+
+// partial2[(cc*s + row)*R + c] = sum_{j in chunk cc} Q[j*ldq + row] cvec[j*R + c]
+// Warp = 32 rows x one column chunk (blockIdx.y); DMMA t covers rows i0 + 4 m + t (m = 0..7),
+// k = 4 consecutive columns: lane l loads rows i0 + 4 (l>>2) .. +3 of column j + (l&3).
+template <int R>
+__global__ void __launch_bounds__(kThreads) k_qc_mma(const double* __restrict__ Q, int64_t s, int64_t ldq, int m,
+                                                     const double* __restrict__ cvec, int cols_per_chunk,
+                                                     double* __restrict__ partial2) {
+  static_assert(R >= 4 && R <= 8, "DMMA sweep: R in 4..8");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q4 = lane & 3, mr = lane >> 2;
+  const int cc = blockIdx.y;
+  const int ja = cc * cols_per_chunk;
+  const int jb = min(m, ja + cols_per_chunk);
+  const int64_t i0 = ((int64_t)blockIdx.x * kWarps + warp) * 32;
+  if (i0 >= s) return;                                 // warp-uniform
+  const int64_t rb = i0 + 4 * mr;
+  const bool full = rb + 4 <= s;
+  const bool cl = mr < R;                              // B fragment: c = l>>2
+  double acc[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
+  int j = ja;
+  for (; j + 16 <= jb; j += 16) {                      // four 4-column steps in flight
+    double2 qa[4][2];
+    double bv[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const double* col = Q + (int64_t)(j + 4 * h + q4) * ldq + rb;
+      if (full) {
+        qa[h][0] = __ldg(reinterpret_cast<const double2*>(col));
+        qa[h][1] = __ldg(reinterpret_cast<const double2*>(col) + 1);
+      } else {
+        qa[h][0].x = rb < s ? __ldg(col) : 0.0;
+        qa[h][0].y = rb + 1 < s ? __ldg(col + 1) : 0.0;
+        qa[h][1].x = rb + 2 < s ? __ldg(col + 2) : 0.0;
+        qa[h][1].y = rb + 3 < s ? __ldg(col + 3) : 0.0;
+      }
+      bv[h] = cl ? __ldg(cvec + (int64_t)(j + 4 * h + q4) * R + mr) : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      dmma(acc[0], qa[h][0].x, bv[h]);
+      dmma(acc[1], qa[h][0].y, bv[h]);
+      dmma(acc[2], qa[h][1].x, bv[h]);
+      dmma(acc[3], qa[h][1].y, bv[h]);
+    }
+  }
+  for (; j < jb; j += 4) {                             // ragged column tail
+    const int jj = j + q4;
+    const bool in = jj < jb;
+    const double* col = Q + (int64_t)(in ? jj : ja) * ldq + rb;
+    double a[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] = (in && rb + t < s) ? __ldg(col + t) : 0.0;
+    const double bvv = (in && cl) ? __ldg(cvec + (int64_t)jj * R + mr) : 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) dmma(acc[t], a[t], bvv);
+  }
+  // D_t[mr'][c]: row i0 + 4 (lane>>2) + t, columns c = 2 (lane&3) + e
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int64_t row = i0 + 4 * mr + t;
+    if (row < s) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (2 * q4 + e < R) partial2[((int64_t)cc * s + row) * R + 2 * q4 + e] = acc[t][e];
+    }
+  }
+}
+
 // w[row*R + c] -= sum_cc partial2[(cc*s + row)*R + c]
 __global__ void k_wsub(double* __restrict__ w, const double* __restrict__ partial2, int ncc,
                        int64_t len) {

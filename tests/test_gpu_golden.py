@@ -114,6 +114,8 @@ def test_time_to_tolerance_matches_oracle_golden(name):
     else:
         # R27: the oracle's own true residual exceeds its sketched residual by > 10x (the sketched
         # bases have lost the embedding, kappa(T) ~ 1e13 - 1e16: SURVEY A22); the true residual is
-        # then set by rounding amplified by kappa(T) and only its order of magnitude is reproducible
-        assert 0.1 * gold["true_rel"] <= rel <= 10.0 * gold["true_rel"], msg
+        # then set by rounding amplified by kappa(T): the GPU's may not be worse than the oracle's
+        # by more than an order of magnitude, and (exact arithmetic puts the true residual within
+        # the embedding distortion of rho) not below a tenth of the sketched residual
+        assert 0.1 * gold["rho_rel_star"] <= rel <= 10.0 * gold["true_rel"], msg
     g.close()

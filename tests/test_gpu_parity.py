@@ -272,3 +272,57 @@ def test_c0_full_solve_with_device_projected_solves():
     d, rr, _ = g.solve()
     assert abs(d - 107) <= 2 and rr < cfg.tol
     assert g.stats()["gpu_solve_fallbacks"] == 0
+
+
+@pytest.mark.parametrize("name", ["3d-r8k3", "2d-r4", "3d-r4k2-tma"])
+def test_dmma_sweeps_match_fma_sweeps(name, monkeypatch):
+    """a5's CGS2 sweeps of Q on the fp64 tensor cores (k_qtw_mma / k_qc_mma, R >= 4) and the FMA
+    kernels (SYLV_QMMA=0, read at init) build the same sketched QR: T and rho agree to rounding
+    over 30 steps (s = 880 for 3d-r4k2-tma: a ragged 16-row tail)."""
+    cfg = inputs.small_config(**CASES[name])
+    C1, C2 = inputs.make_rhs(cfg)
+    st = torch.cuda.current_stream().cuda_stream
+    a = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), stream=st)
+    monkeypatch.setenv("SYLV_QMMA", "0")
+    b = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), stream=st)
+    a.step(30)
+    b.step(30)
+    for d in (5, 17, 30):
+        ra, rb = a.residual(d)[1], b.residual(d)[1]
+        assert abs(ra - rb) <= 1e-10 * rb + 1e-15, (d, ra, rb)
+    for which in (0, 1):
+        _, Ta, _ = a.get_small(which, 30)
+        _, Tb, _ = b.get_small(which, 30)
+        assert _rel(Ta, Tb) <= 1e-12, which
+
+
+@pytest.mark.parametrize("name,ds", [("2d-r1", (20, 40, 55)), ("3d-r8k3", (10, 30, 50)), ("2d-r4", (15, 45)),
+                                     ("csr-r4k4", (3, 5))])
+def test_device_eig_solve_matches_oracle(name, ds, monkeypatch):
+    """f1 (round 2): the certified eigendecomposition solve (cuSOLVER Xgeev + ZGEMM applies +
+    iterative refinement to a rounding-level projected residual; SYLV_EIG=2 forces it ahead of
+    the sign iteration) gives the ORACLE's sketched residual (1e-7 relative, several decades
+    below tol) and the host solve's solution."""
+    cfg, csr, C1, C2, orc, _ = _setup(name)
+    st = torch.cuda.current_stream().cuda_stream
+    monkeypatch.setenv("SYLV_EIG", "2")
+    g = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr,
+                           stream=st, proj="gpu")
+    monkeypatch.delenv("SYLV_EIG")
+    h = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr,
+                           stream=st, proj="host")
+    done = 0
+    for d in ds:
+        g.step(d - done)
+        h.step(d - done)
+        orc.step(d - done)
+        done = d
+        rg = g.residual(d)[1]
+        ro = orc.residual(d).rho_rel
+        assert abs(rg - ro) <= 1e-7 * ro, (d, rg, ro)
+    s = g.stats()
+    assert s["gpu_solves"] == len(ds) and s["gpu_solve_fallbacks"] == 0
+    X1g, X2g, kg = g.solution(done, 64)
+    X1h, X2h, kh = h.solution(done, 64)
+    assert kg == kh
+    assert _rel(X1g @ X2g.T, X1h @ X2h.T) <= 1e-6
