@@ -215,6 +215,34 @@ def run_reference(args, cfg):
     return 0
 
 
+def _warm_solvers(cfg, stream):
+    """Untimed: one small solve through each device projected solver (sign iteration and the
+    certified eigendecomposition, SYLV_EIG=2) and the host one, so the time to tolerance does not
+    include first-touch costs of the solver libraries (cuSOLVER's Xgeev: ~25 s on a fresh box)."""
+    import torch
+    import paper_2311_16019_b200 as pkg
+    from synth import inputs
+    small = inputs.small_config(kind="stencil2d", N=23, r=cfg.r, k=2, d_max=70)
+    C1, C2 = inputs.make_rhs(small)
+    for eig, proj in (("2", "gpu"), ("1", "gpu"), ("1", "host")):
+        old = os.environ.get("SYLV_EIG")
+        os.environ["SYLV_EIG"] = eig
+        try:
+            w = pkg.from_config(small, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(),
+                                stream=stream.cuda_stream, proj=proj)
+        finally:
+            if old is None:
+                os.environ.pop("SYLV_EIG")
+            else:
+                os.environ["SYLV_EIG"] = old
+        w.step(64)
+        w.residual(64)
+        X = torch.zeros((small.n, 64), dtype=torch.float64, device="cuda")
+        w.solution(64, 64, X, X.clone())
+        w.close()
+    torch.cuda.synchronize()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -332,6 +360,7 @@ def main():
     ttt = None
     gold = _golden(cfg.name)
     if not args.no_ttt:
+        _warm_solvers(cfg, stream)
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()

@@ -329,9 +329,12 @@ def solve(obj: SylvesterSketchedKrylov, tol: float, d_max: int, keep_Y=True) -> 
     Schedule: check_schedule(); past its every-10 regime, when the log-linear extrapolation of
     the last two valid checks puts the crossing d_hat before the next scheduled check, the
     next check is at max(d_last + 1, ceil(d_hat) + 2) instead; inside the every-10 regime a
-    check is skipped while d_hat lies more than 10 steps past it and the next check is still in
-    that regime (round 2: the cheap early checks; skipping into the geometric regime overshot
-    c1's crossing by 250 steps in a simulation on the goldens' rho(d), so it is not done).  Search on the bracket
+    check is skipped while d_hat lies more than 10 steps past it, the next check is still in
+    that regime and lies at most 50 steps past the last valid check (round 2: the cheap early
+    checks; skipping into the geometric regime overshot c1's crossing by 250 steps in a
+    simulation on the goldens' rho(d), so it is not done; without the 50-step bound Ex. 6.1
+    nu = 0.001 (r = 1: the every-10 regime reaches d_max = 800) skipped from d = 270 to 800,
+    where rho_rel = 3.5 (kappa(T) ~ 1e16), and found no crossing).  Search on the bracket
     (d_fail, d_pass]: regula falsi on log rho_rel (x = lo + (log r_lo - log tol) /
     (log r_lo - log r_hi) (hi - lo), checked at ceil(x) clamped into the bracket, or at hi - 1 when
 that is within 2 of hi), a bisection
@@ -351,7 +354,7 @@ that is within 2 of hi), a bisection
             if math.isfinite(dh) and sched[idx] * obj.r > 800 and dh + 2 < sched[idx]:
                 sched[idx] = max(d2 + 1, math.ceil(dh) + 2)
             elif (math.isfinite(dh) and dh - 10 > sched[idx] and idx + 1 < len(sched)
-                  and sched[idx + 1] * obj.r <= 800):
+                  and sched[idx + 1] * obj.r <= 800 and sched[idx + 1] - d2 <= 50):
                 continue          # every-10 regime: crossing predicted > 10 steps past: skip (R9)
         dc = sched[idx]
         t0 = time.perf_counter()

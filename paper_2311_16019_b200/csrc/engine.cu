@@ -274,6 +274,7 @@ struct sylv_ctx {
   int gpu_fail_d = 1 << 30;     // smallest d where the device solve fell back to the host
   int sign_fail_d = 1 << 30;    // smallest d where the sign iteration failed (eig solve from there)
   int eig_solve = 1;            // certified eigendecomposition solve (SYLV_EIG=0: off, 2: first; tests)
+  bool dev_svd = true;          // second pass: SVD + T^-1 Y on the device (SYLV_DEVSVD=0: host)
   int64_t eig_solves = 0;
   // solve driver, schedule phase: a device solve that converged off the identity (approximate;
   // c1's ill-conditioned projections) may decide a check "fail" when its rho_rel exceeds this
@@ -1831,6 +1832,7 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     SYLV_DISPATCH_R(r, { c->tileQ = qtw_tile<R_>(); });
     if (const char* e = std::getenv("SYLV_QMMA")) c->qmma = std::atoi(e) != 0;   // A/B switch
     if (const char* e = std::getenv("SYLV_EIG")) c->eig_solve = std::atoi(e);   // A/B switch, tests
+    if (const char* e = std::getenv("SYLV_DEVSVD")) c->dev_svd = std::atoi(e) != 0;   // A/B switch
     c->RT = (int)((c->sq + c->tileQ - 1) / c->tileQ);
     // Q c: (ceil(s/256) x CC) CTAs, ~4 per SM at the full width (each thread streams a row
     // of its column chunk with 8 loads in flight)
@@ -2072,29 +2074,102 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
     InitTrace tr;   // SYLV_TRACE_INIT=1: phase times on stderr
     std::vector<double> Y1, Y2;
     std::string err;
-    const int l = svd_truncate(m, c->Y, c->rank_tol, max_rank, Y1, Y2, err);
-    tr.mark("solution: SVD of Y", c->st);
-    if (l < 0) return fail(c, SYLV_E_LAPACK, err);
+    // Device front end (round 2; SYLV_DEVSVD=0: host): SVD of Y by cuSOLVER Xgesvdp, the rank at
+    // rank_tol from the singular values (R12), Y_q = U/V[:, :l] sqrt(S), Z = T_d^{-1} Y_q (cuBLAS
+    // DTRSM on the device T) and the M_b = R_b Z_b blocks by a kernel: no m x m host round trip.
+    // Falls back to the host SVD (LAPACK dgesdd) if cuSOLVER fails.
+    double* Mdev[2] = {nullptr, nullptr};
+    int l = -1;
+    if (c->dev_svd && c->method != SYLV_METHOD_FULL) {
+      try {
+        if (!c->gsolve) {
+          c->gsolve = new GpuSylv();
+          c->gsolve->mcap = (c->dmax + 1) * r;
+        }
+        GpuSylv& gs = *c->gsolve;
+        gs.ensure(m, r, c->st);
+        if (!c->y_dev)
+          CK(cudaMemcpyAsync(gs.C, c->Y.data(), (size_t)m * m * sizeof(double), cudaMemcpyHostToDevice, c->st));
+        double* Sd = dalloc<double>((size_t)m);
+        double esig = 0.0;
+        const bool ok = gs.svd(gs.C, m, Sd, &esig);
+        std::vector<double> S((size_t)m);
+        if (ok) {
+          CK(cudaMemcpyAsync(S.data(), Sd, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+          CK(cudaStreamSynchronize(c->st));
+        }
+        if (ok && m > 0 && std::isfinite(S[0])) {
+          int ll = 0;
+          if (S[0] > 0.0)
+            while (ll < m && S[ll] > c->rank_tol * S[0]) ++ll;
+          l = std::min(ll, max_rank);
+          const int64_t ml = (int64_t)m * l;
+          const int g = (int)std::max<int64_t>(1, std::min<int64_t>(4096, (ml + 255) / 256));
+          tr.mark("solution: SVD of Y (device)", c->st);
+          double* Yq[2] = {gs.Ai, gs.Bi};
+          if (l > 0) {
+            k_scale_cols<<<g, 256, 0, c->st>>>(gs.A, Sd, m, l, Yq[0]);
+            k_scale_cols<<<g, 256, 0, c->st>>>(gs.B, Sd, m, l, Yq[1]);
+            count(c, 2);
+            CK(cudaGetLastError());
+            if (cublasSetStream(gs.hb, c->st) != CUBLAS_STATUS_SUCCESS) throw Status{SYLV_E_CUDA, "cublasSetStream"};
+            const double one = 1.0;
+            for (int qi = 0; qi < 2; ++qi) {
+              Sequence& q = c->seq[qi];
+              if (cublasDtrsm(gs.hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, l,
+                              &one, q.Tdev, (int)q.ldT, Yq[qi], m) != CUBLAS_STATUS_SUCCESS)
+                throw Status{SYLV_E_CUDA, "cublasDtrsm (T^-1 Y)"};
+              Mdev[qi] = dalloc<double>((size_t)ml);
+              k_rblocks<<<g, 256, 0, c->st>>>(q.Rall, Yq[qi], d, r, l, Mdev[qi]);
+              count(c);
+              CK(cudaGetLastError());
+            }
+          }
+          tr.mark("solution: T^-1 Y, R_b blocks (device)", c->st);
+        }
+        dfree(Sd);
+      } catch (const ProjError& e) {
+        cudaGetLastError();
+        for (double*& p : Mdev)
+          if (p) { dfree(p); p = nullptr; }
+        l = -1;
+      }
+    }
+    const bool dev_front = l >= 0;
+    if (!dev_front) {
+      if (c->y_dev) {
+        c->Y.resize((size_t)m * m);
+        CK(cudaMemcpyAsync(c->Y.data(), c->gsolve->C, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        c->y_dev = false;
+      }
+      l = svd_truncate(m, c->Y, c->rank_tol, max_rank, Y1, Y2, err);
+      tr.mark("solution: SVD of Y", c->st);
+      if (l < 0) return fail(c, SYLV_E_LAPACK, err);
+    }
     if (rank) *rank = l;
     double* Xout[2] = {X1, X2};
     std::vector<double>* Ys[2] = {&Y1, &Y2};
     for (int qi = 0; qi < 2; ++qi) {
       int C = c->chunk;   // 0: chosen below from the free device memory
       Sequence& q = c->seq[qi];
-      // Z = T_d^{-1} Y_q ; M_b = R_b Z[b-block]  (U_b = Z_b R_b)
-      trsm_left_upper(m, l, q.Th, q.ldT, Ys[qi]->data());
-      CK(cudaMemcpyAsync(q.Rh, q.Rall, (size_t)(d + 2) * r * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-      CK(cudaStreamSynchronize(c->st));
-      std::vector<double> M((size_t)m * std::max(l, 1), 0.0);
-      for (int b = 1; b <= d; ++b)
-        for (int a = 0; a < r; ++a)
-          for (int col = 0; col < l; ++col) {
-            double s = 0.0;
-            for (int p = 0; p < r; ++p)
-              s += q.Rh[(size_t)b * r * r + a * r + p] * (*Ys[qi])[(size_t)col * m + (b - 1) * r + p];
-            M[(size_t)((b - 1) * r + a) * l + col] = s;
-          }
-      tr.mark("solution: T^-1 Y, R_b blocks", c->st);
+      std::vector<double> M;
+      if (!dev_front) {
+        // Z = T_d^{-1} Y_q ; M_b = R_b Z[b-block]  (U_b = Z_b R_b)
+        trsm_left_upper(m, l, q.Th, q.ldT, Ys[qi]->data());
+        CK(cudaMemcpyAsync(q.Rh, q.Rall, (size_t)(d + 2) * r * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        M.assign((size_t)m * std::max(l, 1), 0.0);
+        for (int b = 1; b <= d; ++b)
+          for (int a = 0; a < r; ++a)
+            for (int col = 0; col < l; ++col) {
+              double s = 0.0;
+              for (int p = 0; p < r; ++p)
+                s += q.Rh[(size_t)b * r * r + a * r + p] * (*Ys[qi])[(size_t)col * m + (b - 1) * r + p];
+              M[(size_t)((b - 1) * r + a) * l + col] = s;
+            }
+        tr.mark("solution: T^-1 Y, R_b blocks", c->st);
+      }
       const bool dev_out = is_device_ptr(Xout[qi]);
       double* Xd = dev_out ? Xout[qi] : dalloc<double>((size_t)c->n * ldx);
       CK(cudaMemsetAsync(Xd, 0, (size_t)c->n * ldx * sizeof(double), c->st));
@@ -2116,7 +2191,8 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
         CK(cudaStreamSynchronize(c->st));
         dfree(Md);
       } else if (l > 0) {
-        double* Md = dalloc<double>(M.size());
+        double* Md = dev_front ? Mdev[qi] : dalloc<double>(M.size());
+        Mdev[qi] = nullptr;
         if (C <= 0) {
           // replay chunk: every chunk of C blocks is one pass over X (n x l) — with the default
           // C = k + 1 the X traffic dominated the second pass (c3 at rank 216: 58 passes over
@@ -2128,7 +2204,7 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
         }
         double* rbuf = dalloc<double>((size_t)(K + C) * q.ld * r);
         CK(cudaMemsetAsync(rbuf, 0, (size_t)(K + C) * q.ld * r * sizeof(double), c->st));   // ghosts = 0
-        CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+        if (!dev_front) CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
         auto rslot = [&](int j) { return rbuf + (int64_t)(j % (K + C)) * q.ld * r + q.gz; };
         CK(cudaMemcpyAsync(rslot(1) - q.gz, q.Cdev, (size_t)q.ld * r * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
         // the 2.5-D TMA pass 2 for the replay too: tensor maps of the replay slots
@@ -2216,6 +2292,8 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
         dfree(Xd);
       }
     }
+    for (double* p : Mdev)
+      if (p) dfree(p);
     CK(cudaStreamSynchronize(c->st));
     return SYLV_OK;
   });
@@ -2329,8 +2407,8 @@ sylv_status sylv_sketch_solve(sylv_ctx* c, int32_t* d_star, double* rho_rel) {
           }
         }
       } else if (std::isfinite(dh) && dh - 10 > sched[idx] && idx + 1 < sched.size() &&
-                 (int64_t)sched[idx + 1] * c->R <= 800) {
-        continue;
+                 (int64_t)sched[idx + 1] * c->R <= 800 && sched[idx + 1] - b.first <= 50) {
+        continue;   // every-10 regime, crossing far ahead: skip (R9; a valid check every <= 50 steps)
       }
     }
     const int dc = sched[idx];

@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace sylv {
@@ -133,6 +134,32 @@ __global__ void k_add_real(const cuDoubleComplex* __restrict__ Z, int64_t n, dou
     Y[e] += cuCreal(Z[e]);
 }
 
+// second pass front end on the device (round 2): Yq = U[:, :l] sqrt(S) (column scaling)
+__global__ void k_scale_cols(const double* __restrict__ U, const double* __restrict__ S, int m, int l,
+                             double* __restrict__ out) {
+  const int64_t total = (int64_t)m * l;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int col = (int)(e / m);
+    out[e] = U[e] * sqrt(S[col]);
+  }
+}
+
+// M[((b-1) r + a) l + col] = sum_p Rall[b r r + a r + p] Z[col m + (b-1) r + p]  (U_b = Z_b R_b)
+__global__ void k_rblocks(const double* __restrict__ Rall, const double* __restrict__ Z, int d, int r, int l,
+                          double* __restrict__ M) {
+  const int m = d * r;
+  const int64_t total = (int64_t)m * l;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(e / l), col = (int)(e - (int64_t)row * l);
+    const int b = row / r + 1, a = row % r;
+    const double* Rb = Rall + (int64_t)b * r * r + a * r;
+    const double* z = Z + (int64_t)col * m + (int64_t)(b - 1) * r;
+    double s = 0.0;
+    for (int p = 0; p < r; ++p) s += Rb[p] * z[p];
+    M[e] = s;
+  }
+}
+
 struct GpuSylv {
   cublasHandle_t hb = nullptr;
   cusolverDnHandle_t hs = nullptr;
@@ -146,6 +173,7 @@ struct GpuSylv {
   int cap = 0, capr = 0, lwork = 0;
   int mcap = 1 << 30;            // largest m ever needed ((d_max + 1) r)
   cudaStream_t cur = nullptr;    // stream of the current solve
+  int dev = 0;                   // device of the context (the lane-1 thread sets it)
   double *A = nullptr, *B = nullptr, *C = nullptr, *Ai = nullptr, *Bi = nullptr, *W = nullptr, *LU = nullptr;
   double *Hb = nullptr, *work = nullptr, *dlog = nullptr;
   int *ipiv = nullptr, *info = nullptr;
@@ -159,8 +187,9 @@ struct GpuSylv {
   cuDoubleComplex *VA = nullptr, *VB = nullptr, *VAi = nullptr, *VBi = nullptr, *G1 = nullptr, *G2 = nullptr;
   cuDoubleComplex *wA = nullptr, *wB = nullptr;
   int* pairs = nullptr;                  // 2 m packing flags (A then B)
-  void* gbuf = nullptr;                  // Xgeev device workspace
-  std::vector<char> ghost;               // Xgeev host workspace
+  void* gbuf = nullptr;                  // Xgeev device workspace (lane 0; lane 1: gbuf2)
+  void* gbuf2 = nullptr;
+  std::vector<char> ghost, ghost2;       // Xgeev host workspaces
   size_t gws = 0;
   cusolverDnParams_t gparams = nullptr;
   int ecap = 0;
@@ -174,9 +203,10 @@ struct GpuSylv {
       if (p) cudaFree(p);
     if (pairs) cudaFree(pairs);
     if (gbuf) cudaFree(gbuf);
+    if (gbuf2) cudaFree(gbuf2);
     VA = VB = VAi = VBi = G1 = G2 = wA = wB = nullptr;
     pairs = nullptr;
-    gbuf = nullptr;
+    gbuf = gbuf2 = nullptr;
     gws = 0;
     ecap = 0;
   }
@@ -218,6 +248,7 @@ struct GpuSylv {
 
   void ensure(int m, int r, cudaStream_t st) {
     cur = st;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
     if (!hb) {
       ckb(cublasCreate(&hb), "cublasCreate");
       cks(cusolverDnCreate(&hs), "cusolverDnCreate");
@@ -461,28 +492,42 @@ struct GpuSylv {
     cks(cusolverDnZgetrf_bufferSize(hs, cap, cap, G1, cap, &lw), "zgetrf_bufferSize");
     gws = std::max(wd, (size_t)lw * sizeof(cuDoubleComplex));
     ck(cudaMalloc(&gbuf, gws + 16), "cudaMalloc (eig)");
+    ck(cudaMalloc(&gbuf2, gws + 16), "cudaMalloc (eig)");
     ghost.assign(wh + 16, 0);
+    ghost2.assign(wh + 16, 0);
     ecap = cap;
   }
 
-  // eigenvalues w and complex right eigenvectors V of the real m x m matrix X (X is copied)
-  void eig(const double* X, int m, cuDoubleComplex* w, cuDoubleComplex* V, int* pair_dev) {
-    ck(cudaMemcpyAsync(LU, X, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, cur), "copy (geev)");
+  // eigenvalues w, complex right eigenvectors V and Vi = V^{-1} of the real m x m matrix X (X is
+  // copied) on solver lane 0 (hs, cur; LU, VR in Ai, LU of V in G1) or lane 1 (hs2, st2; LU2,
+  // VR in W, G2): the A and B halves run concurrently from two host threads.
+  void eig_inv(const double* X, int m, cuDoubleComplex* w, cuDoubleComplex* V, cuDoubleComplex* Vi, int* pair_dev,
+               int lane) {
+    cusolverDnHandle_t h = lane ? hs2 : hs;
+    cudaStream_t s = lane ? st2 : cur;
+    double* in = lane ? LU2 : LU;
+    double* vr = lane ? W : Ai;
+    void* gb = lane ? gbuf2 : gbuf;
+    std::vector<char>& gh = lane ? ghost2 : ghost;
+    int* inf_d = lane ? info2 : info;
+    int* piv = lane ? ipiv2 : ipiv;
+    cuDoubleComplex* lu = lane ? G2 : G1;
+    ck(cudaMemcpyAsync(in, X, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy (geev)");
     size_t wd = 0, wh = 0;
-    cks(cusolverDnXgeev_bufferSize(hs, gparams, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_R_64F,
-                                   LU, m, CUDA_C_64F, w, CUDA_R_64F, nullptr, m, CUDA_R_64F, Ai, m, CUDA_R_64F, &wd,
+    cks(cusolverDnXgeev_bufferSize(h, gparams, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_R_64F,
+                                   in, m, CUDA_C_64F, w, CUDA_R_64F, nullptr, m, CUDA_R_64F, vr, m, CUDA_R_64F, &wd,
                                    &wh),
         "Xgeev_bufferSize");
-    if (wd > gws || wh + 16 > ghost.size()) throw ProjError{"Xgeev workspace grew"};
-    cks(cusolverDnXgeev(hs, gparams, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_R_64F, LU, m,
-                        CUDA_C_64F, w, CUDA_R_64F, nullptr, m, CUDA_R_64F, Ai, m, CUDA_R_64F, gbuf, gws, ghost.data(),
-                        wh, info),
+    if (wd > gws || wh + 16 > gh.size()) throw ProjError{"Xgeev workspace grew"};
+    cks(cusolverDnXgeev(h, gparams, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_R_64F, in, m,
+                        CUDA_C_64F, w, CUDA_R_64F, nullptr, m, CUDA_R_64F, vr, m, CUDA_R_64F, gb, gws, gh.data(), wh,
+                        inf_d),
         "Xgeev");
     int inf = 0;
     std::vector<cuDoubleComplex> wh_((size_t)m);
-    ck(cudaMemcpyAsync(&inf, info, sizeof(int), cudaMemcpyDeviceToHost, cur), "D2H");
-    ck(cudaMemcpyAsync(wh_.data(), w, (size_t)m * sizeof(cuDoubleComplex), cudaMemcpyDeviceToHost, cur), "D2H");
-    ck(cudaStreamSynchronize(cur), "sync");
+    ck(cudaMemcpyAsync(&inf, inf_d, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaMemcpyAsync(wh_.data(), w, (size_t)m * sizeof(cuDoubleComplex), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
     if (inf != 0) throw ProjError{"Xgeev info " + std::to_string(inf)};
     std::vector<int> pr((size_t)m, 0);
     for (int j = 0; j < m; ++j) {
@@ -493,23 +538,18 @@ struct GpuSylv {
         pr[j + 1] = 2;
       }
     }
-    ck(cudaMemcpyAsync(pair_dev, pr.data(), (size_t)m * sizeof(int), cudaMemcpyHostToDevice, cur), "H2D");
+    ck(cudaMemcpyAsync(pair_dev, pr.data(), (size_t)m * sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
     const int64_t mm = (int64_t)m * m;
-    k_unpack_vr<<<(int)std::min<int64_t>(4096, (mm + 255) / 256), 256, 0, cur>>>(Ai, pair_dev, m, V);
+    const int g = (int)std::min<int64_t>(4096, (mm + 255) / 256);
+    k_unpack_vr<<<g, 256, 0, s>>>(vr, pair_dev, m, V);
     ck(cudaGetLastError(), "k_unpack_vr");
-    ck(cudaStreamSynchronize(cur), "sync");   // pr (host) is read by the async copy
-  }
-
-  // Vi = V^{-1} (complex LU in G1)
-  void cinv(const cuDoubleComplex* V, cuDoubleComplex* Vi, int m) {
-    const int64_t mm = (int64_t)m * m;
-    ck(cudaMemcpyAsync(G1, V, (size_t)mm * sizeof(cuDoubleComplex), cudaMemcpyDeviceToDevice, cur), "copy");
-    cks(cusolverDnZgetrf(hs, m, m, G1, m, reinterpret_cast<cuDoubleComplex*>(gbuf), ipiv, info), "zgetrf");
-    k_ceye<<<(int)std::min<int64_t>(4096, (mm + 255) / 256), 256, 0, cur>>>(Vi, m);
-    cks(cusolverDnZgetrs(hs, CUBLAS_OP_N, m, m, G1, m, ipiv, Vi, m, info), "zgetrs");
-    int inf = 0;
-    ck(cudaMemcpyAsync(&inf, info, sizeof(int), cudaMemcpyDeviceToHost, cur), "D2H");
-    ck(cudaStreamSynchronize(cur), "sync");
+    // Vi = V^{-1}: complex LU, then solves against the identity
+    ck(cudaMemcpyAsync(lu, V, (size_t)mm * sizeof(cuDoubleComplex), cudaMemcpyDeviceToDevice, s), "copy");
+    cks(cusolverDnZgetrf(h, m, m, lu, m, reinterpret_cast<cuDoubleComplex*>(gb), piv, inf_d), "zgetrf");
+    k_ceye<<<g, 256, 0, s>>>(Vi, m);
+    cks(cusolverDnZgetrs(h, CUBLAS_OP_N, m, m, lu, m, piv, Vi, m, inf_d), "zgetrs");
+    ck(cudaMemcpyAsync(&inf, inf_d, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");   // also: pr (host) was read by the async copy
     if (inf != 0) throw ProjError{"singular eigenvector matrix"};
   }
 
@@ -549,10 +589,29 @@ struct GpuSylv {
     ck(cudaMemcpy2DAsync(Bi, (size_t)m * sizeof(double), cb.data(), (size_t)r * sizeof(double),
                          (size_t)r * sizeof(double), r, cudaMemcpyHostToDevice, st),
        "H2D (rhs)");
-    eig(A, m, wA, VA, pairs);
-    eig(B, m, wB, VB, pairs + m);
-    cinv(VA, VAi, m);
-    cinv(VB, VBi, m);
+    // lane 1 (B = M_V^T) on its own thread and stream, concurrently with lane 0 (A = M_U)
+    ck(cudaEventRecord(ev_fork, st), "event");
+    ck(cudaStreamWaitEvent(st2, ev_fork, 0), "event");
+    std::string err1;
+    std::thread lane1([&]() {
+      try {
+        ck(cudaSetDevice(dev), "cudaSetDevice");
+        eig_inv(B, m, wB, VB, VBi, pairs + m, 1);
+      } catch (const ProjError& e) {
+        err1 = e.what.empty() ? "lane 1 failed" : e.what;
+      }
+    });
+    std::string err0;
+    try {
+      eig_inv(A, m, wA, VA, VAi, pairs, 0);
+    } catch (const ProjError& e) {
+      err0 = e.what.empty() ? "lane 0 failed" : e.what;
+    }
+    lane1.join();
+    if (!err0.empty()) throw ProjError{err0};
+    if (!err1.empty()) throw ProjError{err1};
+    ck(cudaEventRecord(ev_join, st2), "event");
+    ck(cudaStreamWaitEvent(st, ev_join, 0), "event");
     auto t1 = std::chrono::steady_clock::now();
     t_eig = std::chrono::duration<double>(t1 - t0).count();
     const double nA = fro(A, mm), nB = fro(B, mm), nF = fro(Bi, mm);
@@ -581,6 +640,29 @@ struct GpuSylv {
       std::fprintf(stderr, "[proj] m=%d eig %.1f ms, %d refinements %.1f ms, residual %.2e (%s)\n", m, 1e3 * t_eig,
                    eig_refine, 1e3 * t_refine, eig_res, okc ? "certified" : "rejected");
     return okc;
+  }
+
+  // SVD Y = U diag(S) V^T of the m x m Yd (device, not modified) by cuSOLVER Xgesvdp (polar
+  // decomposition + symmetric eigensolver, backward stable): U -> A, V -> B, S -> Sd (device,
+  // descending).  false when cuSOLVER reports failure (the caller uses the host SVD).
+  bool svd(const double* Yd, int m, double* Sd, double* err_sigma) {
+    ck(cudaMemcpyAsync(W, Yd, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, cur), "copy (svd)");
+    if (!gparams) cks(cusolverDnCreateParams(&gparams), "cusolverDnCreateParams");
+    size_t wd = 0, wh = 0;
+    cks(cusolverDnXgesvdp_bufferSize(hs, gparams, CUSOLVER_EIG_MODE_VECTOR, 0, m, m, CUDA_R_64F, W, m, CUDA_R_64F, Sd,
+                                     CUDA_R_64F, A, m, CUDA_R_64F, B, m, CUDA_R_64F, &wd, &wh),
+        "Xgesvdp_bufferSize");
+    void* bd = nullptr;
+    ck(cudaMalloc(&bd, wd + 16), "cudaMalloc (svd)");
+    std::vector<char> bh(wh + 16);
+    cusolverStatus_t stt = cusolverDnXgesvdp(hs, gparams, CUSOLVER_EIG_MODE_VECTOR, 0, m, m, CUDA_R_64F, W, m,
+                                             CUDA_R_64F, Sd, CUDA_R_64F, A, m, CUDA_R_64F, B, m, CUDA_R_64F, bd, wd,
+                                             bh.data(), wh, info, err_sigma);
+    int inf = -1;
+    if (stt == CUSOLVER_STATUS_SUCCESS) ck(cudaMemcpyAsync(&inf, info, sizeof(int), cudaMemcpyDeviceToHost, cur), "D2H");
+    ck(cudaStreamSynchronize(cur), "sync");
+    cudaFree(bd);
+    return stt == CUSOLVER_STATUS_SUCCESS && inf == 0;
   }
 };
 
