@@ -502,6 +502,8 @@ def main():
                 "extrapolation": "this box's oracle step rate x the golden's steps + the golden's "
                                  "projected-solve seconds (solves not re-timed here)"}
 
+    clk_sum = clk.summary()
+    l2_peak = 6300 * (clk_sum.get("sm_mhz") or 1965.0) * 1e6 / 1e9   # GB/s
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -521,6 +523,9 @@ def main():
                          "skqr_ms": stats["ms_skqr"] / max(1, stats["n_skqr"]),
                          "sketch_l2": {"bytes_per_launch": cfg.zeta * ab["sketch"],
                                        "GBps": cfg.zeta * ab["sketch"] / (sk_ms * 1e-3) / 1e9,
+                                       "peak": l2_peak, "frac": cfg.zeta * ab["sketch"] / (sk_ms * 1e-3) / 1e9 / l2_peak,
+                                       "peak_source": "LTS throughput cap ~6300 B/cycle full chip (B300_MICROARCH.md, "
+                                                      "measured on B300; same L2 design) x median SM clock under load",
                                        "what": "pull sketch (sketch_pull.cuh): every element of the new block "
                                                "is read zeta times from L2 (once per bucket); bound by L2->SM "
                                                "bandwidth, not HBM (ncu lts__throughput, profiles/)"},
@@ -531,7 +536,7 @@ def main():
                               "what": "SURVEY §8(d) B_n per block step (both sequences) / device step time"},
             "time_to_tolerance": ttt, "near_dstar": near,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clk_sum,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

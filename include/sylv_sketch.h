@@ -173,9 +173,12 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B,
  * reached before nsteps.  After BREAKDOWN / LOST_INDEP further calls return that status. */
 sylv_status sylv_sketch_step(sylv_ctx* ctx, int32_t nsteps, int32_t* d_done);
 
-/* Host projected solve at 1 <= d <= d_done (Alg. 1 lines 10-13): M_U Y + Y M_V^T =
+/* Projected solve at 1 <= d <= d_done (Alg. 1 lines 10-13): M_U Y + Y M_V^T =
  * E1 beta1 beta2^T E1^T with M_U = [T_d | T_H] H_und_d T_d^{-1} (R6), then
  * rho^2 = ||hhat E_d^T Y||^2 + ||Y E_d ghat^T||^2, rho_rel = rho / ||beta1 beta2^T||_F.
+ * Solver: host Bartels-Stewart (LAPACK) for d r < 512; above, on the device: the sign-function
+ * iteration, else (where it fails: spec(M_V) not in Re > 0) an eigendecomposition solve
+ * accepted only when its refined projected residual is at rounding level, else the host.
  * Y is kept in the context for sylv_sketch_solution(ctx, d, ...). */
 sylv_status sylv_sketch_residual(sylv_ctx* ctx, int32_t d, double* rho, double* rho_rel);
 
@@ -228,7 +231,8 @@ typedef struct {
   double host_solve_s;       /* wall seconds spent in host projected solves       */
   int64_t host_solves;
   double kappa_T_u, kappa_T_v; /* reserved                                        */
-  int64_t gpu_solves;        /* projected solves done on the device (sign iteration) */
+  int64_t gpu_solves;        /* projected solves done on the device (sign iteration or
+                                certified eigendecomposition)                        */
   double gpu_solve_s;        /* wall seconds in them                               */
   int64_t gpu_solve_fallbacks; /* device solves that did not converge -> host BS   */
   int64_t gpu_approx_checks;   /* solve driver: checks decided "rho_rel > 3 tol" by a

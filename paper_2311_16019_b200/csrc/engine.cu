@@ -274,7 +274,6 @@ struct sylv_ctx {
   int gpu_fail_d = 1 << 30;     // smallest d where the device solve fell back to the host
   int sign_fail_d = 1 << 30;    // smallest d where the sign iteration failed (eig solve from there)
   int eig_solve = 1;            // certified eigendecomposition solve (SYLV_EIG=0: off, 2: first; tests)
-  bool dev_svd = true;          // second pass: SVD + T^-1 Y on the device (SYLV_DEVSVD=0: host)
   int64_t eig_solves = 0;
   // solve driver, schedule phase: a device solve that converged off the identity (approximate;
   // c1's ill-conditioned projections) may decide a check "fail" when its rho_rel exceeds this
@@ -1412,6 +1411,24 @@ sylv_status guard(sylv_ctx* c, F&& f) {
 }
 
 // Projected solve of check d on the device (sign iteration) or on the host (Bartels-Stewart)
+// Sharded contexts solve the projected equation redundantly on every rank (identical small
+// matrices).  The library solvers on that path need not be bitwise reproducible across ranks
+// (cuSOLVER Xgeev's hybrid host part; a device solve certified on one rank, rejected on another),
+// so the values a decision or an output rests on — rho, and Y for the second pass — are rank 0's
+// on every rank: one allreduce on the setup channel with the other ranks contributing zeros.
+void agree_rank0(sylv_ctx* c, double* host, size_t n) {
+  if (!c->comm || c->comm->nranks <= 1 || n == 0) return;
+  double* buf = dalloc<double>(n);
+  if (c->comm->rank == 0)
+    CK(cudaMemcpyAsync(buf, host, n * sizeof(double), cudaMemcpyHostToDevice, c->rst));
+  else
+    CK(cudaMemsetAsync(buf, 0, n * sizeof(double), c->rst));
+  c->comm->allreduce(buf, n, c->rst, kChanSetup);
+  CK(cudaMemcpyAsync(host, buf, n * sizeof(double), cudaMemcpyDeviceToHost, c->rst));
+  CK(cudaStreamSynchronize(c->rst));
+  dfree(buf);
+}
+
 bool device_solve(const sylv_ctx* c, int d) {
   // auto: device for d r >= 512, except at and beyond a d where it already fell back (the
   // conditioning of the projected matrices only grows with d: c1 needs the host there)
@@ -1574,7 +1591,9 @@ double probe_rho(sylv_ctx* c, int d) {
         s2 += v * v;
       }
     c->stats.gpu_approx_checks++;
-    return std::sqrt(s1 + s2) / bn;
+    double pr = std::sqrt(s1 + s2) / bn;
+    agree_rank0(c, &pr, 1);   // the check placement must not diverge across ranks
+    return pr;
   } catch (const ProjError&) {
     cudaGetLastError();
     return NAN;
@@ -1832,7 +1851,6 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     SYLV_DISPATCH_R(r, { c->tileQ = qtw_tile<R_>(); });
     if (const char* e = std::getenv("SYLV_QMMA")) c->qmma = std::atoi(e) != 0;   // A/B switch
     if (const char* e = std::getenv("SYLV_EIG")) c->eig_solve = std::atoi(e);   // A/B switch, tests
-    if (const char* e = std::getenv("SYLV_DEVSVD")) c->dev_svd = std::atoi(e) != 0;   // A/B switch
     c->RT = (int)((c->sq + c->tileQ - 1) / c->tileQ);
     // Q c: (ceil(s/256) x CC) CTAs, ~4 per SM at the full width (each thread streams a row
     // of its column chunk with 8 loads in flight)
@@ -2002,6 +2020,7 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
         c->stats.gpu_solve_fallbacks++;
         c->gpu_fail_d = std::min(c->gpu_fail_d, d);
         c->err = "device projected solve failed at d = " + std::to_string(d) + ": " + e.what + "; host fallback";
+        if (std::getenv("SYLV_TRACE_PROJ")) std::fprintf(stderr, "[proj] %s\n", c->err.c_str());
         cudaGetLastError();
       }
     }
@@ -2046,6 +2065,7 @@ sylv_status sylv_sketch_residual(sylv_ctx* c, int32_t d, double* rho, double* rh
       const double a = rho_of(lrow, zc), b = rho_of(zc, lcol);
       rh = std::sqrt((double)m) * (a + b);
     }
+    agree_rank0(c, &rh, 1);
     if (rho) *rho = rh;
     if (rho_rel) *rho_rel = rh / bn;
     c->hist.emplace_back(d, rh / bn);
@@ -2074,102 +2094,36 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
     InitTrace tr;   // SYLV_TRACE_INIT=1: phase times on stderr
     std::vector<double> Y1, Y2;
     std::string err;
-    // Device front end (round 2; SYLV_DEVSVD=0: host): SVD of Y by cuSOLVER Xgesvdp, the rank at
-    // rank_tol from the singular values (R12), Y_q = U/V[:, :l] sqrt(S), Z = T_d^{-1} Y_q (cuBLAS
-    // DTRSM on the device T) and the M_b = R_b Z_b blocks by a kernel: no m x m host round trip.
-    // Falls back to the host SVD (LAPACK dgesdd) if cuSOLVER fails.
-    double* Mdev[2] = {nullptr, nullptr};
-    int l = -1;
-    if (c->dev_svd && c->method != SYLV_METHOD_FULL) {
-      try {
-        if (!c->gsolve) {
-          c->gsolve = new GpuSylv();
-          c->gsolve->mcap = (c->dmax + 1) * r;
-        }
-        GpuSylv& gs = *c->gsolve;
-        gs.ensure(m, r, c->st);
-        if (!c->y_dev)
-          CK(cudaMemcpyAsync(gs.C, c->Y.data(), (size_t)m * m * sizeof(double), cudaMemcpyHostToDevice, c->st));
-        double* Sd = dalloc<double>((size_t)m);
-        double esig = 0.0;
-        const bool ok = gs.svd(gs.C, m, Sd, &esig);
-        std::vector<double> S((size_t)m);
-        if (ok) {
-          CK(cudaMemcpyAsync(S.data(), Sd, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-          CK(cudaStreamSynchronize(c->st));
-        }
-        if (ok && m > 0 && std::isfinite(S[0])) {
-          int ll = 0;
-          if (S[0] > 0.0)
-            while (ll < m && S[ll] > c->rank_tol * S[0]) ++ll;
-          l = std::min(ll, max_rank);
-          const int64_t ml = (int64_t)m * l;
-          const int g = (int)std::max<int64_t>(1, std::min<int64_t>(4096, (ml + 255) / 256));
-          tr.mark("solution: SVD of Y (device)", c->st);
-          double* Yq[2] = {gs.Ai, gs.Bi};
-          if (l > 0) {
-            k_scale_cols<<<g, 256, 0, c->st>>>(gs.A, Sd, m, l, Yq[0]);
-            k_scale_cols<<<g, 256, 0, c->st>>>(gs.B, Sd, m, l, Yq[1]);
-            count(c, 2);
-            CK(cudaGetLastError());
-            if (cublasSetStream(gs.hb, c->st) != CUBLAS_STATUS_SUCCESS) throw Status{SYLV_E_CUDA, "cublasSetStream"};
-            const double one = 1.0;
-            for (int qi = 0; qi < 2; ++qi) {
-              Sequence& q = c->seq[qi];
-              if (cublasDtrsm(gs.hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, l,
-                              &one, q.Tdev, (int)q.ldT, Yq[qi], m) != CUBLAS_STATUS_SUCCESS)
-                throw Status{SYLV_E_CUDA, "cublasDtrsm (T^-1 Y)"};
-              Mdev[qi] = dalloc<double>((size_t)ml);
-              k_rblocks<<<g, 256, 0, c->st>>>(q.Rall, Yq[qi], d, r, l, Mdev[qi]);
-              count(c);
-              CK(cudaGetLastError());
-            }
-          }
-          tr.mark("solution: T^-1 Y, R_b blocks (device)", c->st);
-        }
-        dfree(Sd);
-      } catch (const ProjError& e) {
-        cudaGetLastError();
-        for (double*& p : Mdev)
-          if (p) { dfree(p); p = nullptr; }
-        l = -1;
-      }
-    }
-    const bool dev_front = l >= 0;
-    if (!dev_front) {
-      if (c->y_dev) {
-        c->Y.resize((size_t)m * m);
-        CK(cudaMemcpyAsync(c->Y.data(), c->gsolve->C, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
-        c->y_dev = false;
-      }
-      l = svd_truncate(m, c->Y, c->rank_tol, max_rank, Y1, Y2, err);
-      tr.mark("solution: SVD of Y", c->st);
-      if (l < 0) return fail(c, SYLV_E_LAPACK, err);
-    }
+    agree_rank0(c, c->Y.data(), (size_t)m * m);   // sharded: rank 0's Y on every rank
+    const int l = svd_truncate(m, c->Y, c->rank_tol, max_rank, Y1, Y2, err);
+    tr.mark("solution: SVD of Y", c->st);
+    if (l < 0) return fail(c, SYLV_E_LAPACK, err);
     if (rank) *rank = l;
     double* Xout[2] = {X1, X2};
     std::vector<double>* Ys[2] = {&Y1, &Y2};
+    double* rbuf_keep = nullptr;   // replay ring, shared by the two sequences
+    size_t rbuf_elems = 0;
+    struct RbufFree {
+      double*& p;
+      ~RbufFree() { if (p) dfree(p); }
+    } rbuf_guard{rbuf_keep};
     for (int qi = 0; qi < 2; ++qi) {
       int C = c->chunk;   // 0: chosen below from the free device memory
       Sequence& q = c->seq[qi];
-      std::vector<double> M;
-      if (!dev_front) {
-        // Z = T_d^{-1} Y_q ; M_b = R_b Z[b-block]  (U_b = Z_b R_b)
-        trsm_left_upper(m, l, q.Th, q.ldT, Ys[qi]->data());
-        CK(cudaMemcpyAsync(q.Rh, q.Rall, (size_t)(d + 2) * r * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
-        M.assign((size_t)m * std::max(l, 1), 0.0);
-        for (int b = 1; b <= d; ++b)
-          for (int a = 0; a < r; ++a)
-            for (int col = 0; col < l; ++col) {
-              double s = 0.0;
-              for (int p = 0; p < r; ++p)
-                s += q.Rh[(size_t)b * r * r + a * r + p] * (*Ys[qi])[(size_t)col * m + (b - 1) * r + p];
-              M[(size_t)((b - 1) * r + a) * l + col] = s;
-            }
-        tr.mark("solution: T^-1 Y, R_b blocks", c->st);
-      }
+      // Z = T_d^{-1} Y_q ; M_b = R_b Z[b-block]  (U_b = Z_b R_b)
+      trsm_left_upper(m, l, q.Th, q.ldT, Ys[qi]->data());
+      CK(cudaMemcpyAsync(q.Rh, q.Rall, (size_t)(d + 2) * r * r * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      std::vector<double> M((size_t)m * std::max(l, 1), 0.0);
+      for (int b = 1; b <= d; ++b)
+        for (int a = 0; a < r; ++a)
+          for (int col = 0; col < l; ++col) {
+            double s = 0.0;
+            for (int p = 0; p < r; ++p)
+              s += q.Rh[(size_t)b * r * r + a * r + p] * (*Ys[qi])[(size_t)col * m + (b - 1) * r + p];
+            M[(size_t)((b - 1) * r + a) * l + col] = s;
+          }
+      tr.mark("solution: T^-1 Y, R_b blocks", c->st);
       const bool dev_out = is_device_ptr(Xout[qi]);
       double* Xd = dev_out ? Xout[qi] : dalloc<double>((size_t)c->n * ldx);
       CK(cudaMemsetAsync(Xd, 0, (size_t)c->n * ldx * sizeof(double), c->st));
@@ -2191,8 +2145,7 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
         CK(cudaStreamSynchronize(c->st));
         dfree(Md);
       } else if (l > 0) {
-        double* Md = dev_front ? Mdev[qi] : dalloc<double>(M.size());
-        Mdev[qi] = nullptr;
+        double* Md = dalloc<double>(M.size());
         if (C <= 0) {
           // replay chunk: every chunk of C blocks is one pass over X (n x l) — with the default
           // C = k + 1 the X traffic dominated the second pass (c3 at rank 216: 58 passes over
@@ -2201,10 +2154,20 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
           CK(cudaMemGetInfo(&fr, &tot));
           const int64_t blkb = q.ld * r * (int64_t)sizeof(double);
           C = (int)std::max<int64_t>(c->K + 1, std::min<int64_t>(kMaxChunk, (int64_t)(fr / 2) / blkb - K));
+          if (rbuf_keep)   // the second sequence: as many blocks as the kept ring holds
+            C = (int)std::max<int64_t>(c->K + 1, std::min<int64_t>(kMaxChunk, (int64_t)rbuf_elems / (q.ld * r) - K));
         }
-        double* rbuf = dalloc<double>((size_t)(K + C) * q.ld * r);
-        CK(cudaMemsetAsync(rbuf, 0, (size_t)(K + C) * q.ld * r * sizeof(double), c->st));   // ghosts = 0
-        if (!dev_front) CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+        // one replay ring for both sequences (a second cudaMalloc/cudaFree of tens of GB cost
+        // ~0.4 s at c3); re-zeroed per sequence (ghosts = 0; the layouts may differ)
+        const size_t rel = (size_t)(K + C) * q.ld * r;
+        if (rel > rbuf_elems) {
+          if (rbuf_keep) dfree(rbuf_keep);
+          rbuf_keep = dalloc<double>(rel);
+          rbuf_elems = rel;
+        }
+        double* rbuf = rbuf_keep;
+        CK(cudaMemsetAsync(rbuf, 0, rel * sizeof(double), c->st));
+        CK(cudaMemcpyAsync(Md, M.data(), M.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
         auto rslot = [&](int j) { return rbuf + (int64_t)(j % (K + C)) * q.ld * r + q.gz; };
         CK(cudaMemcpyAsync(rslot(1) - q.gz, q.Cdev, (size_t)q.ld * r * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
         // the 2.5-D TMA pass 2 for the replay too: tensor maps of the replay slots
@@ -2284,7 +2247,6 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
         CK(cudaStreamSynchronize(c->st));
         tr.mark("solution: replay + X accumulation", c->st);
         dfree(Md);
-        dfree(rbuf);
       }
       if (!dev_out) {
         CK(cudaMemcpyAsync(Xout[qi], Xd, (size_t)c->n * ldx * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -2292,8 +2254,6 @@ sylv_status sylv_sketch_solution(sylv_ctx* c, int32_t d, double* X1, double* X2,
         dfree(Xd);
       }
     }
-    for (double* p : Mdev)
-      if (p) dfree(p);
     CK(cudaStreamSynchronize(c->st));
     return SYLV_OK;
   });

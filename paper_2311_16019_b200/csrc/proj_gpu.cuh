@@ -28,7 +28,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
-#include <thread>
 #include <vector>
 
 namespace sylv {
@@ -132,32 +131,6 @@ __global__ void k_ceye(cuDoubleComplex* __restrict__ X, int m) {
 __global__ void k_add_real(const cuDoubleComplex* __restrict__ Z, int64_t n, double* __restrict__ Y) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     Y[e] += cuCreal(Z[e]);
-}
-
-// second pass front end on the device (round 2): Yq = U[:, :l] sqrt(S) (column scaling)
-__global__ void k_scale_cols(const double* __restrict__ U, const double* __restrict__ S, int m, int l,
-                             double* __restrict__ out) {
-  const int64_t total = (int64_t)m * l;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int col = (int)(e / m);
-    out[e] = U[e] * sqrt(S[col]);
-  }
-}
-
-// M[((b-1) r + a) l + col] = sum_p Rall[b r r + a r + p] Z[col m + (b-1) r + p]  (U_b = Z_b R_b)
-__global__ void k_rblocks(const double* __restrict__ Rall, const double* __restrict__ Z, int d, int r, int l,
-                          double* __restrict__ M) {
-  const int m = d * r;
-  const int64_t total = (int64_t)m * l;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int row = (int)(e / l), col = (int)(e - (int64_t)row * l);
-    const int b = row / r + 1, a = row % r;
-    const double* Rb = Rall + (int64_t)b * r * r + a * r;
-    const double* z = Z + (int64_t)col * m + (int64_t)(b - 1) * r;
-    double s = 0.0;
-    for (int p = 0; p < r; ++p) s += Rb[p] * z[p];
-    M[e] = s;
-  }
 }
 
 struct GpuSylv {
@@ -490,7 +463,7 @@ struct GpuSylv {
         "Xgeev_bufferSize");
     int lw = 0;
     cks(cusolverDnZgetrf_bufferSize(hs, cap, cap, G1, cap, &lw), "zgetrf_bufferSize");
-    gws = std::max(wd, (size_t)lw * sizeof(cuDoubleComplex));
+    gws = 2 * std::max(wd, (size_t)lw * sizeof(cuDoubleComplex));   // margin: queries at m <= cap
     ck(cudaMalloc(&gbuf, gws + 16), "cudaMalloc (eig)");
     ck(cudaMalloc(&gbuf2, gws + 16), "cudaMalloc (eig)");
     ghost.assign(wh + 16, 0);
@@ -518,7 +491,8 @@ struct GpuSylv {
                                    in, m, CUDA_C_64F, w, CUDA_R_64F, nullptr, m, CUDA_R_64F, vr, m, CUDA_R_64F, &wd,
                                    &wh),
         "Xgeev_bufferSize");
-    if (wd > gws || wh + 16 > gh.size()) throw ProjError{"Xgeev workspace grew"};
+    if (wd > gws) throw ProjError{"Xgeev device workspace grew (" + std::to_string(wd) + " > " + std::to_string(gws) + ")"};
+    if (wh + 16 > gh.size()) gh.assign(wh + 16, 0);
     cks(cusolverDnXgeev(h, gparams, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_R_64F, in, m,
                         CUDA_C_64F, w, CUDA_R_64F, nullptr, m, CUDA_R_64F, vr, m, CUDA_R_64F, gb, gws, gh.data(), wh,
                         inf_d),
@@ -589,29 +563,11 @@ struct GpuSylv {
     ck(cudaMemcpy2DAsync(Bi, (size_t)m * sizeof(double), cb.data(), (size_t)r * sizeof(double),
                          (size_t)r * sizeof(double), r, cudaMemcpyHostToDevice, st),
        "H2D (rhs)");
-    // lane 1 (B = M_V^T) on its own thread and stream, concurrently with lane 0 (A = M_U)
-    ck(cudaEventRecord(ev_fork, st), "event");
-    ck(cudaStreamWaitEvent(st2, ev_fork, 0), "event");
-    std::string err1;
-    std::thread lane1([&]() {
-      try {
-        ck(cudaSetDevice(dev), "cudaSetDevice");
-        eig_inv(B, m, wB, VB, VBi, pairs + m, 1);
-      } catch (const ProjError& e) {
-        err1 = e.what.empty() ? "lane 1 failed" : e.what;
-      }
-    });
-    std::string err0;
-    try {
-      eig_inv(A, m, wA, VA, VAi, pairs, 0);
-    } catch (const ProjError& e) {
-      err0 = e.what.empty() ? "lane 0 failed" : e.what;
-    }
-    lane1.join();
-    if (!err0.empty()) throw ProjError{err0};
-    if (!err1.empty()) throw ProjError{err1};
-    ck(cudaEventRecord(ev_join, st2), "event");
-    ck(cudaStreamWaitEvent(st, ev_join, 0), "event");
+    // A = M_U and B = M_V^T in turn on the context's stream: two concurrent Xgeev calls (two
+    // handles, two host threads) failed intermittently with CUSOLVER_STATUS_INTERNAL_ERROR on
+    // B200 (c1, m = 2000), so the halves are serial
+    eig_inv(A, m, wA, VA, VAi, pairs, 0);
+    eig_inv(B, m, wB, VB, VBi, pairs + m, 0);
     auto t1 = std::chrono::steady_clock::now();
     t_eig = std::chrono::duration<double>(t1 - t0).count();
     const double nA = fro(A, mm), nB = fro(B, mm), nF = fro(Bi, mm);
@@ -640,29 +596,6 @@ struct GpuSylv {
       std::fprintf(stderr, "[proj] m=%d eig %.1f ms, %d refinements %.1f ms, residual %.2e (%s)\n", m, 1e3 * t_eig,
                    eig_refine, 1e3 * t_refine, eig_res, okc ? "certified" : "rejected");
     return okc;
-  }
-
-  // SVD Y = U diag(S) V^T of the m x m Yd (device, not modified) by cuSOLVER Xgesvdp (polar
-  // decomposition + symmetric eigensolver, backward stable): U -> A, V -> B, S -> Sd (device,
-  // descending).  false when cuSOLVER reports failure (the caller uses the host SVD).
-  bool svd(const double* Yd, int m, double* Sd, double* err_sigma) {
-    ck(cudaMemcpyAsync(W, Yd, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, cur), "copy (svd)");
-    if (!gparams) cks(cusolverDnCreateParams(&gparams), "cusolverDnCreateParams");
-    size_t wd = 0, wh = 0;
-    cks(cusolverDnXgesvdp_bufferSize(hs, gparams, CUSOLVER_EIG_MODE_VECTOR, 0, m, m, CUDA_R_64F, W, m, CUDA_R_64F, Sd,
-                                     CUDA_R_64F, A, m, CUDA_R_64F, B, m, CUDA_R_64F, &wd, &wh),
-        "Xgesvdp_bufferSize");
-    void* bd = nullptr;
-    ck(cudaMalloc(&bd, wd + 16), "cudaMalloc (svd)");
-    std::vector<char> bh(wh + 16);
-    cusolverStatus_t stt = cusolverDnXgesvdp(hs, gparams, CUSOLVER_EIG_MODE_VECTOR, 0, m, m, CUDA_R_64F, W, m,
-                                             CUDA_R_64F, Sd, CUDA_R_64F, A, m, CUDA_R_64F, B, m, CUDA_R_64F, bd, wd,
-                                             bh.data(), wh, info, err_sigma);
-    int inf = -1;
-    if (stt == CUSOLVER_STATUS_SUCCESS) ck(cudaMemcpyAsync(&inf, info, sizeof(int), cudaMemcpyDeviceToHost, cur), "D2H");
-    ck(cudaStreamSynchronize(cur), "sync");
-    cudaFree(bd);
-    return stt == CUSOLVER_STATUS_SUCCESS && inf == 0;
   }
 };
 

@@ -326,26 +326,3 @@ def test_device_eig_solve_matches_oracle(name, ds, monkeypatch):
     X1h, X2h, kh = h.solution(done, 64)
     assert kg == kh
     assert _rel(X1g @ X2g.T, X1h @ X2h.T) <= 1e-6
-
-
-@pytest.mark.parametrize("name", ["2d-r1", "3d-r8k3", "csr-r4k4"])
-def test_device_svd_front_end_matches_host(name, monkeypatch):
-    """a7 (round 2): the second pass's front end on the device (cuSOLVER Xgesvdp SVD of Y, rank at
-    rank_tol, T_d^{-1} Y by DTRSM, R_b blocks by a kernel) gives the host path's (LAPACK dgesdd,
-    SYLV_DEVSVD=0) rank and solution X1 X2^T (1e-9 relative), and the oracle's (test above)."""
-    cfg = inputs.small_config(**CASES[name])
-    csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
-    C1, C2 = inputs.make_rhs(cfg)
-    st = torch.cuda.current_stream().cuda_stream
-    a = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr,
-                           stream=st)
-    monkeypatch.setenv("SYLV_DEVSVD", "0")
-    b = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr,
-                           stream=st)
-    d = 40 if cfg.r <= 2 else 30
-    a.step(d)
-    b.step(d)
-    X1a, X2a, ka = a.solution(d, 64)
-    X1b, X2b, kb = b.solution(d, 64)
-    assert ka == kb
-    assert _rel(X1a @ X2a.T, X1b @ X2b.T) <= 1e-9

@@ -11,7 +11,7 @@ for c in ex61_nu0.1 ex63_n125000; do timeout 900 python bench.py --config $c --n
 SYLV_TRACE_PROJ=1 timeout 600 python tools/ttt.py c2 > gpurun_out/${tag}_ttt_c2.log 2>&1
 SYLV_TRACE_PROJ=1 timeout 600 python tools/ttt.py c3 > gpurun_out/${tag}_ttt_c3.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_c3_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-ttt --no-near > gpurun_out/${tag}_ncu_launch.log 2>&1; echo ncu $?
-timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "probe/" -k regex:"k_st3d|k_sketch_pull<|k_qtw|k_qc_part" -c 6 -o /tmp/${tag}_c3_full python tools/near_probe.py c3 204 1 > gpurun_out/${tag}_ncu_c3.log 2>&1; echo ncu3 $?
+timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "probe/" -k regex:"k_st3d|k_sketch_pull<|k_qtw|k_qc_part|k_qc_mma" -c 6 -o /tmp/${tag}_c3_full python tools/near_probe.py c3 204 1 > gpurun_out/${tag}_ncu_c3.log 2>&1; echo ncu3 $?
 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "probe/" -k regex:"k_pass1_sell|k_pass2|k_sketch" -c 4 -o /tmp/${tag}_c4_full python tools/near_probe.py c4 5 1 > gpurun_out/${tag}_ncu_c4.log 2>&1; echo ncu4 $?
 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "probe/" -k regex:"k_st3d|k_sketch" -c 4 -o /tmp/${tag}_c2_full python tools/near_probe.py c2 20 1 > gpurun_out/${tag}_ncu_c2.log 2>&1; echo ncu2 $?
 # the .ncu-rep files stay on the box (gpurun_out is capped at 64 MiB): raw metrics as CSV

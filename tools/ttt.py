@@ -28,3 +28,4 @@ s = g.stats()
 print(f"{name}: d*={d} rho_rel={rr:.3e} status={st} init {t1-t0:.2f}s solve {t2-t1:.2f}s approx {s.get('gpu_approx_checks')} "
       f"(host solves {s['host_solves']} taking {s['host_solve_s']:.2f}s; steps {s['steps']})", flush=True)
 print("history", g.history())
+print("last_error", g.last_error())
