@@ -258,6 +258,23 @@ def test_search_is_a_valid_crossing_with_bumps_and_singular_checks():
     assert max(below) == res.d_star - 1 or all(d not in fake.calls for d in range(max(below) + 1, res.d_star))
 
 
+def test_skipping_keeps_a_valid_check_every_50_steps():
+    """R9 (round 2): inside the every-10 regime a check is skipped only while the next one lies
+    at most 50 steps past the last valid check.  A slowly decaying rho (r = 1, so the regime
+    runs to d_max: Ex. 6.1's shape) whose early checks predict a crossing far past d_max must
+    still be checked every <= 50 steps and reach its true crossing — without the bound the
+    search jumped from d = 270 straight to d_max."""
+    tol, d_max = 1e-6, 800
+    rho = lambda d: 0.1 * math.exp(-0.012 * d) if d < 600 else 0.1 * math.exp(-7.2) * math.exp(-0.09 * (d - 600))
+    first = next(d for d in range(1, d_max + 1) if rho(d) < tol)
+    fake = _FakeRun(rho, r=1)
+    res = alg1.solve(fake, tol, d_max, keep_Y=False)
+    assert res.converged and res.d_star == first
+    valid = sorted(d for d in fake.calls if d <= first)
+    gaps = [b - a for a, b in zip(valid, valid[1:])]
+    assert max(gaps) <= 50, gaps
+
+
 def test_c0_regression_expectation():
     """Not a pin (parity unpinned for d* on the BJ configs): c0 converges near the
     survey-time expectation d* = 107 with a true residual of the same order."""
