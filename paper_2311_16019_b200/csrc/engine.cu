@@ -669,7 +669,7 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cud
     // band window of Z_d staged in shared memory (no AoS copy, gathers from shared memory)
     if (q.sell_cv) {
       SYLV_DISPATCH_R124_K(R, K, {
-        k_pass1_sell_win<R_, K_><<<q.csr_grid, kCsrWinThreads, q.csr_smem, st>>>(
+        k_pass1_sell_win<R_, K_><<<q.csr_grid, kSellThreads, q.csr_smem, st>>>(
             q.op, win, nwin, q.ld, q.gz, q.band, q.csrT, q.sell_ptr, q.sell_ci, q.sell_cv, q.Yt, q.part1);
       });
     } else {
@@ -903,10 +903,18 @@ void setup_csr_window(sylv_ctx* c, Sequence& q) {
   int dev = 0, max_optin = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const int64_t rows_fit = ((int64_t)max_optin - (int64_t)kCsrWinWarps * K * R * R * 8 - 256) / (8 * R);
+  const int64_t rows_fit =
+      ((int64_t)max_optin - (int64_t)std::max(kCsrWinWarps, kSellWarps) * K * R * R * 8 - 256) / (8 * R);
   int64_t T = (rows_fit - 2 * band - 2) / 512 * 512;
   if (T < 1024) return;
   T = std::min<int64_t>(T, (c->n + 511) / 512 * 512);
+  {
+    // balance the persistent CTAs: the same number of tiles per CTA (c4: 683 tiles of 6144 rows
+    // on 148 CTAs = 5 or 4 per CTA -> 737 tiles of 5696 rows, 5 per CTA), tiles of 32-row slices
+    const int64_t per_cta = (((c->n + T - 1) / T) + c->sm - 1) / c->sm;
+    const int64_t Tb = ((c->n + per_cta * c->sm - 1) / (per_cta * c->sm) + 31) / 32 * 32;
+    if (Tb >= 1024 && Tb <= T) T = Tb;
+  }
   q.csrT = T;
   q.csr_smem = (size_t)R * (T + 2 * band + 2) * 8 + 16;
   q.csr_grid = (int)std::min<int64_t>(c->sm, (c->n + T - 1) / T);

@@ -940,8 +940,19 @@ __global__ void k_sell_fill(const int64_t* __restrict__ rp, const int32_t* __res
 
 // Windowed pass 1 on the SELL-32 copy: CTA = tiles of T rows (T multiple of 32), band window of
 // Z_d in shared memory (bulk copies, as k_pass1_csr_win), warp = slice, lane = row.
+// kSellNE slice entries (value + column index) in flight per lane (A/B: -DSYLV_SELL_NE=8,
+// -DSYLV_SELL_THREADS=512 — fewer warps with more registers each)
+#ifndef SYLV_SELL_THREADS
+#define SYLV_SELL_THREADS 1024
+#endif
+#ifndef SYLV_SELL_NE
+#define SYLV_SELL_NE 4
+#endif
+constexpr int kSellThreads = SYLV_SELL_THREADS;
+constexpr int kSellWarps = kSellThreads / 32;
+constexpr int kSellNE = SYLV_SELL_NE;
 template <int R, int K>
-__global__ void __launch_bounds__(kCsrWinThreads, 1)
+__global__ void __launch_bounds__(kSellThreads, 1)
     k_pass1_sell_win(OpParams op, Win win, int nwin, int64_t ld, int64_t gz, int64_t band, int64_t T,
                      const int64_t* __restrict__ sptr, const int32_t* __restrict__ sci,
                      const double* __restrict__ scv, double* __restrict__ Yt, double* __restrict__ partial) {
@@ -949,7 +960,7 @@ __global__ void __launch_bounds__(kCsrWinThreads, 1)
   const int64_t Wcap = T + 2 * band + 2;
   double* zw = reinterpret_cast<double*>(sell_smraw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(zw + (int64_t)R * Wcap);
-  __shared__ double red[kCsrWinWarps * K * R * R];
+  __shared__ double red[kSellWarps * K * R * R];
   double acc[K * R * R];
 #pragma unroll
   for (int e = 0; e < K * R * R; ++e) acc[e] = 0.0;
@@ -992,7 +1003,7 @@ __global__ void __launch_bounds__(kCsrWinThreads, 1)
       }
       phase ^= 1u;
     }
-    for (int64_t sl = i0 / 32 + warp; sl * 32 < i1; sl += kCsrWinWarps) {
+    for (int64_t sl = i0 / 32 + warp; sl * 32 < i1; sl += kSellWarps) {
       const int64_t row = sl * 32 + lane;
       const bool valid = row < i1;
       // window blocks' values of this row (independent of the slice stream)
@@ -1006,16 +1017,16 @@ __global__ void __launch_bounds__(kCsrWinThreads, 1)
 #pragma unroll
       for (int c = 0; c < R; ++c) y[c] = 0.0;
       int64_t p = b0 + lane;
-      for (; p + 3 * 32 < b1; p += 4 * 32) {       // 4 entries in flight
-        double v[4];
-        int32_t cl[4];
+      for (; p + (kSellNE - 1) * 32 < b1; p += kSellNE * 32) {   // kSellNE entries in flight
+        double v[kSellNE];
+        int32_t cl[kSellNE];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kSellNE; ++u) {
           v[u] = __ldg(scv + p + 32 * u);
           cl[u] = __ldg(sci + p + 32 * u);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kSellNE; ++u) {
           const int64_t off = cl[u] - w0;
 #pragma unroll
           for (int c = 0; c < R; ++c) y[c] = fma(v[u], zw[c * Wcap + off], y[c]);
@@ -1057,7 +1068,7 @@ __global__ void __launch_bounds__(kCsrWinThreads, 1)
   __syncthreads();
   for (int e = threadIdx.x; e < K * R * R; e += blockDim.x) {
     double s = 0.0;
-    for (int w = 0; w < kCsrWinWarps; ++w) s += red[w * K * R * R + e];
+    for (int w = 0; w < kSellWarps; ++w) s += red[w * K * R * R + e];
     partial[(int64_t)blockIdx.x * K * R * R + e] = s;
   }
 }

@@ -160,9 +160,8 @@ struct GpuSylv {
   cuDoubleComplex *VA = nullptr, *VB = nullptr, *VAi = nullptr, *VBi = nullptr, *G1 = nullptr, *G2 = nullptr;
   cuDoubleComplex *wA = nullptr, *wB = nullptr;
   int* pairs = nullptr;                  // 2 m packing flags (A then B)
-  void* gbuf = nullptr;                  // Xgeev device workspace (lane 0; lane 1: gbuf2)
-  void* gbuf2 = nullptr;
-  std::vector<char> ghost, ghost2;       // Xgeev host workspaces
+  void* gbuf = nullptr;                  // Xgeev / zgetrf device workspace
+  std::vector<char> ghost;               // Xgeev host workspace
   size_t gws = 0;
   cusolverDnParams_t gparams = nullptr;
   int ecap = 0;
@@ -176,10 +175,9 @@ struct GpuSylv {
       if (p) cudaFree(p);
     if (pairs) cudaFree(pairs);
     if (gbuf) cudaFree(gbuf);
-    if (gbuf2) cudaFree(gbuf2);
     VA = VB = VAi = VBi = G1 = G2 = wA = wB = nullptr;
     pairs = nullptr;
-    gbuf = gbuf2 = nullptr;
+    gbuf = nullptr;
     gws = 0;
     ecap = 0;
   }
@@ -465,26 +463,22 @@ struct GpuSylv {
     cks(cusolverDnZgetrf_bufferSize(hs, cap, cap, G1, cap, &lw), "zgetrf_bufferSize");
     gws = 2 * std::max(wd, (size_t)lw * sizeof(cuDoubleComplex));   // margin: queries at m <= cap
     ck(cudaMalloc(&gbuf, gws + 16), "cudaMalloc (eig)");
-    ck(cudaMalloc(&gbuf2, gws + 16), "cudaMalloc (eig)");
     ghost.assign(wh + 16, 0);
-    ghost2.assign(wh + 16, 0);
     ecap = cap;
   }
 
   // eigenvalues w, complex right eigenvectors V and Vi = V^{-1} of the real m x m matrix X (X is
-  // copied) on solver lane 0 (hs, cur; LU, VR in Ai, LU of V in G1) or lane 1 (hs2, st2; LU2,
-  // VR in W, G2): the A and B halves run concurrently from two host threads.
-  void eig_inv(const double* X, int m, cuDoubleComplex* w, cuDoubleComplex* V, cuDoubleComplex* Vi, int* pair_dev,
-               int lane) {
-    cusolverDnHandle_t h = lane ? hs2 : hs;
-    cudaStream_t s = lane ? st2 : cur;
-    double* in = lane ? LU2 : LU;
-    double* vr = lane ? W : Ai;
-    void* gb = lane ? gbuf2 : gbuf;
-    std::vector<char>& gh = lane ? ghost2 : ghost;
-    int* inf_d = lane ? info2 : info;
-    int* piv = lane ? ipiv2 : ipiv;
-    cuDoubleComplex* lu = lane ? G2 : G1;
+  // copied; VR in Ai, the LU of V in G1) on the solve's stream
+  void eig_inv(const double* X, int m, cuDoubleComplex* w, cuDoubleComplex* V, cuDoubleComplex* Vi, int* pair_dev) {
+    cusolverDnHandle_t h = hs;
+    cudaStream_t s = cur;
+    double* in = LU;
+    double* vr = Ai;
+    void* gb = gbuf;
+    std::vector<char>& gh = ghost;
+    int* inf_d = info;
+    int* piv = ipiv;
+    cuDoubleComplex* lu = G1;
     ck(cudaMemcpyAsync(in, X, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy (geev)");
     size_t wd = 0, wh = 0;
     cks(cusolverDnXgeev_bufferSize(h, gparams, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, m, CUDA_R_64F,
@@ -566,8 +560,8 @@ struct GpuSylv {
     // A = M_U and B = M_V^T in turn on the context's stream: two concurrent Xgeev calls (two
     // handles, two host threads) failed intermittently with CUSOLVER_STATUS_INTERNAL_ERROR on
     // B200 (c1, m = 2000), so the halves are serial
-    eig_inv(A, m, wA, VA, VAi, pairs, 0);
-    eig_inv(B, m, wB, VB, VBi, pairs + m, 0);
+    eig_inv(A, m, wA, VA, VAi, pairs);
+    eig_inv(B, m, wB, VB, VBi, pairs + m);
     auto t1 = std::chrono::steady_clock::now();
     t_eig = std::chrono::duration<double>(t1 - t0).count();
     const double nA = fro(A, mm), nB = fro(B, mm), nF = fro(Bi, mm);

@@ -240,9 +240,7 @@ def test_device_projected_solve_matches_host(name, ds):
     gives the same sketched residual as the host Bartels-Stewart solve (1e-7 relative: the
     Newton sign iteration's forward error, several decades below the 1e-6 stopping
     tolerance), on the same device-built basis."""
-    cfg = inputs.small_config(**CASES[name])
-    csr = inputs.config_csr(cfg) if cfg.kind == "csr" else None
-    C1, C2 = inputs.make_rhs(cfg)
+    cfg, csr, C1, C2, orc, _ = _setup(name)
     st = torch.cuda.current_stream().cuda_stream
     g = _pkg().from_config(cfg, C1=torch.from_numpy(C1).cuda(), C2=torch.from_numpy(C2).cuda(), csr_pair=csr,
                            stream=st, proj="gpu")
@@ -252,9 +250,12 @@ def test_device_projected_solve_matches_host(name, ds):
     for d in ds:
         g.step(d - done)
         h.step(d - done)
+        orc.step(d - done)
         done = d
         rg, rh = g.residual(d)[1], h.residual(d)[1]
+        ro = orc.residual(d).rho_rel
         assert abs(rg - rh) <= 1e-7 * rh, (d, rg, rh)
+        assert abs(rg - ro) <= 1e-7 * ro, (d, rg, ro)      # and the oracle's
     s = g.stats()
     assert s["gpu_solves"] == len(ds) and s["gpu_solve_fallbacks"] == 0
     # the solution from the device-solved Y equals the host-solved one
