@@ -948,6 +948,8 @@ void setup_csr_window(sylv_ctx* c, Sequence& q) {
   CK(cudaStreamSynchronize(c->st));
 }
 
+void qtw_split(const sylv_ctx* c, int64_t rows, int m, bool mma, int R, int64_t* chunk, int* nrt);
+
 void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, bool transpose,
                    const double* C, uint64_t seed, const int8_t* sr_sign, const int64_t* sr_rows) {
   InitTrace tr;
@@ -1042,7 +1044,17 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
     CK(cudaEventCreateWithFlags(&q.ev_sk[i], cudaEventDisableTiming));
   }
   if (sketched || full) {
-    q.cpart = dalloc<double>((size_t)(full ? c->RTn : c->RT) * ldT * R);
+    size_t cpart_len = (size_t)(full ? c->RTn : c->RT) * ldT * R;
+    if (sketched) {   // Q^T w partials: nrt(m) x m x R (qtw_split, both sweep kernels)
+      for (int mm = R; mm <= ldT; mm += R)
+        for (int mma = 0; mma < 2; ++mma) {
+          int64_t ch = 0;
+          int nrt = 0;
+          qtw_split(c, q.sq, mm, mma != 0, R, &ch, &nrt);
+          cpart_len = std::max(cpart_len, (size_t)nrt * mm * R);
+        }
+    }
+    q.cpart = dalloc<double>(cpart_len);
     q.csum = dalloc<double>(ldT * R);
     q.c2 = dalloc<double>(ldT * R);
     q.qcpart = dalloc<double>(full ? (size_t)c->CCn * c->n * R : (size_t)c->CC * q.sq * R);
@@ -1144,6 +1156,26 @@ void init_sequence(sylv_ctx* c, Sequence& q, int which, const sylv_operator* A, 
 // QR update on `side`, which overlaps the next step's passes.
 void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st);
 
+// Row split of the Q^T w sweeps for m columns over `rows` rows.  DMMA (k_qtw_mma): one warp per
+// (32 columns, row chunk); FMA (k_qtw): a CTA per (64 columns, row tile <= qtw_tile<R>(), the w
+// tile it stages in shared memory), i.e. ~8 columns per warp.  A fixed tile left most of the GPU
+// idle at small m (c2, m <= 100: 13 CTAs, 40 us per sweep; c0 / c4: 1-2 CTAs), so the row chunks
+// (multiples of 32 rows, >= 128) are chosen for about 16 busy warps per SM; deterministic for a
+// given (rows, m).
+void qtw_split(const sylv_ctx* c, int64_t rows, int m, bool mma, int R, int64_t* chunk, int* nrt) {
+  const int64_t wn = mma ? (m + 31) / 32 : (m + 7) / 8;
+  const int64_t target = (int64_t)c->sm * 16;
+  const int64_t rt = std::max<int64_t>(1, std::min<int64_t>((rows + 127) / 128, (target + wn - 1) / wn));
+  int64_t ch = ((rows + rt - 1) / rt + 31) / 32 * 32;
+  if (!mma) {
+    int64_t cap = 0;
+    SYLV_DISPATCH_R(R, { cap = qtw_tile<R_>(); });
+    ch = std::min(ch, cap);
+  }
+  *chunk = ch;
+  *nrt = (int)((rows + ch - 1) / ch);
+}
+
 void step_passes(sylv_ctx* c, Sequence& q, int j, cudaStream_t st, bool sketch_on_side) {
   const int R = c->R, K = c->K;
   const int nwin = std::min(K, j);
@@ -1233,8 +1265,11 @@ void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
   const int chan = q.which == 0 ? kChanUSide : kChanVSide;
   // tensor-core sweeps (k_qtw_mma / k_qc_mma) for R >= 4 with 16-byte aligned columns
   const bool mma = R >= 4 && rows % 4 == 0 && c->qmma;
+  int64_t qchunk = c->tileQ;
+  int nrt = c->RT;
+  qtw_split(c, rows, m, mma, R, &qchunk, &nrt);
   const dim3 gq(mma ? (unsigned)(((m + 31) / 32 + kWarps - 1) / kWarps) : (unsigned)((m + kQtwCols - 1) / kQtwCols),
-                c->RT);
+                nrt);
   int cols_per_chunk = (m + c->CC - 1) / c->CC;
   if (mma) cols_per_chunk = (cols_per_chunk + 15) / 16 * 16;
   const int ncc = (m + cols_per_chunk - 1) / cols_per_chunk;
@@ -1246,11 +1281,11 @@ void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
     auto qtw = [&]() {
       if constexpr (R_ >= 4) {
         if (mma) {
-          k_qtw_mma<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, c->tileQ, q.cpart);
+          k_qtw_mma<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, qchunk, q.cpart);
           return;
         }
       }
-      k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, c->tileQ, 1, q.cpart);
+      k_qtw<R_><<<gq, kThreads, 0, st>>>(q.Q, rows, rows, m, q.w, qchunk, 1, q.cpart);
     };
     auto qc = [&](const double* cv) {
       if constexpr (R_ >= 4) {
@@ -1261,9 +1296,16 @@ void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
       }
       k_qc_part<R_><<<gc, kThreads, 0, st>>>(q.Q, rows, rows, m, cv, cols_per_chunk, q.qcpart);
     };
+    // sum of the nrt row-chunk partials: many parts of a short vector -> the part-parallel kernel
+    auto red_parts = [&](const double* part, int np, int64_t len, double* out, double* acc) {
+      if (np >= 32 && len <= (int64_t)np * 256)
+        k_red_parts_wide<<<(unsigned)((len + 31) / 32), 32 * std::min(32, (np + 3) / 4), 0, st>>>(part, np, len, out, acc);
+      else
+        k_red_parts<<<gr, 256, 0, st>>>(part, np, len, out, acc);
+    };
     // pass A: c1 = Q^T w (sharded: local rows, then the m R coefficients summed over the ranks)
     qtw();
-    k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.csum, nullptr);
+    red_parts(q.cpart, nrt, mR, q.csum, nullptr);
     if (shard) c->comm->allreduce(q.csum, (size_t)mR, st, chan);
     // w -= Q c1
     qc(q.csum);
@@ -1271,11 +1313,11 @@ void qr_update(sylv_ctx* c, Sequence& q, int j, cudaStream_t st) {
     // pass B: c2 = Q^T w, csum += c2
     qtw();
     if (shard) {
-      k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.c2, nullptr);
+      red_parts(q.cpart, nrt, mR, q.c2, nullptr);
       c->comm->allreduce(q.c2, (size_t)mR, st, chan);
       k_axpy_inplace<<<gr, 256, 0, st>>>(q.c2, q.csum, mR);
     } else {
-      k_red_parts<<<gr, 256, 0, st>>>(q.cpart, c->RT, mR, q.c2, q.csum);
+      red_parts(q.cpart, nrt, mR, q.c2, q.csum);
     }
     qc(q.c2);
     k_wsub<<<gw, 256, 0, st>>>(q.w, q.qcpart, ncc, rows * R);
@@ -1884,7 +1926,12 @@ sylv_status sylv_sketch_init(const sylv_operator* A, const sylv_operator* B, con
     CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
     const int per_sm = std::max(1, (int)(smem_sm / (c->sk_smem + 1024)));
     const int64_t ngroups = (c->n + 31) / 32;
-    c->nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(ngroups, (int64_t)c->sm * per_sm / r));
+    // a chunk also costs 2 s shared-memory ops (zero, write out) and s partial reads in the
+    // reduction: give every chunk at least ~s scatter updates (32 zeta per group), so small n
+    // does not end in one-group chunks (c0: 128 chunks of 1 group, a 25 us reduction)
+    const int64_t min_gpc = std::max<int64_t>(1, c->s / (32 * std::max(1, c->zeta)));
+    c->nchunk = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + min_gpc - 1) / min_gpc,
+                                                            (int64_t)c->sm * per_sm / r));
     c->gpc = (ngroups + c->nchunk - 1) / c->nchunk;
     c->nchunk = (int)((ngroups + c->gpc - 1) / c->gpc);
     {

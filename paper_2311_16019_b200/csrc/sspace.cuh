@@ -334,6 +334,30 @@ __global__ void k_red_parts(const double* __restrict__ partial, int nparts, int6
   }
 }
 
+// The same sum for many parts (the row-split Q^T w sweeps at small m: ~200 parts of a few
+// hundred elements): a CTA takes 32 consecutive elements (lane = element, coalesced) and
+// blockDim / 32 part chunks (warp c sums parts c, c + nc, ... in order), then the chunk sums
+// in chunk order — a fixed order, deterministic.  blockDim = 32 * nc, nc <= 32.
+__global__ void k_red_parts_wide(const double* __restrict__ partial, int nparts, int64_t len,
+                                 double* __restrict__ out, double* __restrict__ acc_out) {
+  __shared__ double sm[32][33];
+  const int lane = threadIdx.x & 31, ci = threadIdx.x >> 5, nc = blockDim.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (e < len) {
+#pragma unroll 8
+    for (int p = ci; p < nparts; p += nc) s += __ldg(partial + (int64_t)p * len + e);
+  }
+  sm[ci][lane] = s;
+  __syncthreads();
+  if (ci == 0 && e < len) {
+    double v = 0.0;
+    for (int c = 0; c < nc; ++c) v += sm[c][lane];
+    out[e] = v;
+    if (acc_out) acc_out[e] += v;
+  }
+}
+
 // acc[e] += x[e]  (sharded sketch space: csum += the rank-summed c2)
 __global__ void k_axpy_inplace(const double* __restrict__ x, double* __restrict__ acc, int64_t len) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x)
