@@ -158,6 +158,8 @@ struct Sequence {
   size_t csr_smem = 0;
   int64_t* sell_ptr = nullptr;            // SELL-32 copy of the operator (k_pass1_sell_win)
   int32_t* sell_ci = nullptr;
+  int16_t* sell_off = nullptr;            // 16-bit band offsets (k_pass1_sell_ring)
+  int ringT = 0, ringCap = 0;             // sliding-ring pass 1: tile rows, ring rows per column
   double* sell_cv = nullptr;
   int64_t gz = 0;                         // ghost rows before/after a column (N^2 3-D, N 2-D, 0 CSR)
   OpParams op{};
@@ -441,6 +443,7 @@ void free_seq(Sequence& q) {
   dfree(q.sr_V);
   dfree(q.sell_ptr);
   dfree(q.sell_ci);
+  dfree(q.sell_off);
   dfree(q.sell_cv);
   for (double* p : dp) dfree(p);
   dfree(q.flags);
@@ -667,7 +670,12 @@ void launch_pass1(sylv_ctx* c, Sequence& q, const Win& win, int nwin, int j, cud
 #undef SYLV_ST3D_P1
   } else if (q.op.kind == kCSR && q.csrT > 0) {
     // band window of Z_d staged in shared memory (no AoS copy, gathers from shared memory)
-    if (q.sell_cv) {
+    if (q.sell_off) {
+      SYLV_DISPATCH_R124_K(R, K, {
+        k_pass1_sell_ring<R_, K_><<<q.csr_grid, kSellThreads, q.csr_smem, st>>>(
+            q.op, win, nwin, q.ld, q.gz, q.band, q.ringT, q.ringCap, q.sell_ptr, q.sell_off, q.sell_cv, q.Yt, q.part1);
+      });
+    } else if (q.sell_cv) {
       SYLV_DISPATCH_R124_K(R, K, {
         k_pass1_sell_win<R_, K_><<<q.csr_grid, kSellThreads, q.csr_smem, st>>>(
             q.op, win, nwin, q.ld, q.gz, q.band, q.csrT, q.sell_ptr, q.sell_ci, q.sell_cv, q.Yt, q.part1);
@@ -760,8 +768,14 @@ void launch_sketch(sylv_ctx* c, Sequence& q, const double* X, int R, const doubl
     SYLV_DISPATCH_R(R, {
       k_sketch_pull<R_><<<(nw + kPullWarps - 1) / kPullWarps, kPullWarps * 32, 0, st>>>(
           c->n, X, q.ld, q.sp, q.pl_list, q.pl_off, q.pl_wpb, q.pl_bpw, q.pl_strips);
-      k_sketch_pull_fold_apply<R_><<<(int)std::min<int64_t>(8 * c->sm, (q.s + 256 / R_ - 1) / (256 / R_)), 256, 0, st>>>(
-          q.pl_strips, q.sp, q.pl_wpb, q.pl_bpw, q.pl_kmax, M, w);
+      // small s (c4: 3200 x 2): 256-thread blocks leave 25 CTAs, latency-bound at 20 us -> 64-thread blocks
+      if ((int64_t)q.s * R_ < (int64_t)4 * 256 * c->sm) {
+        k_sketch_pull_fold_apply<R_, 64><<<(int)((q.s + 64 / R_ - 1) / (64 / R_)), 64, 0, st>>>(
+            q.pl_strips, q.sp, q.pl_wpb, q.pl_bpw, q.pl_kmax, M, w);
+      } else {
+        k_sketch_pull_fold_apply<R_><<<(int)std::min<int64_t>(8 * c->sm, (q.s + 256 / R_ - 1) / (256 / R_)), 256, 0, st>>>(
+            q.pl_strips, q.sp, q.pl_wpb, q.pl_bpw, q.pl_kmax, M, w);
+      }
     });
     count(c, 2);
     return;
@@ -939,10 +953,27 @@ void setup_csr_window(sylv_ctx* c, Sequence& q) {
   CK(cudaStreamSynchronize(c->st));
   dfree(w);
   dfree(tmp);
-  q.sell_ci = dalloc<int32_t>(std::max<int64_t>(1, total));
   q.sell_cv = dalloc<double>(std::max<int64_t>(1, total));
-  k_sell_fill<<<(int)std::min<int64_t>(4096, (ns * 32 + 255) / 256), 256, 0, c->st>>>(q.rp, q.ci, q.cv, c->n, q.sell_ptr,
-                                                                                     q.sell_ci, q.sell_cv);
+  // sliding ring (k_pass1_sell_ring) when two tiles of >= 1024 rows and the band fit in shared
+  // memory and the band offsets fit in 16 bits; SYLV_SELL_RING=0: the static-window kernel (A/B)
+  const char* re = std::getenv("SYLV_SELL_RING");
+  const int64_t cap = rows_fit & ~(int64_t)1;
+  const int64_t Tr = (cap - 2 * band - 2) / 2 / 1024 * 1024;
+  const int fill_grid = (int)std::min<int64_t>(4096, (ns * 32 + 255) / 256);
+  if (!(re && std::strcmp(re, "0") == 0) && Tr >= 1024 && band <= 32767) {
+    q.ringT = (int)Tr;
+    q.ringCap = (int)cap;
+    q.csr_smem = (size_t)R * cap * 8 + 32;
+    q.csr_grid = (int)std::min<int64_t>(c->sm, (ns + 31) / 32);
+    SYLV_DISPATCH_R124_K(R, K, {
+      CK(cudaFuncSetAttribute(k_pass1_sell_ring<R_, K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.csr_smem));
+    });
+    q.sell_off = dalloc<int16_t>(std::max<int64_t>(1, total));
+    k_sell_fill<int16_t><<<fill_grid, 256, 0, c->st>>>(q.rp, q.ci, q.cv, c->n, q.sell_ptr, q.sell_off, q.sell_cv);
+  } else {
+    q.sell_ci = dalloc<int32_t>(std::max<int64_t>(1, total));
+    k_sell_fill<int32_t><<<fill_grid, 256, 0, c->st>>>(q.rp, q.ci, q.cv, c->n, q.sell_ptr, q.sell_ci, q.sell_cv);
+  }
   count(c, 2);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->st));

@@ -921,18 +921,24 @@ __global__ void k_sell_widths(const int64_t* __restrict__ rp, int64_t n, int64_t
   }
 }
 
+// IdxT = int32_t: column indices; IdxT = int16_t: band offsets col - row (k_pass1_sell_ring; the
+// caller checks band <= 32767; padding = offset 0)
+template <typename IdxT>
 __global__ void k_sell_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ cv, int64_t n, const int64_t* __restrict__ sptr,
-                            int32_t* __restrict__ sci, double* __restrict__ scv) {
+                            IdxT* __restrict__ sci, double* __restrict__ scv) {
+  constexpr bool kOff = sizeof(IdxT) == 2;
   const int64_t ns = (n + 31) / 32;
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < ns * 32; row += (int64_t)gridDim.x * blockDim.x) {
     const int64_t sl = row / 32, l = row % 32;
     const int64_t w = (sptr[sl + 1] - sptr[sl]) / 32;
     const int64_t p0 = row < n ? rp[row] : 0, p1 = row < n ? rp[row + 1] : 0;
+    const int64_t self = min(row, n - 1);
     for (int64_t k = 0; k < w; ++k) {
       const int64_t p = p0 + k;
       const bool ok = p < p1;
-      sci[sptr[sl] + 32 * k + l] = ok ? ci[p] : (int32_t)min(row, n - 1);
+      const int64_t col = ok ? (int64_t)ci[p] : self;
+      sci[sptr[sl] + 32 * k + l] = (IdxT)(kOff ? col - self : col);
       scv[sptr[sl] + 32 * k + l] = ok ? cv[p] : 0.0;
     }
   }
@@ -1057,6 +1063,168 @@ __global__ void __launch_bounds__(kSellThreads, 1)
         }
       }
     }
+  }
+#pragma unroll
+  for (int e = 0; e < K * R * R; ++e) {
+    double s = acc[e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(SYLV_FULL_MASK, s, o);
+    if (lane == 0) red[warp * K * R * R + e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < K * R * R; e += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < kSellWarps; ++w) s += red[w * K * R * R + e];
+    partial[(int64_t)blockIdx.x * K * R * R + e] = s;
+  }
+}
+
+// Sliding-ring pass 1 on the SELL-32 copy (round 2, default when two tiles and the band fit):
+// a CTA owns a CONTIGUOUS range of slices, so the band window of Z_d slides: only the T new rows
+// of the next tile are loaded (the static-window kernel reloads T + 2 band rows per tile, 2.4x at
+// c4, and waits for them).  Z_d lives in a shared-memory ring of `cap` rows per column, row
+// u = i + gz at position u mod cap; 2 T + 2 band + 2 <= cap, so the rows of tile i + 1 arrive
+// (cp.async.bulk on full[(i+1)&1]) while tile i is streamed.  No CTA-wide barrier in the loop:
+// every warp arrives on done[i&1] after its slices of tile i; warp 0 waits for done(i-1) — all
+// warps are past the rows tile i + 1 overwrites — before it issues that load.  Warp w streams
+// slices s0 + w + 32 k in order; a tile is T/32 consecutive slices (T a multiple of 1024: the same
+// number of slices per warp and tile).  Column indices are 16-bit band offsets (col - row):
+// 10 instead of 12 bytes per stored entry.
+__device__ __forceinline__ void sell_mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+template <int R, int K>
+__global__ void __launch_bounds__(kSellThreads, 1)
+    k_pass1_sell_ring(OpParams op, Win win, int nwin, int64_t ld, int64_t gz, int64_t band, int T, int cap,
+                      const int64_t* __restrict__ sptr, const int16_t* __restrict__ soff,
+                      const double* __restrict__ scv, double* __restrict__ Yt, double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char sell_smraw[];
+  double* zw = reinterpret_cast<double*>(sell_smraw);                    // [R][cap]
+  uint64_t* full = reinterpret_cast<uint64_t*>(zw + (int64_t)R * cap);   // [2]
+  uint64_t* done = full + 2;                                             // [2]
+  __shared__ double red[kSellWarps * K * R * R];
+  double acc[K * R * R];
+#pragma unroll
+  for (int e = 0; e < K * R * R; ++e) acc[e] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(full + b)) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(done + b)),
+                   "r"(kSellWarps)
+                   : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* __restrict__ Zs = win.p[nwin - 1] - gz;   // row u = i + gz >= 0; Zs 16-byte aligned, ld even
+  const int64_t n = op.n;
+  const int64_t ns = (n + 31) / 32;
+  const int64_t s0 = ns * blockIdx.x / gridDim.x, s1 = ns * (blockIdx.x + 1) / gridDim.x;
+  const int Ts = T / 32;
+  const int nt = (int)((s1 - s0 + Ts - 1) / Ts);
+  const int64_t utop = n + 2 * gz;
+  // window of tile i in u coordinates: [ulo(i), uhi(i)), even bounds
+  auto ulo = [&](int i) -> int64_t { return max((int64_t)0, (s0 + (int64_t)i * Ts) * 32 + gz - band) & ~(int64_t)1; };
+  auto uhi = [&](int i) -> int64_t {
+    const int64_t h = min(utop, min(s1, s0 + (int64_t)(i + 1) * Ts) * 32 + gz + band);
+    return h + (h & 1);
+  };
+  // rows [a, b) of every column into the ring, completing on bar (thread 0)
+  auto load = [&](int64_t a, int64_t b, uint64_t* bar) {
+    const uint32_t tx = (uint32_t)((b - a) * 8 * R);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+                 "r"(tx)
+                 : "memory");
+    int64_t u = a;
+    while (u < b) {
+      const int64_t pos = u % cap;
+      const int64_t len = min(min(b - u, (int64_t)cap - pos), (int64_t)4096);   // <= 32 KB per copy
+      for (int c = 0; c < R; ++c)
+        bulk_g2s(zw + (int64_t)c * cap + pos, Zs + (int64_t)c * ld + u, (uint32_t)(len * 8), bar);
+      u += len;
+    }
+  };
+  if (nt > 0 && threadIdx.x == 0) load(ulo(0), uhi(0), full);
+  for (int i = 0; i < nt; ++i) {
+    if (warp == 0 && i + 1 < nt) {
+      if (i >= 1) sell_mbar_wait(done + ((i - 1) & 1), (uint32_t)(((i - 1) >> 1) & 1));
+      if (lane == 0) load(uhi(i), uhi(i + 1), full + ((i + 1) & 1));
+      __syncwarp();
+    }
+    sell_mbar_wait(full + (i & 1), (uint32_t)((i >> 1) & 1));
+    const int64_t lo = ulo(i);
+    const int plo = (int)(lo % cap);
+    const int64_t sle = min(s1, s0 + (int64_t)(i + 1) * Ts);
+    for (int64_t sl = s0 + (int64_t)i * Ts + warp; sl < sle; sl += kSellWarps) {
+      const int64_t row = sl * 32 + lane;
+      const bool valid = row < n;
+      double zo[K > 1 ? K - 1 : 1][R];
+#pragma unroll
+      for (int i2 = 0; i2 < K - 1; ++i2)
+#pragma unroll
+        for (int a = 0; a < R; ++a) zo[i2][a] = (valid && i2 < nwin - 1) ? __ldg(win.p[i2] + a * ld + row) : 0.0;
+      const int64_t b0 = __ldg(sptr + sl), b1 = __ldg(sptr + sl + 1);
+      // ring position of this lane's own row (padding rows of the last slice: row n - 1)
+      const int rb = plo + (int)(min(row, n - 1) + gz - lo);
+      double y[R];
+#pragma unroll
+      for (int c = 0; c < R; ++c) y[c] = 0.0;
+      int64_t p = b0 + lane;
+      for (; p + (kSellNE - 1) * 32 < b1; p += kSellNE * 32) {   // kSellNE entries in flight
+        double v[kSellNE];
+        int cl[kSellNE];
+#pragma unroll
+        for (int u = 0; u < kSellNE; ++u) {
+          v[u] = __ldg(scv + p + 32 * u);
+          cl[u] = (int)__ldg(soff + p + 32 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < kSellNE; ++u) {
+          int off = rb + cl[u];
+          off -= off >= cap ? cap : 0;
+#pragma unroll
+          for (int c = 0; c < R; ++c) y[c] = fma(v[u], zw[c * cap + off], y[c]);
+        }
+      }
+      for (; p < b1; p += 32) {
+        const double v = __ldg(scv + p);
+        int off = rb + (int)__ldg(soff + p);
+        off -= off >= cap ? cap : 0;
+#pragma unroll
+        for (int c = 0; c < R; ++c) y[c] = fma(v, zw[c * cap + off], y[c]);
+      }
+      if (valid) {
+        if (Yt) {
+#pragma unroll
+          for (int c = 0; c < R; ++c) Yt[c * ld + row] = y[c];
+        }
+        const int own = rb - (rb >= cap ? cap : 0);
+#pragma unroll
+        for (int i2 = 0; i2 < K; ++i2) {
+          if (i2 < nwin) {
+            double z[R];
+#pragma unroll
+            for (int a = 0; a < R; ++a) z[a] = (i2 == nwin - 1) ? zw[a * cap + own] : zo[i2 < K - 1 ? i2 : 0][a];
+#pragma unroll
+            for (int a = 0; a < R; ++a)
+#pragma unroll
+              for (int c = 0; c < R; ++c) acc[(i2 * R + a) * R + c] = fma(z[a], y[c], acc[(i2 * R + a) * R + c]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(done + (i & 1))) : "memory");
   }
 #pragma unroll
   for (int e = 0; e < K * R * R; ++e) {

@@ -192,14 +192,14 @@ __global__ void __launch_bounds__(kPullWarps * 32, pull_min_blocks<R>()) k_sketc
 // of the warps whose bases q0 .. q0+bpw-1 reach it (slots q0 .. q0+bpw+30 mod b; zero past the
 // warp's own bases + 30), summed nearest first — a fixed order.  Needs b >= bpw + 31 so a
 // strip never covers a slot twice (b >= 64 is required at init).
-template <int R>
-__global__ void __launch_bounds__(256) k_sketch_pull_fold_apply(const double* __restrict__ strips, SketchParams sp,
+template <int R, int TPB = 256>
+__global__ void __launch_bounds__(TPB) k_sketch_pull_fold_apply(const double* __restrict__ strips, SketchParams sp,
                                                                 uint32_t wpb, uint32_t bpw, uint32_t kmax,
                                                                 const double* __restrict__ M, double* __restrict__ w) {
   // one thread per (slot, column): the strip sums; then one per (slot, output column): x M.
   // kmax bounds the candidate warps (their distance grows with k; the predicated loop keeps
   // every candidate's load in flight, and adds them nearest first like the break-loop did)
-  constexpr int SPB = 256 / R;                         // slots per block
+  constexpr int SPB = TPB / R;                         // slots per block (TPB = 64 for small s: more CTAs)
   __shared__ double vs[SPB][R];
   const uint32_t b = sp.b;
   const int64_t s = (int64_t)b * sp.zeta;

@@ -112,6 +112,26 @@ def test_window_blocks(name):
             assert _rel(Ug, seq.U[j]) <= 1e-9, (which, j)
 
 
+def test_csr_ring_multi_tile():
+    """Sliding-ring SELL pass 1 (k_pass1_sell_ring) with several tiles per CTA and a ragged last
+    one: band 6000 at r = 2 gives tiles of 1024 rows; 450011 rows = 3 tiles for each of the 148
+    CTAs.  Window blocks and per-step rho against the oracle."""
+    CASES["csr-ring"] = dict(kind="csr", n=450011, nnz_off=12, band=6000, r=2, k=2, d_max=30)
+    try:
+        cfg, csr, C1, C2, orc, gpu = _setup("csr-ring", keep_basis=True)
+    finally:
+        del CASES["csr-ring"]
+    for d in range(1, 7):
+        gpu.step(1)
+        orc.step(1)
+        _, rr = gpu.residual(d)
+        ro = orc.residual(d).rho_rel
+        assert _rho_close(rr, ro), (d, rr, ro)
+    for which, seq in ((0, orc.U), (1, orc.V)):
+        for j in range(6 + 2 - cfg.k, 6 + 2):
+            assert _rel(gpu.get_block(which, j), seq.U[j]) <= 1e-9, (which, j)
+
+
 @pytest.mark.parametrize("name", ["2d-r1", "csr-r2", "3d-r8k3", "3d-r8k3-tma"])
 def test_solution_and_true_residual(name):
     cfg, csr, C1, C2, orc, gpu = _setup(name)
