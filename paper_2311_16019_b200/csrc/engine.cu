@@ -768,9 +768,8 @@ void launch_sketch(sylv_ctx* c, Sequence& q, const double* X, int R, const doubl
     SYLV_DISPATCH_R(R, {
       k_sketch_pull<R_><<<(nw + kPullWarps - 1) / kPullWarps, kPullWarps * 32, 0, st>>>(
           c->n, X, q.ld, q.sp, q.pl_list, q.pl_off, q.pl_wpb, q.pl_bpw, q.pl_strips);
-      // small s (c4: 3200 x 2): 256-thread blocks leave 25 CTAs, latency-bound at 20 us -> 64-thread blocks
-      if ((int64_t)q.s * R_ < (int64_t)4 * 256 * c->sm) {
-        k_sketch_pull_fold_apply<R_, 64><<<(int)((q.s + 64 / R_ - 1) / (64 / R_)), 64, 0, st>>>(
+      if (q.pl_kmax > 8) {   // many strips per slot (one or two bases per warp): warp per slot, lane = strip
+        k_sketch_pull_fold_wide<R_><<<(int)std::min<int64_t>(16 * c->sm, (q.s + 3) / 4), 128, 0, st>>>(
             q.pl_strips, q.sp, q.pl_wpb, q.pl_bpw, q.pl_kmax, M, w);
       } else {
         k_sketch_pull_fold_apply<R_><<<(int)std::min<int64_t>(8 * c->sm, (q.s + 256 / R_ - 1) / (256 / R_)), 256, 0, st>>>(

@@ -192,14 +192,14 @@ __global__ void __launch_bounds__(kPullWarps * 32, pull_min_blocks<R>()) k_sketc
 // of the warps whose bases q0 .. q0+bpw-1 reach it (slots q0 .. q0+bpw+30 mod b; zero past the
 // warp's own bases + 30), summed nearest first — a fixed order.  Needs b >= bpw + 31 so a
 // strip never covers a slot twice (b >= 64 is required at init).
-template <int R, int TPB = 256>
-__global__ void __launch_bounds__(TPB) k_sketch_pull_fold_apply(const double* __restrict__ strips, SketchParams sp,
+template <int R>
+__global__ void __launch_bounds__(256) k_sketch_pull_fold_apply(const double* __restrict__ strips, SketchParams sp,
                                                                 uint32_t wpb, uint32_t bpw, uint32_t kmax,
                                                                 const double* __restrict__ M, double* __restrict__ w) {
   // one thread per (slot, column): the strip sums; then one per (slot, output column): x M.
   // kmax bounds the candidate warps (their distance grows with k; the predicated loop keeps
   // every candidate's load in flight, and adds them nearest first like the break-loop did)
-  constexpr int SPB = TPB / R;                         // slots per block (TPB = 64 for small s: more CTAs)
+  constexpr int SPB = 256 / R;                         // slots per block
   __shared__ double vs[SPB][R];
   const uint32_t b = sp.b;
   const int64_t s = (int64_t)b * sp.zeta;
@@ -231,6 +231,53 @@ __global__ void __launch_bounds__(TPB) k_sketch_pull_fold_apply(const double* __
       w[q * R + c] = o;
     }
     __syncthreads();
+  }
+}
+
+// The same fold for many candidate strips per slot (bpw small: c4 has one base per warp, so ~33
+// warps' strips cover a slot and the per-thread candidate loop above — a 64-bit division per
+// candidate — ran 20 us on 25 CTAs): one warp per slot, lane = candidate (k = lane, lane + 32),
+// xor-butterfly sum (a fixed order: deterministic), lanes c < R apply the r x r factor.
+template <int R>
+__global__ void __launch_bounds__(128) k_sketch_pull_fold_wide(const double* __restrict__ strips, SketchParams sp,
+                                                               uint32_t wpb, uint32_t bpw, uint32_t kmax,
+                                                               const double* __restrict__ M, double* __restrict__ w) {
+  const uint32_t b = sp.b;
+  const int64_t s = (int64_t)b * sp.zeta;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < s; q += nw) {
+    const uint32_t t = (uint32_t)(q / b), p = (uint32_t)(q - (int64_t)t * b);
+    const uint32_t wl = pull_owner(p, b, wpb);
+    double va[R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) va[a] = 0.0;
+    for (uint32_t k = (uint32_t)lane; k < kmax; k += 32u) {
+      const uint32_t wq = (wl + wpb - k % wpb) % wpb;
+      const uint32_t dd = (p + b - pull_q0(wq, b, wpb)) % b;
+      if (dd < bpw + 31u) {
+        const double* sp0 = strips + ((size_t)(t * wpb + wq) * R) * kPullS + dd;
+#pragma unroll
+        for (int a = 0; a < R; ++a) va[a] += sp0[(size_t)a * kPullS];
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) va[a] += __shfl_xor_sync(0xffffffffu, va[a], o);
+      va[a] *= sp.scale;
+    }
+    if (lane < R) {
+      double o = 0.0;
+      if (M) {
+#pragma unroll
+        for (int e = 0; e < R; ++e) o = fma(va[e], __ldg(M + e * R + lane), o);
+      } else {
+#pragma unroll
+        for (int e = 0; e < R; ++e) o = (e == lane) ? va[e] : o;
+      }
+      w[q * R + lane] = o;
+    }
   }
 }
 
